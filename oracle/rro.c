@@ -1,0 +1,827 @@
+/*
+ * rro.c — FP64 CPU ORACLE (test infrastructure only; never the product).
+ *
+ * Plain-C restatement of the reference path (see rro.h).  Operation order
+ * follows the reference expression by expression; compile with
+ * -ffp-contract=off (oracle/Makefile), as the reference is
+ * (proj/CMakeLists.txt:12-13).  Reference paths below are relative to
+ * /root/reference/proj.
+ */
+#include "rro.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
+#include <stdio.h>
+#include <string.h>
+
+static _Thread_local char g_err[256];
+const char* rro_last_error(void) { return g_err; }
+
+
+/* ---- tiny parallel-for over [0, n) (dynamic chunks, pthreads) ------------ */
+typedef void (*rro_body)(void* arg, long lo, long hi);
+typedef struct { rro_body body; void* arg; long n, chunk; atomic_long next; } PFor;
+
+static void* pfor_worker(void* p) {
+    PFor* f = (PFor*)p;
+    for (;;) {
+        const long lo = atomic_fetch_add(&f->next, f->chunk);
+        if (lo >= f->n) break;
+        const long hi = lo + f->chunk < f->n ? lo + f->chunk : f->n;
+        f->body(f->arg, lo, hi);
+    }
+    return NULL;
+}
+
+static void parallel_for(long n, long chunk, int threads, rro_body body, void* arg) {
+    PFor f;
+    f.body = body;
+    f.arg = arg;
+    f.n = n;
+    f.chunk = chunk > 0 ? chunk : 1;
+    atomic_init(&f.next, 0);
+    if (threads > 64) threads = 64;
+    if (threads <= 1 || n <= f.chunk) {
+        pfor_worker(&f);
+        return;
+    }
+    pthread_t tids[64];
+    int started = 0;
+    for (int i = 0; i < threads - 1; ++i)
+        if (pthread_create(&tids[started], NULL, pfor_worker, &f) == 0) ++started;
+    pfor_worker(&f);
+    for (int i = 0; i < started; ++i) pthread_join(tids[i], NULL);
+}
+
+/* ---- core algebra (include/rray/core/linalg.hpp) ------------------------- */
+typedef struct { double x, y, z; } V3;
+typedef struct { double xx, xy, xz, yy, yz, zz; } S3;     /* SymMat3T :85-95 */
+typedef struct { double m[3][3]; } M3;                    /* Mat3T :172-188 */
+typedef struct { S3 s[3]; } T3;                           /* Tensor3T :278-285 */
+
+static V3 v3(double x, double y, double z) { V3 r = {x, y, z}; return r; }
+static V3 vadd(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }     /* :28-31 */
+static V3 vsub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }     /* :33-36 */
+static V3 vneg(V3 a) { return v3(-a.x, -a.y, -a.z); }                         /* :38-41 */
+static V3 vscale(double s, V3 a) { return v3(s * a.x, s * a.y, s * a.z); }     /* :43-46 */
+static V3 vdiv(V3 a, double s) { return v3(a.x / s, a.y / s, a.z / s); }       /* :53-56 */
+static double vdot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }   /* :58-61 */
+static V3 vcross(V3 a, V3 b) {                                                 /* :73-75 */
+    return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+static double vcomp(V3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+static void vset(V3* v, int i, double x) { if (i == 0) v->x = x; else if (i == 1) v->y = x; else v->z = x; }
+static V3 vload(const double* p) { return v3(p[0], p[1], p[2]); }
+static V3 vfrom(rr_vec3 a) { return v3(a.x, a.y, a.z); }
+
+static S3 s3_zero(void) { S3 r = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}; return r; }
+static S3 s3_identity(void) { S3 r = {1.0, 0.0, 0.0, 1.0, 0.0, 1.0}; return r; }
+static S3 s3_add(S3 a, S3 b) {                                                 /* :99-102 */
+    S3 r = {a.xx + b.xx, a.xy + b.xy, a.xz + b.xz, a.yy + b.yy, a.yz + b.yz, a.zz + b.zz};
+    return r;
+}
+static S3 s3_scale(double s, S3 a) {                                           /* :109-112 */
+    S3 r = {s * a.xx, s * a.xy, s * a.xz, s * a.yy, s * a.yz, s * a.zz};
+    return r;
+}
+/* Bilinear form u^T m v with the reference's fixed accumulation order (:121-132). */
+static double quad_form(S3 m, V3 u, V3 v) {
+    double acc = m.xx * u.x * v.x;
+    acc = acc + m.xy * (u.x * v.y + u.y * v.x);
+    acc = acc + m.xz * (u.x * v.z + u.z * v.x);
+    acc = acc + m.yy * u.y * v.y;
+    acc = acc + m.yz * (u.y * v.z + u.z * v.y);
+    acc = acc + m.zz * u.z * v.z;
+    return acc;
+}
+static double s3_det(S3 m) {                                                   /* :139-144 */
+    return m.xx * (m.yy * m.zz - m.yz * m.yz) - m.xy * (m.xy * m.zz - m.yz * m.xz) +
+           m.xz * (m.xy * m.yz - m.yy * m.xz);
+}
+static S3 outer_sym(V3 v) {                                                    /* :147-150 */
+    S3 r = {v.x * v.x, v.x * v.y, v.x * v.z, v.y * v.y, v.y * v.z, v.z * v.z};
+    return r;
+}
+static M3 m3_identity(void) {
+    M3 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) r.m[i][j] = (i == j ? 1.0 : 0.0);
+    return r;
+}
+static V3 m3_mulv(const M3* a, V3 v) {                                         /* :200-205 */
+    return v3(a->m[0][0] * v.x + a->m[0][1] * v.y + a->m[0][2] * v.z,
+              a->m[1][0] * v.x + a->m[1][1] * v.y + a->m[1][2] * v.z,
+              a->m[2][0] * v.x + a->m[2][1] * v.y + a->m[2][2] * v.z);
+}
+static M3 m3_mul(const M3* a, const M3* b) {                                   /* :207-214 */
+    M3 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.m[i][j] = a->m[i][0] * b->m[0][j] + a->m[i][1] * b->m[1][j] + a->m[i][2] * b->m[2][j];
+    return r;
+}
+static double m3_det(const M3* a) {                                            /* :216-221 */
+    return a->m[0][0] * (a->m[1][1] * a->m[2][2] - a->m[1][2] * a->m[2][1]) -
+           a->m[0][1] * (a->m[1][0] * a->m[2][2] - a->m[1][2] * a->m[2][0]) +
+           a->m[0][2] * (a->m[1][0] * a->m[2][1] - a->m[1][1] * a->m[2][0]);
+}
+static M3 m3_inverse_unchecked(const M3* a, double d) {                        /* :223-236 */
+    M3 r;
+    r.m[0][0] = (a->m[1][1] * a->m[2][2] - a->m[1][2] * a->m[2][1]) / d;
+    r.m[0][1] = (a->m[0][2] * a->m[2][1] - a->m[0][1] * a->m[2][2]) / d;
+    r.m[0][2] = (a->m[0][1] * a->m[1][2] - a->m[0][2] * a->m[1][1]) / d;
+    r.m[1][0] = (a->m[1][2] * a->m[2][0] - a->m[1][0] * a->m[2][2]) / d;
+    r.m[1][1] = (a->m[0][0] * a->m[2][2] - a->m[0][2] * a->m[2][0]) / d;
+    r.m[1][2] = (a->m[0][2] * a->m[1][0] - a->m[0][0] * a->m[1][2]) / d;
+    r.m[2][0] = (a->m[1][0] * a->m[2][1] - a->m[1][1] * a->m[2][0]) / d;
+    r.m[2][1] = (a->m[0][1] * a->m[2][0] - a->m[0][0] * a->m[2][1]) / d;
+    r.m[2][2] = (a->m[0][0] * a->m[1][1] - a->m[0][1] * a->m[1][0]) / d;
+    return r;
+}
+static S3 gram(const M3* j) {                                                  /* :239-249 */
+    S3 r;
+    r.xx = j->m[0][0] * j->m[0][0] + j->m[1][0] * j->m[1][0] + j->m[2][0] * j->m[2][0];
+    r.xy = j->m[0][0] * j->m[0][1] + j->m[1][0] * j->m[1][1] + j->m[2][0] * j->m[2][1];
+    r.xz = j->m[0][0] * j->m[0][2] + j->m[1][0] * j->m[1][2] + j->m[2][0] * j->m[2][2];
+    r.yy = j->m[0][1] * j->m[0][1] + j->m[1][1] * j->m[1][1] + j->m[2][1] * j->m[2][1];
+    r.yz = j->m[0][1] * j->m[0][2] + j->m[1][1] * j->m[1][2] + j->m[2][1] * j->m[2][2];
+    r.zz = j->m[0][2] * j->m[0][2] + j->m[1][2] * j->m[1][2] + j->m[2][2] * j->m[2][2];
+    return r;
+}
+static S3 congruence(const M3* a, S3 s) {                                      /* :252-274 */
+    double t[3][3];
+    const double s00 = s.xx, s01 = s.xy, s02 = s.xz;
+    const double s11 = s.yy, s12 = s.yz, s22 = s.zz;
+    for (int j = 0; j < 3; ++j) {
+        t[0][j] = s00 * a->m[0][j] + s01 * a->m[1][j] + s02 * a->m[2][j];
+        t[1][j] = s01 * a->m[0][j] + s11 * a->m[1][j] + s12 * a->m[2][j];
+        t[2][j] = s02 * a->m[0][j] + s12 * a->m[1][j] + s22 * a->m[2][j];
+    }
+#define ENTRY(i, j) (a->m[0][i] * t[0][j] + a->m[1][i] * t[1][j] + a->m[2][i] * t[2][j])
+    S3 r = {ENTRY(0, 0), ENTRY(0, 1), ENTRY(0, 2), ENTRY(1, 1), ENTRY(1, 2), ENTRY(2, 2)};
+#undef ENTRY
+    return r;
+}
+static double dmin(double a, double b) { return a < b ? a : b; }  /* simd/pack.hpp:120 */
+
+static const double kSingularDetEps = 1e-14;                       /* linalg.hpp:165 */
+
+/* ---- scalar fields (include/rray/fields/scalar_field.hpp) ---------------- */
+typedef struct { double value; V3 gradient; S3 hessian; } ScalarSample;
+
+static double ipow(double x, int n) {                              /* :97-102 */
+    double r = 1.0;
+    for (int i = 0; i < n; ++i) r = r * x;
+    return r;
+}
+
+static ScalarSample eval_gaussian(const rr_gaussian* g, V3 p) {     /* :104-126 */
+    const double ux = (p.x - g->center.x) / g->sigma.x;
+    const double uy = (p.y - g->center.y) / g->sigma.y;
+    const double uz = (p.z - g->center.z) / g->sigma.z;
+    const double e = exp(-0.5 * (ux * ux + uy * uy + uz * uz));
+    const double val = g->amplitude * e;
+    ScalarSample r;
+    r.value = val;
+    r.gradient = v3(-(val * ux) / g->sigma.x, -(val * uy) / g->sigma.y, -(val * uz) / g->sigma.z);
+    r.hessian.xx = val * (ux * ux - 1.0) / (g->sigma.x * g->sigma.x);
+    r.hessian.yy = val * (uy * uy - 1.0) / (g->sigma.y * g->sigma.y);
+    r.hessian.zz = val * (uz * uz - 1.0) / (g->sigma.z * g->sigma.z);
+    r.hessian.xy = val * (ux * uy) / (g->sigma.x * g->sigma.y);
+    r.hessian.xz = val * (ux * uz) / (g->sigma.x * g->sigma.z);
+    r.hessian.yz = val * (uy * uz) / (g->sigma.y * g->sigma.z);
+    return r;
+}
+
+static ScalarSample eval_polynomial(const rr_poly_term* terms, int n, V3 p) { /* :128-161 */
+    ScalarSample out;
+    out.value = 0.0;
+    out.gradient = v3(0.0, 0.0, 0.0);
+    out.hessian = s3_zero();
+    for (int i = 0; i < n; ++i) {
+        const int a = terms[i].powers[0], b = terms[i].powers[1], c = terms[i].powers[2];
+        const double xa = ipow(p.x, a), yb = ipow(p.y, b), zc = ipow(p.z, c);
+        const double coef = terms[i].coef;
+        out.value = out.value + coef * xa * yb * zc;
+        const double xa1 = a > 0 ? ipow(p.x, a - 1) : 0.0;
+        const double yb1 = b > 0 ? ipow(p.y, b - 1) : 0.0;
+        const double zc1 = c > 0 ? ipow(p.z, c - 1) : 0.0;
+        if (a > 0) out.gradient.x = out.gradient.x + coef * (double)a * xa1 * yb * zc;
+        if (b > 0) out.gradient.y = out.gradient.y + coef * (double)b * xa * yb1 * zc;
+        if (c > 0) out.gradient.z = out.gradient.z + coef * (double)c * xa * yb * zc1;
+        if (a > 1)
+            out.hessian.xx = out.hessian.xx + coef * (double)(a * (a - 1)) * ipow(p.x, a - 2) * yb * zc;
+        if (b > 1)
+            out.hessian.yy = out.hessian.yy + coef * (double)(b * (b - 1)) * xa * ipow(p.y, b - 2) * zc;
+        if (c > 1)
+            out.hessian.zz = out.hessian.zz + coef * (double)(c * (c - 1)) * xa * yb * ipow(p.z, c - 2);
+        if (a > 0 && b > 0) out.hessian.xy = out.hessian.xy + coef * (double)(a * b) * xa1 * yb1 * zc;
+        if (a > 0 && c > 0) out.hessian.xz = out.hessian.xz + coef * (double)(a * c) * xa1 * yb * zc1;
+        if (b > 0 && c > 0) out.hessian.yz = out.hessian.yz + coef * (double)(b * c) * xa * yb1 * zc1;
+    }
+    return out;
+}
+
+static ScalarSample eval_scalar(const rr_metric_desc* m, int node, V3 p) {   /* :167-187 */
+    const rr_field_node* f = &m->field_nodes[node];
+    if (f->kind == RR_FIELD_GAUSSIAN) return eval_gaussian(&f->gaussian, p);
+    if (f->kind == RR_FIELD_POLYNOMIAL) return eval_polynomial(m->poly_terms + f->first, f->count, p);
+    ScalarSample acc;
+    acc.value = 0.0;
+    acc.gradient = v3(0.0, 0.0, 0.0);
+    acc.hessian = s3_zero();
+    for (int i = 0; i < f->count; ++i) {
+        const ScalarSample s = eval_scalar(m, m->children[f->first + i], p);
+        acc.value = acc.value + s.value;
+        acc.gradient = vadd(acc.gradient, s.gradient);
+        acc.hessian = s3_add(acc.hessian, s.hessian);
+    }
+    return acc;
+}
+
+/* ---- diffeomorphisms (include/rray/fields/diffeo.hpp) -------------------- */
+typedef struct { V3 image; M3 jacobian; T3 second; } DiffeoSample;
+typedef struct { DiffeoSample sample; double validity; } DiffeoEval;
+
+static T3 t3_zero(void) { T3 r; r.s[0] = r.s[1] = r.s[2] = s3_zero(); return r; }
+
+static DiffeoSample compose_samples(const DiffeoSample* outer, const DiffeoSample* inner) { /* :111-124 */
+    DiffeoSample r;
+    r.image = outer->image;
+    r.jacobian = m3_mul(&outer->jacobian, &inner->jacobian);
+    for (int s = 0; s < 3; ++s) {
+        S3 h = congruence(&inner->jacobian, outer->second.s[s]);
+        for (int t = 0; t < 3; ++t) h = s3_add(h, s3_scale(outer->jacobian.m[s][t], inner->second.s[t]));
+        r.second.s[s] = h;
+    }
+    return r;
+}
+
+static DiffeoEval eval_diffeo(const rr_metric_desc* m, int node, V3 p) {
+    const rr_diffeo_node* d = &m->diffeo_nodes[node];
+    DiffeoEval ev;
+    switch (d->kind) {
+        case RR_DIFFEO_IDENTITY:                                                /* :128-131 */
+            ev.sample.image = p;
+            ev.sample.jacobian = m3_identity();
+            ev.sample.second = t3_zero();
+            ev.validity = 1.0;
+            return ev;
+        case RR_DIFFEO_AFFINE: {                                                /* :133-141 */
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) ev.sample.jacobian.m[i][j] = d->matrix[i][j];
+            ev.sample.image = vadd(m3_mulv(&ev.sample.jacobian, p), vfrom(d->offset));
+            ev.sample.second = t3_zero();
+            ev.validity = fabs(m3_det(&ev.sample.jacobian));
+            return ev;
+        }
+        case RR_DIFFEO_TWIST: {                                                 /* :143-173 */
+            const double c = cos(p.z), s = sin(p.z);
+            DiffeoSample* o = &ev.sample;
+            o->image = v3(p.x * c - p.y * s, p.x * s + p.y * c, p.z);
+            o->jacobian.m[0][0] = c;
+            o->jacobian.m[0][1] = -s;
+            o->jacobian.m[0][2] = -(p.x * s) - p.y * c;
+            o->jacobian.m[1][0] = s;
+            o->jacobian.m[1][1] = c;
+            o->jacobian.m[1][2] = p.x * c - p.y * s;
+            o->jacobian.m[2][0] = 0.0;
+            o->jacobian.m[2][1] = 0.0;
+            o->jacobian.m[2][2] = 1.0;
+            o->second = t3_zero();
+            o->second.s[0].xz = -s;
+            o->second.s[0].yz = -c;
+            o->second.s[0].zz = -(p.x * c) + p.y * s;
+            o->second.s[1].xz = c;
+            o->second.s[1].yz = -s;
+            o->second.s[1].zz = -(p.x * s) - p.y * c;
+            ev.validity = fabs(m3_det(&o->jacobian));
+            return ev;
+        }
+        case RR_DIFFEO_LOCAL_BUMP: {                                            /* :175-193 */
+            const ScalarSample f = eval_gaussian(&d->bump, p);
+            const V3 v = vfrom(d->direction);
+            DiffeoSample* o = &ev.sample;
+            o->image = vadd(p, vscale(f.value, v));
+            o->jacobian = m3_identity();
+            const double g[3] = {f.gradient.x, f.gradient.y, f.gradient.z};
+            const double vv[3] = {v.x, v.y, v.z};
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) o->jacobian.m[i][j] = o->jacobian.m[i][j] + vv[i] * g[j];
+            for (int s = 0; s < 3; ++s) o->second.s[s] = s3_scale(vv[s], f.hessian);
+            ev.validity = fabs(m3_det(&o->jacobian));
+            return ev;
+        }
+        default: {                                                              /* :198-212 */
+            DiffeoEval cur = eval_diffeo(m, m->children[d->first + d->count - 1], p);
+            for (int i = d->count - 2; i >= 0; --i) {
+                const DiffeoEval outer = eval_diffeo(m, m->children[d->first + i], cur.sample.image);
+                const DiffeoSample composed = compose_samples(&outer.sample, &cur.sample);
+                double validity = dmin(cur.validity, outer.validity);
+                validity = dmin(validity, fabs(m3_det(&composed.jacobian)));
+                cur.sample = composed;
+                cur.validity = validity;
+            }
+            return cur;
+        }
+    }
+}
+
+/* ---- metrics (include/rray/metrics/metric.hpp) --------------------------- */
+typedef struct { T3 gamma; double validity; } ChristoffelEval;
+
+static ChristoffelEval christoffel_eval(const rr_metric_desc* m, V3 p) {
+    ChristoffelEval ce;
+    if (m->kind == RR_METRIC_EUCLIDEAN) {                                       /* :69-72 */
+        ce.gamma = t3_zero();
+        ce.validity = 1.0;
+    } else if (m->kind == RR_METRIC_GRAPH) {                                    /* :74-83 */
+        const ScalarSample s = eval_scalar(m, m->root, p);
+        const double w = 1.0 + vdot(s.gradient, s.gradient);
+        ce.gamma.s[0] = s3_scale(s.gradient.x / w, s.hessian);
+        ce.gamma.s[1] = s3_scale(s.gradient.y / w, s.hessian);
+        ce.gamma.s[2] = s3_scale(s.gradient.z / w, s.hessian);
+        ce.validity = 1.0;
+    } else {                                                                    /* :85-100 */
+        const DiffeoEval ev = eval_diffeo(m, m->root, p);
+        const double d = m3_det(&ev.sample.jacobian);
+        const M3 jinv = m3_inverse_unchecked(&ev.sample.jacobian, d);
+        for (int k = 0; k < 3; ++k) {
+            S3 acc = s3_scale(jinv.m[k][0], ev.sample.second.s[0]);
+            acc = s3_add(acc, s3_scale(jinv.m[k][1], ev.sample.second.s[1]));
+            acc = s3_add(acc, s3_scale(jinv.m[k][2], ev.sample.second.s[2]));
+            ce.gamma.s[k] = acc;
+        }
+        ce.validity = dmin(ev.validity, fabs(d));
+    }
+    return ce;
+}
+
+/* metric_tensor g at p (metric.cpp:58-73 via sample_metric); returns 0 ok,
+ * 2 when the diffeo metric is singular (eval_checked :29-36 / sym_inverse). */
+static int metric_tensor_checked(const rr_metric_desc* m, V3 p, S3* g) {
+    if (m->kind == RR_METRIC_EUCLIDEAN) {
+        *g = s3_identity();
+        return 0;
+    }
+    if (m->kind == RR_METRIC_GRAPH) {                                           /* metric.cpp:12-15 */
+        const ScalarSample s = eval_scalar(m, m->root, p);
+        *g = s3_add(s3_identity(), outer_sym(s.gradient));
+        return 0;
+    }
+    const DiffeoEval ev = eval_diffeo(m, m->root, p);                           /* metric.cpp:40-42 */
+    if (!(ev.validity > kSingularDetEps)) {
+        snprintf(g_err, sizeof g_err, "diffeo_metric: |det J| <= 1e-14");
+        return 2;
+    }
+    *g = gram(&ev.sample.jacobian);
+    if (fabs(s3_det(*g)) <= kSingularDetEps) {                                  /* linalg.cpp:6-12 */
+        snprintf(g_err, sizeof g_err, "sym_inverse: |det| <= 1e-14");
+        return 2;
+    }
+    return 0;
+}
+
+/* ---- geodesics (include/rray/geodesics/integrate.hpp) -------------------- */
+static V3 flow_accel(const rr_metric_desc* m, V3 pos, V3 vel, double* validity) { /* :46-53 */
+    const ChristoffelEval ce = christoffel_eval(m, pos);
+    *validity = dmin(*validity, ce.validity);
+    return vneg(v3(quad_form(ce.gamma.s[0], vel, vel), quad_form(ce.gamma.s[1], vel, vel),
+                   quad_form(ce.gamma.s[2], vel, vel)));
+}
+
+typedef struct { V3 position, velocity; } State;
+
+static State euler_step(const rr_metric_desc* m, State s, double h, double* validity) { /* :55-61 */
+    *validity = 1.0;
+    const V3 a = flow_accel(m, s.position, s.velocity, validity);
+    State r;
+    r.position = vadd(s.position, vscale(h, s.velocity));
+    r.velocity = vadd(s.velocity, vscale(h, a));
+    return r;
+}
+
+static State rk4_step(const rr_metric_desc* m, State s, double h, double* validity) { /* :63-93 */
+    *validity = 1.0;
+    const double hh = h, half = 0.5 * h, sixth = h / 6.0;
+    const V3 k1x = s.velocity;
+    const V3 k1v = flow_accel(m, s.position, s.velocity, validity);
+    const V3 p2 = vadd(s.position, vscale(half, k1x));
+    const V3 v2 = vadd(s.velocity, vscale(half, k1v));
+    const V3 k2x = v2;
+    const V3 k2v = flow_accel(m, p2, v2, validity);
+    const V3 p3 = vadd(s.position, vscale(half, k2x));
+    const V3 v3_ = vadd(s.velocity, vscale(half, k2v));
+    const V3 k3x = v3_;
+    const V3 k3v = flow_accel(m, p3, v3_, validity);
+    const V3 p4 = vadd(s.position, vscale(hh, k3x));
+    const V3 v4 = vadd(s.velocity, vscale(hh, k3v));
+    const V3 k4x = v4;
+    const V3 k4v = flow_accel(m, p4, v4, validity);
+    const double two = 2.0;
+    State r;
+    r.position = vadd(s.position,
+                      vscale(sixth, vadd(vadd(vadd(k1x, vscale(two, k2x)), vscale(two, k3x)), k4x)));
+    r.velocity = vadd(s.velocity,
+                      vscale(sixth, vadd(vadd(vadd(k1v, vscale(two, k2v)), vscale(two, k3v)), k4v)));
+    return r;
+}
+
+static State flow_step(const rr_metric_desc* m, State s, double h, int scheme, double* validity) {
+    return scheme == RR_SCHEME_EULER ? euler_step(m, s, h, validity) : rk4_step(m, s, h, validity);
+}
+
+void rro_flow_accel(const rr_metric_desc* m, const double pos[3], const double vel[3],
+                    double acc[3], double* validity) {
+    double v = 1.0;
+    const V3 a = flow_accel(m, vload(pos), vload(vel), &v);
+    acc[0] = a.x;
+    acc[1] = a.y;
+    acc[2] = a.z;
+    *validity = v;
+}
+
+void rro_step(const rr_metric_desc* m, const double s[6], double h, int scheme, double out[6],
+              double* validity) {
+    State st = {vload(s), vload(s + 3)};
+    const State r = flow_step(m, st, h, scheme, validity);
+    out[0] = r.position.x;
+    out[1] = r.position.y;
+    out[2] = r.position.z;
+    out[3] = r.velocity.x;
+    out[4] = r.velocity.y;
+    out[5] = r.velocity.z;
+}
+
+/* ---- scene intersection (src/render/scene.cpp) --------------------------- */
+/* chord_box_entry :15-34; returns 1 and *s when the chord enters the box */
+static int chord_box_entry(V3 a, V3 b, V3 lo, V3 hi, double* s_out) {
+    double smin = 0.0, smax = 1.0;
+    for (int e = 0; e < 3; ++e) {
+        const double ae = vcomp(a, e), be = vcomp(b, e);
+        const double l = vcomp(lo, e), h = vcomp(hi, e);
+        const double d = be - ae;
+        if (d == 0.0) {
+            if (ae < l || ae > h) return 0;
+            continue;
+        }
+        double s1 = (l - ae) / d;
+        double s2 = (h - ae) / d;
+        if (s1 > s2) {
+            const double t = s1;
+            s1 = s2;
+            s2 = t;
+        }
+        if (s1 > smin) smin = s1;
+        if (s2 < smax) smax = s2;
+        if (smin > smax) return 0;
+    }
+    *s_out = smin;
+    return 1;
+}
+
+static int hit_grid(const rr_primitive* g, V3 a, V3 b, double* s_out) {    /* :36-54 */
+    int have = 0;
+    double best = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        const double ad = vcomp(a, d), bd = vcomp(b, d);
+        const double clo = ad < bd ? ad : bd, chi = ad < bd ? bd : ad;  /* std::min / std::max */
+        const long kmin = (long)ceil((clo - g->half_width) / g->spacing);
+        const long kmax = (long)floor((chi + g->half_width) / g->spacing);
+        for (long k = kmin; k <= kmax; ++k) {
+            V3 lo = vfrom(g->bounds.min), hi = vfrom(g->bounds.max);
+            const double plane = (double)k * g->spacing;
+            const double l0 = vcomp(lo, d), h0 = vcomp(hi, d);
+            const double pl = plane - g->half_width, ph = plane + g->half_width;
+            vset(&lo, d, l0 < pl ? pl : l0);   /* std::max(lo, plane - hw) */
+            vset(&hi, d, ph < h0 ? ph : h0);   /* std::min(hi, plane + hw) */
+            if (vcomp(lo, d) > vcomp(hi, d)) continue;
+            double s;
+            if (chord_box_entry(a, b, lo, hi, &s) && (!have || s < best)) {
+                best = s;
+                have = 1;
+            }
+        }
+    }
+    *s_out = best;
+    return have;
+}
+
+static int hit_sphere(const rr_primitive* sp, V3 a, V3 b, double* s_out) {  /* :56-71 */
+    const V3 d = vsub(b, a);
+    const V3 oc = vsub(a, vfrom(sp->center));
+    const double c = vdot(oc, oc) - sp->radius * sp->radius;
+    if (c <= 0.0) {
+        *s_out = 0.0;
+        return 1;
+    }
+    const double qa = vdot(d, d);
+    const double qb = 2.0 * vdot(oc, d);
+    if (qb >= 0.0) return 0;
+    const double disc = qb * qb - 4.0 * qa * c;
+    if (disc < 0.0) return 0;
+    const double q = 0.5 * (sqrt(disc) - qb);
+    const double s = c / q;
+    if (s > 1.0) return 0;
+    *s_out = s;
+    return 1;
+}
+
+static int hit_half_space(const rr_primitive* hs, V3 a, V3 b, double* s_out) { /* :73-81 */
+    const double e0 = vdot(vfrom(hs->normal), a) - hs->offset;
+    if (e0 <= 0.0) {
+        *s_out = 0.0;
+        return 1;
+    }
+    const double de = vdot(vfrom(hs->normal), vsub(b, a));
+    if (de >= 0.0) return 0;
+    const double s = -e0 / de;
+    if (s > 1.0) return 0;
+    *s_out = s;
+    return 1;
+}
+
+static int intersect_segment(const rr_scene_desc* sc, V3 a, V3 b, V3* point, double* s_out,
+                             int* prim) {                                      /* :99-109 */
+    int have = 0;
+    double best = 0.0;
+    for (int i = 0; i < sc->n_primitives; ++i) {
+        const rr_primitive* p = &sc->primitives[i];
+        double s;
+        int h;
+        if (p->kind == RR_PRIM_GRID_PLANES) h = hit_grid(p, a, b, &s);
+        else if (p->kind == RR_PRIM_SPHERE) h = hit_sphere(p, a, b, &s);
+        else h = hit_half_space(p, a, b, &s);
+        if (h && (!have || s < best)) {
+            const V3 d = vsub(b, a);
+            *point = vadd(a, vscale(s, d));
+            best = s;
+            *prim = i;
+            have = 1;
+        }
+    }
+    *s_out = best;
+    return have;
+}
+
+int rro_intersect(const rr_scene_desc* sc, const double a[3], const double b[3], double point[3],
+                  double* s, int* prim) {
+    V3 p;
+    if (!intersect_segment(sc, vload(a), vload(b), &p, s, prim)) return 0;
+    point[0] = p.x;
+    point[1] = p.y;
+    point[2] = p.z;
+    return 1;
+}
+
+static int aabb_contains(const rr_aabb* bx, V3 p) {                          /* aabb.hpp:12-15 */
+    return p.x >= bx->min.x && p.x <= bx->max.x && p.y >= bx->min.y && p.y <= bx->max.y &&
+           p.z >= bx->min.z && p.z <= bx->max.z;
+}
+
+/* ---- march (include/rray/render/detail/kernel_impl.hpp:22-94) ------------ */
+static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                      const rr_ray_start* ray, rr_pixel_outcome* res) {
+    memset(res, 0, sizeof *res);
+    res->status = RR_MISS;
+    res->prim = -1;
+    State s = {vfrom(ray->position), vfrom(ray->direction)};
+    const double h = in->h;
+    int active = 1;
+    for (int step = 0; step < in->max_steps && active; ++step) {
+        double validity;
+        const State next = flow_step(m, s, h, in->scheme, &validity);
+        if (!(validity > kSingularDetEps)) {                                  /* :54-61 */
+            res->status = RR_FAILED;
+            res->steps = step;
+            active = 0;
+            break;
+        }
+        V3 point;
+        double hs;
+        int prim;
+        if (intersect_segment(sc, s.position, next.position, &point, &hs, &prim)) { /* :63-76 */
+            res->status = RR_HIT;
+            res->prim = prim;
+            res->point.x = point.x;
+            res->point.y = point.y;
+            res->point.z = point.z;
+            res->t = ((double)step + hs) * h;
+            res->steps = step + 1;
+            active = 0;
+            break;
+        }
+        if (!aabb_contains(&sc->bounds, next.position)) {                     /* :77-82 */
+            res->status = RR_MISS;
+            res->steps = step + 1;
+            active = 0;
+            break;
+        }
+        s = next;
+    }
+    if (active) {                                                              /* :87-91 */
+        res->status = RR_MISS;
+        res->steps = in->max_steps;
+    }
+}
+
+typedef struct {
+    const rr_metric_desc* m; const rr_scene_desc* sc; const rr_integrator* in;
+    const rr_ray_start* rays; rr_pixel_outcome* out;
+} MarchArgs;
+
+static void march_body(void* p, long lo, long hi) {
+    MarchArgs* a = (MarchArgs*)p;
+    for (long i = lo; i < hi; ++i) march_one(a->m, a->sc, a->in, &a->rays[i], &a->out[i]);
+}
+
+void rro_march(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* integ,
+               const rr_ray_start* rays, rr_pixel_outcome* out, size_t n, int threads) {
+    MarchArgs a = {m, sc, integ, rays, out};
+    parallel_for((long)n, 16, threads, march_body, &a);
+}
+
+/* ---- camera (src/render/camera.cpp, src/core/linalg.cpp:18-36) ------------ */
+int rro_build_camera(const rr_metric_desc* m, const double pos[3], const double look[3],
+                     const double up[3], double fov, rr_camera* out) {
+    memset(out, 0, sizeof *out);
+    const V3 p = vload(pos), l = vload(look), u = vload(up);
+    S3 g;
+    const int rc = metric_tensor_checked(m, p, &g);
+    if (rc) return rc;
+    const V3 seed[3] = {l, u, vcross(l, u)};
+    V3 e[3];
+    for (int i = 0; i < 3; ++i) {                                              /* linalg.cpp:18-36 */
+        V3 v = seed[i];
+        for (int j = 0; j < i; ++j) {
+            const double c = quad_form(g, v, e[j]);
+            v = vsub(v, vscale(c, e[j]));
+        }
+        const double n = sqrt(quad_form(g, v, v));
+        if (!(n >= 1e-12)) {
+            snprintf(g_err, sizeof g_err, "gram_schmidt_frame: intermediate norm below 1e-12 at vector %d", i);
+            return 2;
+        }
+        e[i] = vdiv(v, n);
+    }
+    out->position.x = p.x; out->position.y = p.y; out->position.z = p.z;
+    out->look_dir.x = l.x; out->look_dir.y = l.y; out->look_dir.z = l.z;
+    out->up_hint.x = u.x; out->up_hint.y = u.y; out->up_hint.z = u.z;
+    out->fov = fov;
+    for (int i = 0; i < 3; ++i) {
+        out->frame[i].x = e[i].x;
+        out->frame[i].y = e[i].y;
+        out->frame[i].z = e[i].z;
+    }
+    out->g[0] = g.xx; out->g[1] = g.xy; out->g[2] = g.xz;
+    out->g[3] = g.yy; out->g[4] = g.yz; out->g[5] = g.zz;
+    return 0;
+}
+
+void rro_pixel_direction(const rr_camera* cam, int px, int py, int w, int h, double out[3]) {
+    const double tan_half = tan(0.5 * cam->fov);                               /* camera.cpp:22-29 */
+    const double aspect = (double)w / (double)h;
+    const double sx = (2.0 * (px + 0.5) / w - 1.0) * tan_half * aspect;
+    const double sy = (1.0 - 2.0 * (py + 0.5) / h) * tan_half;
+    const V3 f0 = vfrom(cam->frame[0]), f1 = vfrom(cam->frame[1]), f2 = vfrom(cam->frame[2]);
+    const V3 d = vadd(vadd(f0, vscale(sx, f2)), vscale(sy, f1));
+    const S3 g = {cam->g[0], cam->g[1], cam->g[2], cam->g[3], cam->g[4], cam->g[5]};
+    const V3 r = vdiv(d, sqrt(quad_form(g, d, d)));
+    out[0] = r.x;
+    out[1] = r.y;
+    out[2] = r.z;
+}
+
+/* ---- shading (src/render/render.cpp:14-25, :39, :81-83) ------------------ */
+static uint8_t channel(double x, double atten) {
+    const double frac = x - floor(x);
+    long v = lround(255.0 * (frac * atten));
+    if (v < 0) v = 0;
+    if (v > 255) v = 255;
+    return (uint8_t)v;
+}
+
+void rro_shade_outcome(const rr_pixel_outcome* o, double kappa, uint8_t rgb[3]) {
+    if (o->status == RR_FAILED) {
+        rgb[0] = 255; rgb[1] = 0; rgb[2] = 255;
+    } else if (o->status == RR_HIT) {
+        const double atten = exp(-kappa * o->t);
+        rgb[0] = channel(o->point.x, atten);
+        rgb[1] = channel(o->point.y, atten);
+        rgb[2] = channel(o->point.z, atten);
+    } else {
+        rgb[0] = rgb[1] = rgb[2] = 0;
+    }
+}
+
+typedef struct {
+    const rr_metric_desc* m; const rr_scene_desc* sc; const rr_camera* cam;
+    const rr_integrator* in; int w, h; uint8_t* rgb; rr_pixel_outcome* outcomes;
+    atomic_llong total_steps, errors;
+} RenderArgs;
+
+static void render_rows(void* p, long lo, long hi) {
+    RenderArgs* a = (RenderArgs*)p;
+    long long steps = 0, errors = 0;
+    for (long py = lo; py < hi; ++py) {
+        for (int px = 0; px < a->w; ++px) {
+            rr_ray_start ray;
+            double d[3];
+            rro_pixel_direction(a->cam, px, (int)py, a->w, a->h, d);
+            ray.position = a->cam->position;
+            ray.direction.x = d[0];
+            ray.direction.y = d[1];
+            ray.direction.z = d[2];
+            rr_pixel_outcome o;
+            march_one(a->m, a->sc, a->in, &ray, &o);
+            const size_t i = (size_t)py * a->w + px;
+            if (a->outcomes) a->outcomes[i] = o;
+            steps += o.steps;
+            if (o.status == RR_FAILED) ++errors;
+            rro_shade_outcome(&o, a->sc->fog_density, a->rgb + 3 * i);
+        }
+    }
+    atomic_fetch_add(&a->total_steps, steps);
+    atomic_fetch_add(&a->errors, errors);
+}
+
+void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+                const rr_integrator* integ, int w, int h, uint8_t* rgb,
+                rr_pixel_outcome* outcomes, rr_stats* stats, int threads) {
+    RenderArgs a;
+    a.m = m; a.sc = sc; a.cam = cam; a.in = integ; a.w = w; a.h = h;
+    a.rgb = rgb; a.outcomes = outcomes;
+    atomic_init(&a.total_steps, 0);
+    atomic_init(&a.errors, 0);
+    parallel_for(h, 1, threads, render_rows, &a);
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        stats->rays = (int64_t)w * h;
+        stats->total_steps = atomic_load(&a.total_steps);
+        stats->pixel_errors = atomic_load(&a.errors);
+        stats->integrated_steps = stats->total_steps;
+    }
+}
+
+/* ---- parity flags ------------------------------------------- */
+static int near_integer(double x, double eps) { return fabs(x - nearbyint(x)) < eps; }
+
+typedef struct {
+    const rr_metric_desc* m; const rr_scene_desc* sc; const rr_camera* cam;
+    const rr_integrator* in; int w, h; const rr_pixel_outcome* outcomes;
+    double perturb, wrap_eps; uint8_t* flags;
+} FlagArgs;
+
+static void flag_rows(void* p, long lo, long hi) {
+    FlagArgs* a = (FlagArgs*)p;
+    const rr_camera* cam = a->cam;
+    const S3 g = {cam->g[0], cam->g[1], cam->g[2], cam->g[3], cam->g[4], cam->g[5]};
+    const V3 up = vfrom(cam->frame[1]), right = vfrom(cam->frame[2]);
+    for (long py = lo; py < hi; ++py) {
+        for (int px = 0; px < a->w; ++px) {
+            const size_t i = (size_t)py * a->w + px;
+            const rr_pixel_outcome* o = &a->outcomes[i];
+            uint8_t f = 0;
+            if (o->status == RR_HIT && (near_integer(o->point.x, a->wrap_eps) ||
+                                        near_integer(o->point.y, a->wrap_eps) ||
+                                        near_integer(o->point.z, a->wrap_eps)))
+                f |= RRO_FLAG_WRAP;
+            if (o->steps >= a->in->max_steps - 1) f |= RRO_FLAG_LIMIT;
+            double d0[3];
+            rro_pixel_direction(cam, px, (int)py, a->w, a->h, d0);
+            const V3 d = vload(d0);
+            /* Rotate the direction by +-perturb towards the camera's up and
+             * right axes (g-normalised), then renormalise to unit g-speed. */
+            const V3 axes[2] = {up, right};
+            for (int ax = 0; ax < 2 && !(f & RRO_FLAG_GRAZING); ++ax) {
+                for (int sgn = -1; sgn <= 1; sgn += 2) {
+                    const double ang = sgn * a->perturb;
+                    const double dn = sqrt(quad_form(g, d, d));
+                    const double an = sqrt(quad_form(g, axes[ax], axes[ax]));
+                    V3 q = vadd(vscale(cos(ang) / dn, d), vscale(sin(ang) / an, axes[ax]));
+                    q = vdiv(q, sqrt(quad_form(g, q, q)));
+                    rr_ray_start r;
+                    r.position = cam->position;
+                    r.direction.x = q.x;
+                    r.direction.y = q.y;
+                    r.direction.z = q.z;
+                    rr_pixel_outcome po;
+                    march_one(a->m, a->sc, a->in, &r, &po);
+                    if (po.status != o->status || po.prim != o->prim) {
+                        f |= RRO_FLAG_GRAZING;
+                        break;
+                    }
+                }
+            }
+            a->flags[i] = f;
+        }
+    }
+}
+
+void rro_flags(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+               const rr_integrator* integ, int w, int h, const rr_pixel_outcome* outcomes,
+               double perturb_rad, double wrap_eps, uint8_t* flags, int threads) {
+    FlagArgs a = {m, sc, cam, integ, w, h, outcomes, perturb_rad, wrap_eps, flags};
+    parallel_for(h, 1, threads, flag_rows, &a);
+}
