@@ -1,0 +1,350 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-pixel geodesic tracing hot path on B200.
+
+Workload (BASELINE.json configs[2], primary rays): 1920x1080, graph metric of
+16 accumulated Gaussian bumps (SURVEY.md Appendix B literal values), sphere +
+sphere + floor scene, RK4 h=0.05, max 400 steps (configs/c3_bumps16_1080p.json).
+A "step" of this benchmark is one whole frame: raygen -> metric -> RK4 ->
+intersection -> shading for all 2,073,600 pixels.
+
+  value  = geodesic RK4 steps/s, steps counted exactly as the reference's
+           RenderStats.total_steps (sum of PixelOutcome.steps), device-timed
+           with CUDA events around each frame's launch, inputs resident.
+  e2e    = the same metric through the public API with host buffers: scene
+           upload + camera + rr_render (frame D2H into pinned host memory).
+  fps    = frames per second of `value`'s timing.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Under torchrun (N>1) every rank renders a cyclic share of 32x32 tiles, the
+tiles are gathered to rank 0 with one NCCL gather and de-tiled there.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = os.path.join(ROOT, "configs", "c3_bumps16_1080p.json")
+WORKLOAD = "c3_bumps16_1080p"
+METRIC = "geodesic RK4 steps/s (1920x1080, 16 Gaussian bumps, RK4 h=0.05)"
+UNIT = "steps/s"
+TILE = 32
+# SURVEY App. A algorithmic FLOP accounting (FMA = 2): per Gaussian term per
+# accel evaluation 36, fixed per accel evaluation 13, RK4 combination 78,
+# chord test of the sphere+sphere+floor scene 58 per step.
+FLOP_BUMP, FLOP_ACCEL, FLOP_RK4, FLOP_ISECT = 36, 13, 78, 58
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at max clock
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--config", default=CONFIG)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
+    return p.parse_args()
+
+
+# ---- clocks sampling (B200_PROFILING.md clocks line) ---------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- reference CPU path (oracle/_ref = the reference compiled from its sources) ---
+def reference_sample(cfg, row_step: int):
+    from oracle import Reference
+    ref = Reference()
+    w, h = cfg.output.width, cfg.output.height
+    cores = ref.hardware_concurrency()
+    if row_step <= 0:
+        # calibrate to ~10 s of work: time every 135th row first
+        _, st = ref.render_rows(cfg, w, h, 0, 135, kernel="avx2", workers=cores)
+        per_row = st["wall_seconds"] / max(1, len(range(0, h, 135)))
+        row_step = max(1, min(h, int(math.ceil(h * per_row / 10.0))))
+    _, st = ref.render_rows(cfg, w, h, 0, row_step, kernel="avx2", workers=cores)
+    rows = len(range(0, h, row_step))
+    return {
+        "steps_per_s": st["total_steps"] / st["wall_seconds"],
+        "wall_s": st["wall_seconds"],
+        "rows": rows,
+        "row_step": row_step,
+        "cores": st["workers"],
+        "fps_extrapolated": (rows / h) / st["wall_seconds"],
+        "sample": f"every {row_step}th row ({rows} of {h} rows, {rows * w} rays) of the same frame, "
+                  f"reference render() row work items, KernelKind::Avx2, {st['workers']} threads",
+    }
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals, walls, info = [], [], None
+    for i in range(args.warmup + args.steps):
+        info = reference_sample(cfg, args.cpu_row_step if i else args.cpu_row_step)
+        if args.cpu_row_step <= 0:
+            args.cpu_row_step = info["row_step"]
+        if i >= args.warmup:
+            vals.append(info["steps_per_s"])
+            walls.append(info["wall_s"])
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(walls), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "width": cfg.output.width, "height": cfg.output.height,
+                   "bumps": 16, "scheme": cfg.integrator.scheme, "h": cfg.integrator.h,
+                   "max_steps": cfg.integrator.max_steps, "shadows": False},
+        "fps": info["fps_extrapolated"],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- own arm ----------------------------------------------------------------------
+def algorithmic_flops(stats, scheme):
+    evals_per_step = 4 if scheme == "rk4" else 1
+    comb = FLOP_RK4 if scheme == "rk4" else 12
+    steps = stats["integrated_steps"]
+    return (stats["bump_evals"] * FLOP_BUMP + steps * evals_per_step * FLOP_ACCEL +
+            steps * (comb + FLOP_ISECT))
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_05386_b200.render import Renderer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, h = cfg.output.width, cfg.output.height
+    integ = cfg.integrator
+    r = Renderer(local)
+    r.set_config(cfg)
+    cam = r.build_camera(cfg.camera)
+    # a dedicated (non-NULL) stream: NULL selects the context's own stream in the C-ABI
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sp = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    frame = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+    if world > 1:
+        max_k = r.shard_tile_count(w, h, TILE, TILE, 0, world)
+        tiles = torch.zeros(max_k * TILE * TILE * 3, dtype=torch.uint8, device="cuda")
+        gathered = torch.empty((world, tiles.numel()), dtype=torch.uint8, device="cuda") if rank == 0 else None
+
+    def one_frame():
+        if world == 1:
+            r.render_device(cam, integ, w, h, frame, stream=sp)
+        else:
+            r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp)
+            dist.gather(tiles, list(gathered.unbind(0)) if rank == 0 else None, dst=0)
+            if rank == 0:
+                r.detile(gathered, w, h, TILE, TILE, world, frame, stream=sp)
+
+    for _ in range(args.warmup):
+        one_frame()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: K frames, L2 flushed between frames (untimed)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            one_frame()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    times_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(times_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---- per-frame work accounting (deterministic; one extra stats frame)
+    if world == 1:
+        st = r.render_device(cam, integ, w, h, frame, stream=sp, with_stats=True)
+    else:
+        st = r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp,
+                            with_stats=True)
+        keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors"]
+        t = torch.tensor([st[k] for k in keys], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        st.update({k: int(v) for k, v in zip(keys, t.tolist())})
+    steps_per_frame = st["total_steps"]
+    value = steps_per_frame * args.steps / (total_ms * 1e-3)
+    fps = args.steps / (total_ms * 1e-3)
+
+    # roofline of the march kernel (the dominant kernel): algorithmic FLOP per
+    # launch / mean launch time (launch = the single-GPU frame kernel)
+    kernel_ms = statistics.mean(times_ms)
+    flop_launch = algorithmic_flops(st, integ.scheme)
+    peak = r.fp32_peak_tflops()
+    achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
+    traffic = load_traffic().get(r.last_kernel)
+
+    # ---- e2e through the public API with host buffers (rank 0 only, N=1 path)
+    e2e = None
+    if world == 1:
+        host = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
+        from paper_2005_05386_b200.render import Renderer as _R  # noqa: F401
+        e2e_frames = max(3, args.steps)
+        r.render(cam, integ, w, h, out=host)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_frames):
+            r.set_config(cfg)                              # scene upload (params + cull grid)
+            cam_e = r.build_camera(cfg.camera)
+            _, est = r.render(cam_e, integ, w, h, out=host)  # D2H of the frame + stats
+        e2e_s = (time.perf_counter() - t0) / e2e_frames
+        grid = r.options()["cull_grid"]
+        e2e = {"value": est["total_steps"] / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 6144 + 4 * grid ** 3,
+               "d2h_bytes_per_step": 3 * w * h + 64, "fps": 1.0 / e2e_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            info = reference_sample(cfg, args.cpu_row_step)
+            cpu = {"value": info["steps_per_s"], "unit": UNIT, "cores": info["cores"],
+                   "kind": "reference", "sample": info["sample"],
+                   "fps_extrapolated": info["fps_extrapolated"]}
+        except Exception as e:   # reference build absent on this box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        n_eff = st["bump_evals"] / max(1, 4 * st["integrated_steps"])
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "width": w, "height": h, "bumps": 16,
+                       "scheme": integ.scheme, "h": integ.h, "max_steps": integ.max_steps,
+                       "shadows": False, "tile": TILE if world > 1 else None,
+                       "l2": "flushed between frames (256 MB write, untimed)",
+                       "parallelism": f"tiles{world}"},
+            "fps": fps,
+            "frame_steps": steps_per_frame,
+            "avg_steps_per_ray": steps_per_frame / (w * h),
+            "n_eff_bumps": n_eff,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "measured FFMA microbenchmark (rr_measure_fp32_peak)",
+                         "peak_nominal": NOMINAL_FP32_TFLOPS,
+                         "flop_per_launch": flop_launch, "kernel": r.last_kernel},
+            "e2e": e2e,
+            "gpu_launches": args.steps * (1 if world == 1 else (2 if rank == 0 else 1)),
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    r.close()
+
+
+def main():
+    args = parse_args()
+    from paper_2005_05386_b200.config import load_config
+    cfg = load_config(args.config)
+    cfg.scene.lights = []
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

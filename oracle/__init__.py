@@ -25,6 +25,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "librray_ref.so")
 
 FLAG_GRAZING, FLAG_WRAP, FLAG_LIMIT = 1, 2, 4
+FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z = 8, 16, 32
 
 
 def _ptr(a: np.ndarray):
@@ -94,13 +95,13 @@ class Oracle:
         return out
 
     def render(self, cfg: RunConfig, w: int = 0, h: int = 0, with_flags: bool = False,
-               perturb: float = 1e-4, wrap_eps: float = 1e-4):
+               perturb: float = 1e-4, wrap_eps: float = 1e-4, camera_cfg: RunConfig = None):
         """-> (rgb[h,w,3] u8, outcomes[h*w], stats dict, flags[h*w] or None)."""
         w = w or cfg.output.width
         h = h or cfg.output.height
         md, sd = MetricDesc(cfg.metric), SceneDesc(cfg.scene)
         integ = cfg.integrator.to_abi()
-        cam = self.camera(cfg)
+        cam = self.camera(camera_cfg if camera_cfg is not None else cfg)
         rgb = np.zeros((h, w, 3), np.uint8)
         out = np.zeros(w * h, abi.OUTCOME_DTYPE)
         st = abi.rr_stats()
@@ -158,7 +159,7 @@ class Reference:
         D = C.POINTER(C.c_double)
         lib.refc_last_error.restype = C.c_char_p
         lib.refc_render.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, P,
-                                    C.POINTER(refc_stats)]
+                                    C.POINTER(refc_stats), C.c_char_p]
         lib.refc_render_rows.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, P, C.POINTER(refc_stats)]
         lib.refc_camera.argtypes = [C.c_char_p, D]
@@ -186,14 +187,15 @@ class Reference:
             return reference_json(cfg_or_text).encode()
         return cfg_or_text.encode() if isinstance(cfg_or_text, str) else cfg_or_text
 
-    def render(self, cfg, kernel="auto", workers=0, w=0, h=0):
+    def render(self, cfg, kernel="auto", workers=0, w=0, h=0, camera_cfg=None):
         j = self._json(cfg)
+        cj = self._json(camera_cfg) if camera_cfg is not None else None
         if isinstance(cfg, RunConfig):
             w = w or cfg.output.width
             h = h or cfg.output.height
         rgb = np.zeros((h, w, 3), np.uint8)
         st = refc_stats()
-        self._check(self.lib.refc_render(j, KERNELS[kernel], workers, w, h, _ptr(rgb), C.byref(st)))
+        self._check(self.lib.refc_render(j, KERNELS[kernel], workers, w, h, _ptr(rgb), C.byref(st), cj))
         return rgb, {n: getattr(st, n) for n, _ in refc_stats._fields_}
 
     def render_rows(self, cfg, w, h, row0, row_step, kernel="auto", workers=0):

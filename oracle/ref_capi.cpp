@@ -96,15 +96,18 @@ int refc_hardware_concurrency() {
 // Full frame through render::render (render.cpp:43-111).  width/height <= 0
 // keep the config's output size.
 int refc_render(const char* json, int kernel, int workers, int width, int height,
-                std::uint8_t* rgb, refc_stats* st) {
+                std::uint8_t* rgb, refc_stats* st, const char* camera_json) {
     return guarded([&] {
         config::RunConfig cfg = config::parse_config(json);
+        // Optional: build the camera against another document's metric (the
+        // reference's own magenta test does this, test_render.cpp:116-132).
+        const config::RunConfig cam_cfg = camera_json ? config::parse_config(camera_json) : cfg;
         if (width > 0) cfg.output.width = width;
         if (height > 0) cfg.output.height = height;
         render::RenderOptions opt;
         opt.workers = workers;
         opt.kernel = kind_of(kernel);
-        const auto res = render::render(cfg.metric, cfg.scene, camera_of(cfg), cfg.integrator,
+        const auto res = render::render(cfg.metric, cfg.scene, camera_of(cam_cfg), cfg.integrator,
                                         cfg.output.width, cfg.output.height, opt);
         std::memcpy(rgb, res.image.data.data(), res.image.data.size());
         if (st) {

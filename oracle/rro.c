@@ -783,14 +783,29 @@ static void flag_rows(void* p, long lo, long hi) {
             const size_t i = (size_t)py * a->w + px;
             const rr_pixel_outcome* o = &a->outcomes[i];
             uint8_t f = 0;
-            if (o->status == RR_HIT && (near_integer(o->point.x, a->wrap_eps) ||
-                                        near_integer(o->point.y, a->wrap_eps) ||
-                                        near_integer(o->point.z, a->wrap_eps)))
-                f |= RRO_FLAG_WRAP;
-            if (o->steps >= a->in->max_steps - 1) f |= RRO_FLAG_LIMIT;
+            if (o->status == RR_HIT) {
+                if (near_integer(o->point.x, a->wrap_eps)) f |= RRO_FLAG_WRAP | RRO_FLAG_WRAP_X;
+                if (near_integer(o->point.y, a->wrap_eps)) f |= RRO_FLAG_WRAP | RRO_FLAG_WRAP_Y;
+                if (near_integer(o->point.z, a->wrap_eps)) f |= RRO_FLAG_WRAP | RRO_FLAG_WRAP_Z;
+            }
             double d0[3];
             rro_pixel_direction(cam, px, (int)py, a->w, a->h, d0);
             const V3 d = vload(d0);
+            /* LIMIT: a hit on the very last step, or a miss-by-exhaustion that
+             * one more step would turn into a hit. */
+            if (o->status == RR_HIT && o->steps == a->in->max_steps) f |= RRO_FLAG_LIMIT;
+            if (o->status == RR_MISS && o->steps == a->in->max_steps) {
+                rr_integrator longer = *a->in;
+                longer.max_steps += 1;
+                rr_ray_start r0;
+                r0.position = cam->position;
+                r0.direction.x = d.x;
+                r0.direction.y = d.y;
+                r0.direction.z = d.z;
+                rr_pixel_outcome lo;
+                march_one(a->m, a->sc, &longer, &r0, &lo);
+                if (lo.status != RR_MISS) f |= RRO_FLAG_LIMIT;
+            }
             /* Rotate the direction by +-perturb towards the camera's up and
              * right axes (g-normalised), then renormalise to unit g-speed. */
             const V3 axes[2] = {up, right};

@@ -27,8 +27,11 @@ extern "C" {
 /* Flags produced by rro_flags (parity harness). */
 enum {
     RRO_FLAG_GRAZING = 1,   /* status/prim changes under +-perturbation of the direction */
-    RRO_FLAG_WRAP = 2,      /* a hit coordinate lies within wrap_eps of an integer */
-    RRO_FLAG_LIMIT = 4      /* ray ends within one step of max_steps */
+    RRO_FLAG_WRAP = 2,      /* some hit coordinate lies within wrap_eps of an integer */
+    RRO_FLAG_LIMIT = 4,     /* outcome flips if the march were one step longer / shorter */
+    RRO_FLAG_WRAP_X = 8,    /* per-channel wrap bits: R, G, B individually */
+    RRO_FLAG_WRAP_Y = 16,
+    RRO_FLAG_WRAP_Z = 32
 };
 
 const char* rro_last_error(void);

@@ -1,0 +1,129 @@
+// rr_device.cuh — compiled scene/metric program and the per-ray device math
+// of the B200 geodesic tracer (sm_100a).
+//
+// Reference arithmetic this replaces (paths under /root/reference/proj):
+//   raygen        src/render/camera.cpp:22-29                 -> raygen()
+//   metric/Gamma  include/rray/metrics/metric.hpp:69-105,
+//                 include/rray/fields/scalar_field.hpp:104-187,
+//                 include/rray/fields/diffeo.hpp:111-225       -> accel_*()
+//   integrator    include/rray/geodesics/integrate.hpp:46-99   -> march_unit()
+//   intersection  src/render/scene.cpp:15-109                  -> intersect()
+//   march loop    include/rray/render/detail/kernel_impl.hpp:22-94
+//   shading       src/render/render.cpp:14-25                  -> shade()
+//
+// Design: one warp owns a 32-ray unit (an 8x4 pixel micro-tile
+// of a frame, or 32 consecutive rays of a batch) and marches it to
+// completion; warps fetch units from a global counter (persistent CTAs).
+// State is register resident in FP32.  The graph metric never materialises
+// Gamma: with g_j = u_j (.) s_j and v_j = a_j e_j,
+//     a = (Q / (1 + |G|^2)) G,   G = sum_j v_j g_j = -grad f,
+//     Q = y^T Hess(f) y = sum_j v_j [(y.g_j)^2 - sum_k y_k^2 s_jk^2],
+// which is algebraically -Gamma(y,y) of metric.hpp:74-83.
+// Bump parameters live in the kernel's __grid_constant__ parameter block, so
+// every per-bump operand is a constant-bank operand of an FFMA.  Per step a
+// warp-uniform mask (OR of the lanes' culling-cell masks) selects the bumps
+// whose 7-sigma support can reach the unit's stage points.  The diffeo
+// metric is evaluated as a directional jet folded innermost-first,
+//     q <- D^2 Phi_s[w,w] + J_s q,  w <- J_s w,  J <- J_s J,  a = -J^-1 q,
+// equal to Gamma(y,y) = J^-1 q of metric.hpp:85-100 (Theorem 1).
+#pragma once
+
+#include <cstdint>
+
+namespace rr {
+
+constexpr int kMaxBumps = 64;     // Gaussian terms of a graph field
+constexpr int kMaxPoly = 32;      // polynomial terms of a graph field
+constexpr int kMaxStages = 16;    // stages of a linearised diffeo chain
+constexpr int kMaxPrims = 32;     // scene primitives
+constexpr int kMaxLights = 8;     // point lights (EXTENSION)
+constexpr int kUnit = 32;         // rays per warp unit
+constexpr int kMicroW = 8, kMicroH = 4;   // pixel micro-tile of one warp
+
+// g = beta * g' where g'_k = d_k * K_k, K_k = -(1/2) log2(e) / sigma_k^2.
+constexpr float kBeta = -1.3862943611198906f;   // -2 ln 2
+constexpr float kHalfLog2e = 0.7213475204444817f;
+
+enum Kind : int { kEuclid = 0, kBumps = 1, kGraphGeneral = 2, kDiffeo = 3 };
+enum Stage : int { kStageAffine = 0, kStageTwist = 1, kStageBump = 2 };
+enum Prim : int { kPrimGrid = 0, kPrimSphere = 1, kPrimHalfSpace = 2 };
+enum Mode : int { kModeFrame = 0, kModeTiles = 1, kModeRays = 2 };
+
+struct DevBump {          // one Gaussian term in factored form
+    float cx, cy, cz;     // centre
+    float kx, ky, kz;     // K = -(1/2) log2(e) / sigma^2
+    float la;             // log2 |amplitude|
+    float sgn;            // sign(amplitude)
+};
+
+struct DevPoly {          // coef * x^a y^b z^c
+    float coef;
+    int a, b, c;
+};
+
+struct DevStage {         // one stage of a diffeo chain (identity stages dropped)
+    int kind;             // kStage*
+    float det;            // AFFINE: det(matrix)
+    float v[12];          // AFFINE: m[9] row-major, off[3]
+                          // BUMP:   cx,cy,cz, sx,sy,sz (=1/sigma), amp, dx,dy,dz
+};
+
+struct DevPrim {
+    int kind;             // kPrim*
+    float spacing, hw, r; // GRID: spacing, half_width; SPHERE: radius
+    float lo[3], hi[3];   // GRID: clip bounds
+    float c[3];           // SPHERE: centre
+    float n[3];           // HALF_SPACE: normal
+    float off;            // HALF_SPACE: offset
+    float pad;
+};
+
+struct DevLight {
+    float pos[3];
+    float intensity;
+};
+
+struct DevParams {
+    int kind;             // Kind
+    int n_bumps, n_poly, n_stages;
+    int n_prims, n_lights, scheme, max_steps;
+    float h, fog;
+    float lo[3], hi[3];   // scene bounds
+    int cull;             // 1: cull_masks valid
+    int grid;             // culling voxels per axis
+    float grid_lo[3], grid_inv[3];
+    uint32_t all_mask;    // bits of every live bump
+    uint32_t pad0;
+    const uint32_t* cull_masks;   // grid^3 bump masks (device)
+    DevBump bumps[kMaxBumps];
+    DevPoly poly[kMaxPoly];
+    DevStage stages[kMaxStages];
+    DevPrim prims[kMaxPrims];
+    DevLight lights[kMaxLights];
+};
+
+struct DevCamera {        // render::Camera in device form (camera.hpp:15-30)
+    double pos[3];
+    double f0[3], f1[3], f2[3];   // look, up, right (g-orthonormal)
+    double g[6];                  // xx,xy,xz,yy,yz,zz at pos
+    double tan_half, aspect;
+};
+
+struct DevLaunch {
+    DevCamera cam;
+    int mode;                     // Mode
+    int width, height;
+    int tile_w, tile_h;           // tile mode: tile size (multiples of 8x4)
+    int shard, n_shards;
+    int tiles_x;                  // tiles per frame row
+    int micro_per_tile;           // (tile_w/8)*(tile_h/4)
+    unsigned n_units;             // warp units of this launch
+    uint8_t* rgb;                 // frame (row-major) or tile-major buffer
+    const double* rays;           // RAYS: 6 doubles per ray (RayStart)
+    uint8_t* outcomes;            // RAYS: 48-byte PixelOutcome records
+    unsigned long long n_rays;
+    unsigned* counter;            // unit dispenser (zeroed per launch)
+    unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays
+};
+
+} // namespace rr

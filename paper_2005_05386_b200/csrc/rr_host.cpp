@@ -1,0 +1,871 @@
+// rr_host.cpp — the C-ABI of include/rray_cuda.h: contexts, scene
+// compilation (variant trees -> device program), camera construction and
+// launch orchestration.  Host code; the kernels live in rr_kernels.cu.
+//
+// Reference interfaces replaced (paths under /root/reference/proj):
+//   march_fn / MarchFn / KernelKind  include/rray/render/kernel.hpp:24-59,
+//                                    src/render/kernel_dispatch.cpp:40-76
+//   render::render                   src/render/render.cpp:43-111
+//   build_camera / pixel_direction   src/render/camera.cpp:9-29
+//   gram_schmidt_frame               src/core/linalg.cpp:18-36
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rr_device.cuh"
+#include "rr_internal.h"
+#include "rray_cuda.h"
+
+namespace {
+
+using rr::DevParams;
+
+// ---- FP64 host mirror of the metric, used only for the camera frame ----------
+struct HostGauss {
+    double a, c[3], s[3];          // amplitude, centre, sigma
+};
+struct HostPoly {
+    double coef;
+    int p[3];
+};
+struct HostStage {
+    int kind;                      // rr::Stage
+    double m[9], off[3];           // affine
+    HostGauss g;                   // bump
+    double dir[3];                 // bump
+};
+
+struct Compiled {
+    int metric_kind = RR_METRIC_EUCLIDEAN;
+    std::vector<HostGauss> gauss;  // graph leaves with a != 0
+    std::vector<HostPoly> poly;
+    std::vector<HostStage> stages; // diffeo chain, innermost first
+};
+
+struct Options {
+    rr_options o;
+    Options() {
+        std::memset(&o, 0, sizeof o);
+        o.cull = 1;
+        o.cull_grid = 32;
+        o.cull_radius_sigma = 7.0;
+        o.block_x = 32;
+        o.block_y = 32;
+        o.persistent = 1;
+    }
+};
+
+} // namespace
+
+struct rr_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::mutex mu;
+    std::string err;
+    Options opt;
+    bool has_scene = false;
+    Compiled prog;
+    DevParams* P = nullptr;                  // host copy of the kernel parameter block
+    // culling grid (built lazily for the integrator step length in use)
+    uint32_t* d_masks = nullptr;
+    double masks_dilation = -1.0;
+    int masks_grid = 0;
+    double masks_radius = 0.0;
+    // scratch
+    uint8_t* d_aux = nullptr;                // [0,8): counter, [8,8+8*8): stats
+    unsigned long long* h_stats = nullptr;   // pinned
+    void* d_rays = nullptr;
+    void* d_out = nullptr;
+    size_t ray_cap = 0;
+    size_t out_cap = 0;
+    uint8_t* d_rgb = nullptr;
+    size_t rgb_cap = 0;
+    const char* last_kernel = "";
+};
+
+namespace {
+
+int set_err(rr_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_err(rr_ctx* c, cudaError_t e, const char* what) {
+    return set_err(c, RR_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define RR_CUDA(ctx, call)                                   \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call); \
+    } while (0)
+
+// ---- scene compilation ---------------------------------------------------------
+struct CompileError {
+    int code;
+    std::string msg;
+};
+
+void flatten_field(const rr_metric_desc* m, int node, int depth, Compiled& out) {
+    if (node < 0 || node >= m->n_field_nodes)
+        throw CompileError{RR_ERR_CONFIG, "metric.field: node index out of range"};
+    if (depth > 64) throw CompileError{RR_ERR_CONFIG, "metric.field: nesting deeper than 64"};
+    const rr_field_node& f = m->field_nodes[node];
+    if (f.kind == RR_FIELD_GAUSSIAN) {
+        const rr_gaussian& g = f.gaussian;
+        if (!(g.sigma.x > 0.0 && g.sigma.y > 0.0 && g.sigma.z > 0.0))
+            throw CompileError{RR_ERR_CONFIG, "metric.field.sigma: all spreads must be > 0"};
+        if (g.amplitude != 0.0)   // zero-amplitude terms contribute exactly nothing
+            out.gauss.push_back({g.amplitude, {g.center.x, g.center.y, g.center.z},
+                                 {g.sigma.x, g.sigma.y, g.sigma.z}});
+    } else if (f.kind == RR_FIELD_POLYNOMIAL) {
+        if (f.first < 0 || f.count < 0 || f.first + f.count > m->n_poly_terms)
+            throw CompileError{RR_ERR_CONFIG, "metric.field.terms: index out of range"};
+        for (int i = 0; i < f.count; ++i) {
+            const rr_poly_term& t = m->poly_terms[f.first + i];
+            const int tot = t.powers[0] + t.powers[1] + t.powers[2];
+            if (t.powers[0] < 0 || t.powers[1] < 0 || t.powers[2] < 0 || tot > 4)
+                throw CompileError{RR_ERR_CONFIG, "metric.field.terms.powers: degree must be in [0,4]"};
+            if (t.coef != 0.0) out.poly.push_back({t.coef, {t.powers[0], t.powers[1], t.powers[2]}});
+        }
+    } else if (f.kind == RR_FIELD_SUM) {
+        if (f.first < 0 || f.count < 0 || f.first + f.count > m->n_children)
+            throw CompileError{RR_ERR_CONFIG, "metric.field.terms: child index out of range"};
+        for (int i = 0; i < f.count; ++i) flatten_field(m, m->children[f.first + i], depth + 1, out);
+    } else {
+        throw CompileError{RR_ERR_CONFIG, "metric.field.kind: unknown field kind"};
+    }
+}
+
+// Linearise a diffeo tree into a chain applied innermost-first
+// (compose maps[0] is the outermost map, diffeo.hpp:88-93, :198-212).
+void flatten_diffeo(const rr_metric_desc* m, int node, int depth, Compiled& out) {
+    if (node < 0 || node >= m->n_diffeo_nodes)
+        throw CompileError{RR_ERR_CONFIG, "metric.map: node index out of range"};
+    if (depth > 64) throw CompileError{RR_ERR_CONFIG, "metric.map: nesting deeper than 64"};
+    const rr_diffeo_node& d = m->diffeo_nodes[node];
+    HostStage st{};
+    switch (d.kind) {
+        case RR_DIFFEO_IDENTITY:
+            return;
+        case RR_DIFFEO_AFFINE:
+            st.kind = rr::kStageAffine;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) st.m[3 * i + j] = d.matrix[i][j];
+            st.off[0] = d.offset.x;
+            st.off[1] = d.offset.y;
+            st.off[2] = d.offset.z;
+            break;
+        case RR_DIFFEO_TWIST:
+            st.kind = rr::kStageTwist;
+            break;
+        case RR_DIFFEO_LOCAL_BUMP: {
+            const rr_gaussian& g = d.bump;
+            if (!(g.sigma.x > 0.0 && g.sigma.y > 0.0 && g.sigma.z > 0.0))
+                throw CompileError{RR_ERR_CONFIG, "metric.map.sigma: all spreads must be > 0"};
+            st.kind = rr::kStageBump;
+            st.g = {g.amplitude, {g.center.x, g.center.y, g.center.z}, {g.sigma.x, g.sigma.y, g.sigma.z}};
+            st.dir[0] = d.direction.x;
+            st.dir[1] = d.direction.y;
+            st.dir[2] = d.direction.z;
+            break;
+        }
+        case RR_DIFFEO_COMPOSE:
+            if (d.count < 1 || d.first < 0 || d.first + d.count > m->n_children)
+                throw CompileError{RR_ERR_CONFIG, "metric.map.maps: required non-empty array"};
+            for (int i = d.count - 1; i >= 0; --i)
+                flatten_diffeo(m, m->children[d.first + i], depth + 1, out);
+            return;
+        default:
+            throw CompileError{RR_ERR_CONFIG, "metric.map.kind: unknown diffeo kind"};
+    }
+    out.stages.push_back(st);
+}
+
+double det3(const double* a) {
+    return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+           a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
+    std::memset(&P, 0, sizeof P);
+    if (c.metric_kind == RR_METRIC_EUCLIDEAN) {
+        P.kind = rr::kEuclid;
+    } else if (c.metric_kind == RR_METRIC_GRAPH) {
+        if (c.gauss.empty() && c.poly.empty()) P.kind = rr::kEuclid;
+        else if (c.poly.empty() && c.gauss.size() <= 32) P.kind = rr::kBumps;
+        else P.kind = rr::kGraphGeneral;
+    } else {
+        P.kind = c.stages.empty() ? rr::kEuclid : rr::kDiffeo;
+    }
+    P.n_bumps = (int)c.gauss.size();
+    for (size_t j = 0; j < c.gauss.size(); ++j) {
+        const HostGauss& g = c.gauss[j];
+        rr::DevBump& b = P.bumps[j];
+        b.cx = (float)g.c[0];
+        b.cy = (float)g.c[1];
+        b.cz = (float)g.c[2];
+        b.kx = (float)(-rr::kHalfLog2e / (g.s[0] * g.s[0]));
+        b.ky = (float)(-rr::kHalfLog2e / (g.s[1] * g.s[1]));
+        b.kz = (float)(-rr::kHalfLog2e / (g.s[2] * g.s[2]));
+        b.la = (float)std::log2(std::fabs(g.a));
+        b.sgn = g.a < 0.0 ? -1.f : 1.f;
+        P.all_mask |= j < 32 ? (1u << j) : 0u;
+    }
+    P.n_poly = (int)c.poly.size();
+    for (size_t i = 0; i < c.poly.size(); ++i)
+        P.poly[i] = {(float)c.poly[i].coef, c.poly[i].p[0], c.poly[i].p[1], c.poly[i].p[2]};
+    P.n_stages = (int)c.stages.size();
+    for (size_t i = 0; i < c.stages.size(); ++i) {
+        const HostStage& s = c.stages[i];
+        rr::DevStage& d = P.stages[i];
+        d.kind = s.kind;
+        if (s.kind == rr::kStageAffine) {
+            for (int k = 0; k < 9; ++k) d.v[k] = (float)s.m[k];
+            for (int k = 0; k < 3; ++k) d.v[9 + k] = (float)s.off[k];
+            d.det = (float)det3(s.m);
+        } else if (s.kind == rr::kStageBump) {
+            for (int k = 0; k < 3; ++k) {
+                d.v[k] = (float)s.g.c[k];
+                d.v[3 + k] = (float)(1.0 / s.g.s[k]);
+                d.v[7 + k] = (float)s.dir[k];
+            }
+            d.v[6] = (float)s.g.a;
+        }
+    }
+    P.n_prims = sc->n_primitives;
+    for (int i = 0; i < sc->n_primitives; ++i) {
+        const rr_primitive& q = sc->primitives[i];
+        rr::DevPrim& d = P.prims[i];
+        d.kind = q.kind == RR_PRIM_GRID_PLANES ? rr::kPrimGrid
+                 : q.kind == RR_PRIM_SPHERE    ? rr::kPrimSphere
+                                               : rr::kPrimHalfSpace;
+        d.spacing = (float)q.spacing;
+        d.hw = (float)q.half_width;
+        d.r = (float)q.radius;
+        const double lo[3] = {q.bounds.min.x, q.bounds.min.y, q.bounds.min.z};
+        const double hi[3] = {q.bounds.max.x, q.bounds.max.y, q.bounds.max.z};
+        const double cc[3] = {q.center.x, q.center.y, q.center.z};
+        const double nn[3] = {q.normal.x, q.normal.y, q.normal.z};
+        for (int k = 0; k < 3; ++k) {
+            d.lo[k] = (float)lo[k];
+            d.hi[k] = (float)hi[k];
+            d.c[k] = (float)cc[k];
+            d.n[k] = (float)nn[k];
+        }
+        d.off = (float)q.offset;
+    }
+    P.n_lights = sc->n_lights;
+    for (int i = 0; i < sc->n_lights; ++i) {
+        const rr_light& l = sc->lights[i];
+        P.lights[i] = {{(float)l.position.x, (float)l.position.y, (float)l.position.z},
+                       (float)l.intensity};
+    }
+    const double blo[3] = {sc->bounds.min.x, sc->bounds.min.y, sc->bounds.min.z};
+    const double bhi[3] = {sc->bounds.max.x, sc->bounds.max.y, sc->bounds.max.z};
+    for (int k = 0; k < 3; ++k) {
+        P.lo[k] = (float)blo[k];
+        P.hi[k] = (float)bhi[k];
+    }
+    P.fog = (float)sc->fog_density;
+}
+
+// Culling grid: bit j of cell c is set when bump j's R-sigma ellipsoid
+// reaches the cell box dilated by `dil` (stage points of a step lie within
+// h of the step's start because unit g-speed implies |y| <= 1 for graph
+// metrics).  Nearest point of an axis-aligned box to the centre, measured in
+// sigma units, decides (exact for axis-aligned ellipsoids).
+std::vector<uint32_t> build_masks(const Compiled& c, const DevParams& P, int G, double R,
+                                  double dil) {
+    std::vector<uint32_t> masks((size_t)G * G * G, 0u);
+    double lo[3], cell[3];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = P.lo[k];
+        cell[k] = ((double)P.hi[k] - P.lo[k]) / G;
+    }
+    const double R2 = R * R;
+    for (int iz = 0; iz < G; ++iz)
+        for (int iy = 0; iy < G; ++iy)
+            for (int ix = 0; ix < G; ++ix) {
+                const int idx[3] = {ix, iy, iz};
+                uint32_t m = 0;
+                for (size_t j = 0; j < c.gauss.size() && j < 32; ++j) {
+                    const HostGauss& g = c.gauss[j];
+                    double u2 = 0.0;
+                    for (int k = 0; k < 3; ++k) {
+                        // clamp cells at the border extend to infinity (clamped lookups)
+                        const double a = idx[k] == 0 ? -1e30 : lo[k] + idx[k] * cell[k] - dil;
+                        const double b = idx[k] == G - 1 ? 1e30 : lo[k] + (idx[k] + 1) * cell[k] + dil;
+                        const double n = std::min(std::max(g.c[k], a), b);
+                        const double u = (n - g.c[k]) / g.s[k];
+                        u2 += u * u;
+                    }
+                    if (u2 < R2) m |= 1u << j;
+                }
+                masks[((size_t)iz * G + iy) * G + ix] = m;
+            }
+    return masks;
+}
+
+int ensure_masks(rr_ctx* c, double h) {
+    DevParams& P = *c->P;
+    if (P.kind != rr::kBumps || !c->opt.o.cull || c->prog.gauss.size() > 32) {
+        P.cull = 0;
+        return RR_OK;
+    }
+    const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));
+    const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 7.0;
+    const double dil = 1.5 * h;
+    if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil) {
+        P.cull = 1;
+        return RR_OK;
+    }
+    const std::vector<uint32_t> m = build_masks(c->prog, P, G, R, dil);
+    if (c->d_masks && c->masks_grid != G) {
+        cudaFree(c->d_masks);
+        c->d_masks = nullptr;
+    }
+    if (!c->d_masks) RR_CUDA(c, cudaMalloc(&c->d_masks, m.size() * sizeof(uint32_t)));
+    RR_CUDA(c, cudaMemcpyAsync(c->d_masks, m.data(), m.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, c->stream));
+    RR_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->masks_grid = G;
+    c->masks_radius = R;
+    c->masks_dilation = dil;
+    P.cull = 1;
+    P.grid = G;
+    P.cull_masks = c->d_masks;
+    for (int k = 0; k < 3; ++k) {
+        P.grid_lo[k] = P.lo[k];
+        P.grid_inv[k] = (float)(G / ((double)P.hi[k] - P.lo[k]));
+    }
+    return RR_OK;
+}
+
+// ---- FP64 metric tensor at a point (camera only) -------------------------------
+// g = I + grad f grad f^T (metric.cpp:12-15) or J^T J (metric.cpp:40-42).
+int metric_tensor(const Compiled& c, const double p[3], double g[6], std::string& err) {
+    double J[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    if (c.metric_kind == RR_METRIC_GRAPH) {
+        double f[3] = {0, 0, 0};
+        for (const HostGauss& q : c.gauss) {                    // scalar_field.hpp:104-126
+            double u[3], uu = 0;
+            for (int k = 0; k < 3; ++k) {
+                u[k] = (p[k] - q.c[k]) / q.s[k];
+                uu += u[k] * u[k];
+            }
+            const double val = q.a * std::exp(-0.5 * uu);
+            for (int k = 0; k < 3; ++k) f[k] += -(val * u[k]) / q.s[k];
+        }
+        for (const HostPoly& t : c.poly) {                      // scalar_field.hpp:128-161
+            for (int k = 0; k < 3; ++k) {
+                if (t.p[k] == 0) continue;
+                double term = t.coef * t.p[k];
+                for (int i = 0; i < 3; ++i)
+                    term *= std::pow(p[i], i == k ? t.p[i] - 1 : t.p[i]);
+                f[k] += term;
+            }
+        }
+        g[0] = 1.0 + f[0] * f[0];
+        g[1] = 0.0 + f[0] * f[1];
+        g[2] = 0.0 + f[0] * f[2];
+        g[3] = 1.0 + f[1] * f[1];
+        g[4] = 0.0 + f[1] * f[2];
+        g[5] = 1.0 + f[2] * f[2];
+        return RR_OK;
+    }
+    if (c.metric_kind == RR_METRIC_DIFFEO) {
+        double x[3] = {p[0], p[1], p[2]};
+        double vmin = 1.0, dprod = 1.0;
+        for (const HostStage& s : c.stages) {
+            double Js[9], img[3];
+            if (s.kind == rr::kStageAffine) {
+                std::memcpy(Js, s.m, sizeof Js);
+                for (int i = 0; i < 3; ++i) img[i] = s.m[3 * i] * x[0] + s.m[3 * i + 1] * x[1] + s.m[3 * i + 2] * x[2] + s.off[i];
+            } else if (s.kind == rr::kStageTwist) {
+                const double cs = std::cos(x[2]), sn = std::sin(x[2]);
+                const double t[9] = {cs, -sn, -(x[0] * sn) - x[1] * cs, sn, cs, x[0] * cs - x[1] * sn, 0, 0, 1};
+                std::memcpy(Js, t, sizeof Js);
+                img[0] = x[0] * cs - x[1] * sn;
+                img[1] = x[0] * sn + x[1] * cs;
+                img[2] = x[2];
+            } else {
+                double u[3], uu = 0;
+                for (int k = 0; k < 3; ++k) {
+                    u[k] = (x[k] - s.g.c[k]) / s.g.s[k];
+                    uu += u[k] * u[k];
+                }
+                const double val = s.g.a * std::exp(-0.5 * uu);
+                double gr[3];
+                for (int k = 0; k < 3; ++k) gr[k] = -(val * u[k]) / s.g.s[k];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) Js[3 * i + j] = (i == j ? 1.0 : 0.0) + s.dir[i] * gr[j];
+                for (int k = 0; k < 3; ++k) img[k] = x[k] + val * s.dir[k];
+            }
+            const double ds = det3(Js);
+            double R[9];
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j)
+                    R[3 * i + j] = Js[3 * i] * J[j] + Js[3 * i + 1] * J[3 + j] + Js[3 * i + 2] * J[6 + j];
+            std::memcpy(J, R, sizeof J);
+            std::memcpy(x, img, sizeof x);
+            vmin = std::min(vmin, std::fabs(ds));
+            dprod *= ds;
+            vmin = std::min(vmin, std::fabs(dprod));
+        }
+        if (!c.stages.empty() && !(std::min(vmin, std::fabs(det3(J))) > 1e-14)) {
+            err = "diffeo_metric: |det J| <= 1e-14 at the camera";
+            return RR_ERR_NUMERIC;
+        }
+    }
+    // g = J^T J (linalg.hpp:239-249); identity for the Euclidean metric.
+    g[0] = J[0] * J[0] + J[3] * J[3] + J[6] * J[6];
+    g[1] = J[0] * J[1] + J[3] * J[4] + J[6] * J[7];
+    g[2] = J[0] * J[2] + J[3] * J[5] + J[6] * J[8];
+    g[3] = J[1] * J[1] + J[4] * J[4] + J[7] * J[7];
+    g[4] = J[1] * J[2] + J[4] * J[5] + J[7] * J[8];
+    g[5] = J[2] * J[2] + J[5] * J[5] + J[8] * J[8];
+    return RR_OK;
+}
+
+double quad_form(const double g[6], const double* u, const double* v) {   // linalg.hpp:121-132
+    double acc = g[0] * u[0] * v[0];
+    acc = acc + g[1] * (u[0] * v[1] + u[1] * v[0]);
+    acc = acc + g[2] * (u[0] * v[2] + u[2] * v[0]);
+    acc = acc + g[3] * u[1] * v[1];
+    acc = acc + g[4] * (u[1] * v[2] + u[2] * v[1]);
+    acc = acc + g[5] * u[2] * v[2];
+    return acc;
+}
+
+rr::DevCamera dev_camera(const rr_camera* cam, int width, int height) {
+    rr::DevCamera d{};
+    const rr_vec3* f = cam->frame;
+    const double* src[4] = {&cam->position.x, &f[0].x, &f[1].x, &f[2].x};
+    double* dst[4] = {d.pos, d.f0, d.f1, d.f2};
+    for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < 3; ++k) dst[i][k] = src[i][k];
+    for (int k = 0; k < 6; ++k) d.g[k] = cam->g[k];
+    d.tan_half = std::tan(0.5 * cam->fov);
+    d.aspect = (double)width / (double)height;
+    return d;
+}
+
+int ensure_device_buffer(rr_ctx* c, void** buf, size_t* cap, size_t need) {
+    if (*cap >= need) return RR_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    RR_CUDA(c, cudaMalloc(buf, need));
+    *cap = need;
+    return RR_OK;
+}
+
+int check_ready(rr_ctx* c, const rr_integrator* integ) {
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    if (!integ || !(integ->h > 0.0)) return set_err(c, RR_ERR_CONFIG, "integrator.h: must be > 0");
+    if (integ->max_steps < 1) return set_err(c, RR_ERR_CONFIG, "integrator.max_steps: must be >= 1");
+    if (integ->scheme != RR_SCHEME_EULER && integ->scheme != RR_SCHEME_RK4)
+        return set_err(c, RR_ERR_CONFIG, "integrator.scheme: must be euler|rk4");
+    c->P->h = (float)integ->h;
+    c->P->max_steps = integ->max_steps;
+    c->P->scheme = integ->scheme;
+    return ensure_masks(c, integ->h);
+}
+
+// Launch one march over `units` warp units; zeroes counter+stats first.
+int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
+    RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * 8, s));
+    L.counter = reinterpret_cast<unsigned*>(c->d_aux);
+    L.stats = reinterpret_cast<unsigned long long*>(c->d_aux + 8);
+    RR_CUDA(c, cudaEventRecord(c->ev0, s));
+    RR_CUDA(c, rr::launch_march(*c->P, L, s, c->num_sms, &c->last_kernel));
+    RR_CUDA(c, cudaEventRecord(c->ev1, s));
+    return RR_OK;
+}
+
+int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
+    RR_CUDA(c, cudaMemcpyAsync(c->h_stats, c->d_aux + 8, 8 * 8, cudaMemcpyDeviceToHost, s));
+    RR_CUDA(c, cudaStreamSynchronize(s));
+    if (st) {
+        std::memset(st, 0, sizeof *st);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+        st->device_ms = ms;
+        st->total_steps = (int64_t)c->h_stats[0];
+        st->pixel_errors = (int64_t)c->h_stats[1];
+        st->integrated_steps = (int64_t)c->h_stats[2];
+        st->bump_evals = (int64_t)c->h_stats[3];
+        st->rays = (int64_t)c->h_stats[4];
+        st->kernel_launches = 1;
+        const double now = std::chrono::duration<double>(
+                               std::chrono::steady_clock::now().time_since_epoch()).count();
+        st->wall_seconds = now - wall0_s;
+    }
+    return RR_OK;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int tiles_in_shard(int total, int shard, int n_shards) {
+    return shard < total ? (total - shard + n_shards - 1) / n_shards : 0;
+}
+
+int setup_frame_launch(rr_ctx* c, const rr_camera* cam, int width, int height, int tile_w,
+                       int tile_h, int shard, int n_shards, int mode, uint8_t* rgb,
+                       rr::DevLaunch& L) {
+    if (!cam) return set_err(c, RR_ERR_CONFIG, "camera: required");
+    if (width < 1 || height < 1) return set_err(c, RR_ERR_CONFIG, "output.width/height: must be >= 1");
+    if (tile_w < rr::kMicroW || tile_h < rr::kMicroH || tile_w % rr::kMicroW || tile_h % rr::kMicroH)
+        return set_err(c, RR_ERR_CONFIG, "tile size must be a positive multiple of 8x4");
+    if (n_shards < 1 || shard < 0 || shard >= n_shards)
+        return set_err(c, RR_ERR_CONFIG, "shard must lie in [0, n_shards)");
+    std::memset(&L, 0, sizeof L);
+    L.cam = dev_camera(cam, width, height);
+    L.mode = mode;
+    L.width = width;
+    L.height = height;
+    L.tile_w = tile_w;
+    L.tile_h = tile_h;
+    L.shard = shard;
+    L.n_shards = n_shards;
+    L.tiles_x = (width + tile_w - 1) / tile_w;
+    const int tiles_y = (height + tile_h - 1) / tile_h;
+    L.micro_per_tile = rr::micro_per_tile(tile_w, tile_h);
+    const long long nt = tiles_in_shard(L.tiles_x * tiles_y, shard, n_shards);
+    const long long units = nt * L.micro_per_tile;
+    if (units > 0xffffffffLL) return set_err(c, RR_ERR_CONFIG, "frame too large");
+    L.n_units = (unsigned)units;
+    L.rgb = rgb;
+    return RR_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int rr_abi_version(void) { return RR_ABI_VERSION; }
+
+const char* rr_build_info(void) {
+    return "rray_cuda sm_100a (FP32 register-resident RK4/Euler; " __DATE__ ")";
+}
+
+static thread_local std::string g_create_err;
+
+int rr_create(rr_ctx** out, int device) {
+    if (!out) return RR_ERR_CONFIG;
+    *out = nullptr;
+    rr_ctx* c = new rr_ctx();
+    c->device = device;
+    c->P = new DevParams();
+    std::memset(c->P, 0, sizeof *c->P);
+    auto fail = [&](cudaError_t e, const char* what) {
+        g_create_err = std::string(what) + ": " + cudaGetErrorString(e);
+        rr_destroy(c);
+        return RR_ERR_DEVICE;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(e, "cudaSetDevice");
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0) {
+        g_create_err = std::string("device '") + prop.name + "' is not sm_100 (this build carries sm_100a code only)";
+        rr_destroy(c);
+        return RR_ERR_DEVICE;
+    }
+    c->num_sms = prop.multiProcessorCount;
+    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreate(&c->ev0)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    if ((e = cudaEventCreate(&c->ev1)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    if ((e = cudaMalloc(&c->d_aux, 8 + 8 * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMallocHost(&c->h_stats, 8 * 8)) != cudaSuccess) return fail(e, "cudaMallocHost");
+    *out = c;
+    return RR_OK;
+}
+
+void rr_destroy(rr_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->d_masks) cudaFree(c->d_masks);
+    if (c->d_aux) cudaFree(c->d_aux);
+    if (c->h_stats) cudaFreeHost(c->h_stats);
+    if (c->d_rays) cudaFree(c->d_rays);
+    if (c->d_out) cudaFree(c->d_out);
+    if (c->d_rgb) cudaFree(c->d_rgb);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c->P;
+    delete c;
+}
+
+const char* rr_last_error(const rr_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int rr_set_options(rr_ctx* c, const rr_options* opt) {
+    if (!c || !opt) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (opt->cull_grid < 0 || opt->cull_grid > 256)
+        return set_err(c, RR_ERR_CONFIG, "options.cull_grid: must be in [0, 256]");
+    c->opt.o = *opt;
+    c->masks_dilation = -1.0;   // force a rebuild
+    return RR_OK;
+}
+
+int rr_get_options(const rr_ctx* c, rr_options* opt) {
+    if (!c || !opt) return RR_ERR_CONFIG;
+    *opt = c->opt.o;
+    return RR_OK;
+}
+
+int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!m || !sc) return set_err(c, RR_ERR_CONFIG, "metric and scene are required");
+    Compiled prog;
+    prog.metric_kind = m->kind;
+    try {
+        if (m->kind == RR_METRIC_GRAPH) flatten_field(m, m->root, 0, prog);
+        else if (m->kind == RR_METRIC_DIFFEO) flatten_diffeo(m, m->root, 0, prog);
+        else if (m->kind != RR_METRIC_EUCLIDEAN)
+            throw CompileError{RR_ERR_CONFIG, "metric.kind: must be one of euclidean|graph|diffeo"};
+    } catch (const CompileError& e) {
+        return set_err(c, e.code, e.msg);
+    }
+    if ((int)prog.gauss.size() > rr::kMaxBumps)
+        return set_err(c, RR_ERR_CONFIG, "metric.field: more Gaussian terms than this build supports (64)");
+    if ((int)prog.poly.size() > rr::kMaxPoly)
+        return set_err(c, RR_ERR_CONFIG, "metric.field: more polynomial terms than this build supports (32)");
+    if ((int)prog.stages.size() > rr::kMaxStages)
+        return set_err(c, RR_ERR_CONFIG, "metric.map: more chain stages than this build supports (16)");
+    if (sc->n_primitives < 0 || sc->n_primitives > rr::kMaxPrims)
+        return set_err(c, RR_ERR_CONFIG, "scene.primitives: at most 32 primitives");
+    if (sc->n_lights < 0 || sc->n_lights > rr::kMaxLights)
+        return set_err(c, RR_ERR_CONFIG, "scene.lights: at most 8 lights");
+    for (int i = 0; i < sc->n_primitives; ++i) {
+        const rr_primitive& q = sc->primitives[i];
+        if (q.kind == RR_PRIM_GRID_PLANES) {
+            if (!(q.half_width > 0.0) || !(q.spacing > 2.0 * q.half_width))
+                return set_err(c, RR_ERR_CONFIG, "scene.primitives: grid needs half_width > 0, spacing > 2*half_width");
+        } else if (q.kind == RR_PRIM_SPHERE) {
+            if (!(q.radius > 0.0)) return set_err(c, RR_ERR_CONFIG, "scene.primitives: radius must be > 0");
+        } else if (q.kind != RR_PRIM_HALF_SPACE) {
+            return set_err(c, RR_ERR_CONFIG, "scene.primitives.kind: unknown primitive kind");
+        }
+    }
+    c->prog = prog;
+    fill_params(c->prog, sc, *c->P);
+    c->masks_dilation = -1.0;
+    c->has_scene = true;
+    return RR_OK;
+}
+
+int rr_build_camera(rr_ctx* c, const rr_vec3* position, const rr_vec3* look_dir,
+                    const rr_vec3* up_hint, double fov, rr_camera* out) {
+    if (!c || !position || !look_dir || !up_hint || !out) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    std::memset(out, 0, sizeof *out);
+    const double p[3] = {position->x, position->y, position->z};
+    double g[6];
+    std::string err;
+    const int rc = metric_tensor(c->prog, p, g, err);
+    if (rc) return set_err(c, rc, err);
+    const double l[3] = {look_dir->x, look_dir->y, look_dir->z};
+    const double u[3] = {up_hint->x, up_hint->y, up_hint->z};
+    const double r[3] = {l[1] * u[2] - l[2] * u[1], l[2] * u[0] - l[0] * u[2], l[0] * u[1] - l[1] * u[0]};
+    const double* seed[3] = {l, u, r};
+    double e[3][3];
+    for (int i = 0; i < 3; ++i) {                                   // linalg.cpp:18-36
+        double v[3] = {seed[i][0], seed[i][1], seed[i][2]};
+        for (int j = 0; j < i; ++j) {
+            const double cc = quad_form(g, v, e[j]);
+            for (int k = 0; k < 3; ++k) v[k] = v[k] - cc * e[j][k];
+        }
+        const double n = std::sqrt(quad_form(g, v, v));
+        if (!(n >= 1e-12))
+            return set_err(c, RR_ERR_NUMERIC,
+                           "gram_schmidt_frame: intermediate norm below 1e-12 at vector " + std::to_string(i));
+        for (int k = 0; k < 3; ++k) e[i][k] = v[k] / n;
+    }
+    out->position = *position;
+    out->look_dir = *look_dir;
+    out->up_hint = *up_hint;
+    out->fov = fov;
+    for (int i = 0; i < 3; ++i) out->frame[i] = rr_vec3{e[i][0], e[i][1], e[i][2]};
+    for (int k = 0; k < 6; ++k) out->g[k] = g[k];
+    return RR_OK;
+}
+
+int rr_pixel_direction(const rr_camera* cam, int px, int py, int w, int h, rr_vec3* out) {
+    if (!cam || !out || w < 1 || h < 1) return RR_ERR_CONFIG;
+    const double tan_half = std::tan(0.5 * cam->fov);              // camera.cpp:22-29
+    const double aspect = (double)w / (double)h;
+    const double sx = (2.0 * (px + 0.5) / w - 1.0) * tan_half * aspect;
+    const double sy = (1.0 - 2.0 * (py + 0.5) / h) * tan_half;
+    const rr_vec3* f = cam->frame;
+    const double d[3] = {f[0].x + sx * f[2].x + sy * f[1].x, f[0].y + sx * f[2].y + sy * f[1].y,
+                         f[0].z + sx * f[2].z + sy * f[1].z};
+    const double n = std::sqrt(quad_form(cam->g, d, d));
+    *out = rr_vec3{d[0] / n, d[1] / n, d[2] / n};
+    return RR_OK;
+}
+
+int rr_march_device(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* d_rays,
+                    rr_pixel_outcome* d_out, size_t n, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    int rc = check_ready(c, integ);
+    if (rc) return rc;
+    if (n == 0) return RR_OK;
+    if (!d_rays || !d_out) return set_err(c, RR_ERR_CONFIG, "rays/out: required");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    rr::DevLaunch L;
+    std::memset(&L, 0, sizeof L);
+    L.mode = rr::kModeRays;
+    L.rays = reinterpret_cast<const double*>(d_rays);
+    L.outcomes = reinterpret_cast<uint8_t*>(d_out);
+    L.n_rays = n;
+    L.n_units = (unsigned)((n + rr::kUnit - 1) / rr::kUnit);
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    return run_launch(c, L, s);
+}
+
+int rr_march(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* rays,
+             rr_pixel_outcome* out, size_t n) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    int rc = check_ready(c, integ);
+    if (rc) return rc;
+    if (n == 0) return RR_OK;
+    if (!rays || !out) return set_err(c, RR_ERR_CONFIG, "rays/out: required");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    const size_t bytes = n * sizeof(rr_ray_start);
+    if ((rc = ensure_device_buffer(c, &c->d_rays, &c->ray_cap, bytes))) return rc;
+    if ((rc = ensure_device_buffer(c, &c->d_out, &c->out_cap, bytes))) return rc;
+    RR_CUDA(c, cudaMemcpyAsync(c->d_rays, rays, bytes, cudaMemcpyHostToDevice, c->stream));
+    rr::DevLaunch L;
+    std::memset(&L, 0, sizeof L);
+    L.mode = rr::kModeRays;
+    L.rays = reinterpret_cast<const double*>(c->d_rays);
+    L.outcomes = reinterpret_cast<uint8_t*>(c->d_out);
+    L.n_rays = n;
+    L.n_units = (unsigned)((n + rr::kUnit - 1) / rr::kUnit);
+    if ((rc = run_launch(c, L, c->stream))) return rc;
+    RR_CUDA(c, cudaMemcpyAsync(out, c->d_out, bytes, cudaMemcpyDeviceToHost, c->stream));
+    RR_CUDA(c, cudaStreamSynchronize(c->stream));
+    return RR_OK;
+}
+
+int rr_render_device(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                     int height, uint8_t* d_rgb, rr_stats* stats, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    const double t0 = now_s();
+    int rc = check_ready(c, integ);
+    if (rc) return rc;
+    if (!d_rgb) return set_err(c, RR_ERR_CONFIG, "rgb: required");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    rr::DevLaunch L;
+    const int tw = c->opt.o.block_x > 0 ? c->opt.o.block_x : 32;
+    const int th = c->opt.o.block_y > 0 ? c->opt.o.block_y : 32;
+    if ((rc = setup_frame_launch(c, cam, width, height, tw, th, 0, 1, rr::kModeFrame, d_rgb, L)))
+        return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    if ((rc = run_launch(c, L, s))) return rc;
+    if (stats) return collect_stats(c, s, stats, t0);
+    return RR_OK;
+}
+
+int rr_render(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width, int height,
+              uint8_t* rgb_out, rr_stats* stats) {
+    if (!c) return RR_ERR_CONFIG;
+    const double t0 = now_s();
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (!rgb_out) return set_err(c, RR_ERR_CONFIG, "rgb: required");
+        if (width < 1 || height < 1)
+            return set_err(c, RR_ERR_CONFIG, "output.width/height: must be >= 1");
+        RR_CUDA(c, cudaSetDevice(c->device));
+        const size_t bytes = (size_t)3 * width * height;
+        void* buf = c->d_rgb;
+        int rc = ensure_device_buffer(c, &buf, &c->rgb_cap, bytes);
+        c->d_rgb = (uint8_t*)buf;
+        if (rc) return rc;
+    }
+    int rc = rr_render_device(c, cam, integ, width, height, c->d_rgb, nullptr, c->stream);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    RR_CUDA(c, cudaMemcpyAsync(rgb_out, c->d_rgb, (size_t)3 * width * height,
+                               cudaMemcpyDeviceToHost, c->stream));
+    rc = collect_stats(c, c->stream, stats, t0);
+    if (rc == RR_OK && stats) stats->rays = (int64_t)width * height;
+    return rc;
+}
+
+int rr_shard_tile_count(int width, int height, int tile_w, int tile_h, int shard, int n_shards) {
+    if (width < 1 || height < 1 || tile_w < 1 || tile_h < 1 || n_shards < 1 || shard < 0 ||
+        shard >= n_shards)
+        return -1;
+    const int total = ((width + tile_w - 1) / tile_w) * ((height + tile_h - 1) / tile_h);
+    return tiles_in_shard(total, shard, n_shards);
+}
+
+int rr_render_tiles(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                    int height, int tile_w, int tile_h, int shard, int n_shards, uint8_t* d_tiles,
+                    rr_stats* stats, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    const double t0 = now_s();
+    int rc = check_ready(c, integ);
+    if (rc) return rc;
+    if (!d_tiles) return set_err(c, RR_ERR_CONFIG, "tiles: required");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    rr::DevLaunch L;
+    if ((rc = setup_frame_launch(c, cam, width, height, tile_w, tile_h, shard, n_shards,
+                                 rr::kModeTiles, d_tiles, L)))
+        return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    if ((rc = run_launch(c, L, s))) return rc;
+    if (stats) return collect_stats(c, s, stats, t0);
+    return RR_OK;
+}
+
+int rr_detile(rr_ctx* c, const uint8_t* d_gathered, int width, int height, int tile_w, int tile_h,
+              int n_shards, uint8_t* d_rgb, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!d_gathered || !d_rgb || width < 1 || height < 1 || tile_w < 1 || tile_h < 1 || n_shards < 1)
+        return set_err(c, RR_ERR_CONFIG, "rr_detile: invalid arguments");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    const int max_k = rr_shard_tile_count(width, height, tile_w, tile_h, 0, n_shards);
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    RR_CUDA(c, rr::launch_detile(d_gathered, width, height, tile_w, tile_h, n_shards, max_k, d_rgb, s));
+    return RR_OK;
+}
+
+int rr_measure_fp32_peak(rr_ctx* c, double* tflops) {
+    if (!c || !tflops) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    RR_CUDA(c, cudaSetDevice(c->device));
+    RR_CUDA(c, rr::measure_fp32_peak(c->num_sms, tflops));
+    return RR_OK;
+}
+
+// Internal: name of the kernel variant the last launch used (diagnostics).
+const char* rr_last_kernel(const rr_ctx* c) { return c ? c->last_kernel : ""; }
+
+} // extern "C"

@@ -1,0 +1,32 @@
+// rr_internal.h — host-side interface between the C-ABI layer (rr_host.cpp)
+// and the kernel launchers (rr_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "rr_device.cuh"
+
+namespace rr {
+
+// Launches the fused raygen+march+shade kernel variant matching P (kind,
+// bump capacity, scheme).  L.counter / L.stats must already be zeroed on
+// `stream`.  Returns cudaSuccess or the launch error.
+cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream,
+                         int num_sms, const char** kernel_name);
+
+// Reassembles a row-major frame from gathered tile-major shard buffers.
+cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int tile_w,
+                          int tile_h, int n_shards, int max_tiles_per_shard, uint8_t* rgb,
+                          cudaStream_t stream);
+
+// Dense FFMA microbenchmark; returns TFLOP/s (2 flop per FFMA).
+cudaError_t measure_fp32_peak(int num_sms, double* tflops);
+
+// Number of micro-tiles (warp units) covering tile k of a tiling.
+inline int micro_per_tile(int tile_w, int tile_h) {
+    return (tile_w / kMicroW) * (tile_h / kMicroH);
+}
+
+} // namespace rr

@@ -1,0 +1,731 @@
+// rr_kernels.cu — sm_100a kernels of the B200 geodesic tracer.
+//
+// K1 raygen (fused prologue)  <- pixel_direction   src/render/camera.cpp:22-29
+// K2 march                    <- march_group       include/rray/render/detail/kernel_impl.hpp:22-94
+//                                + flow_step_t     include/rray/geodesics/integrate.hpp:46-99
+//                                + christoffel_eval include/rray/metrics/metric.hpp:69-105
+//                                + intersect_segment src/render/scene.cpp:15-109
+// K3 shade (fused epilogue)   <- shade             src/render/render.cpp:14-25
+// K6 detile                   <- (none: the reference is single-process)
+// See rr_device.cuh for the math and DESIGN.md for the roofline.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "rr_device.cuh"
+#include "rr_internal.h"
+
+namespace rr {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 128;   // 4 warps per CTA
+
+struct F3 {
+    float x, y, z;
+};
+
+__device__ __forceinline__ F3 f3(float x, float y, float z) { return F3{x, y, z}; }
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---------------------------------------------------------------------------
+// Graph metric, Gaussian bumps only (factored form, rr_device.cuh header).
+// `um` is warp-uniform: bit j set <=> bump j is evaluated by the whole warp.
+template <int NB>
+__device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p, F3 y) {
+    float Gx = 0.f, Gy = 0.f, Gz = 0.f, Q1 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        if (um & (1u << j)) {
+            const DevBump& b = P.bumps[j];
+            const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
+            const float gx = dx * b.kx, gy = dy * b.ky, gz = dz * b.kz;
+            const float q = fmaf(dx, gx, fmaf(dy, gy, fmaf(dz, gz, b.la)));
+            const float vs = ex2(q) * b.sgn;
+            Gx = fmaf(vs, gx, Gx);
+            Gy = fmaf(vs, gy, Gy);
+            Gz = fmaf(vs, gz, Gz);
+            const float t = fmaf(y.x, gx, fmaf(y.y, gy, y.z * gz));
+            Q1 = fmaf(vs * t, t, Q1);
+            Sx = fmaf(vs, b.kx, Sx);
+            Sy = fmaf(vs, b.ky, Sy);
+            Sz = fmaf(vs, b.kz, Sz);
+        }
+    }
+    // G = beta G';  Q = beta^2 Q1 - beta (Y . S');  a = (Q / (1 + |G|^2)) G
+    const float ys = fmaf(y.x * y.x, Sx, fmaf(y.y * y.y, Sy, y.z * y.z * Sz));
+    const float Q = fmaf(kBeta * kBeta, Q1, -kBeta * ys);
+    const float w = fmaf(kBeta * kBeta, fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)), 1.f);
+    const float r = __fdividef(Q, w) * kBeta;
+    return f3(r * Gx, r * Gy, r * Gz);
+}
+
+// ---------------------------------------------------------------------------
+// Graph metric, general field: any number of bumps (<= kMaxBumps) plus
+// polynomial terms (scalar_field.hpp:128-161); full gradient + Hessian.
+__device__ __forceinline__ F3 accel_graph_general(const DevParams& P, F3 p, F3 y) {
+    float fx = 0.f, fy = 0.f, fz = 0.f;                               // grad f
+    float hxx = 0.f, hxy = 0.f, hxz = 0.f, hyy = 0.f, hyz = 0.f, hzz = 0.f;
+    for (int j = 0; j < P.n_bumps; ++j) {
+        const DevBump& b = P.bumps[j];
+        const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
+        const float gx = dx * b.kx * kBeta, gy = dy * b.ky * kBeta, gz = dz * b.kz * kBeta;
+        const float v = ex2(fmaf(dx * b.kx, dx, fmaf(dy * b.ky, dy, fmaf(dz * b.kz, dz, b.la)))) * b.sgn;
+        fx = fmaf(-v, gx, fx);
+        fy = fmaf(-v, gy, fy);
+        fz = fmaf(-v, gz, fz);
+        hxx = fmaf(v, fmaf(gx, gx, -b.kx * kBeta), hxx);
+        hyy = fmaf(v, fmaf(gy, gy, -b.ky * kBeta), hyy);
+        hzz = fmaf(v, fmaf(gz, gz, -b.kz * kBeta), hzz);
+        hxy = fmaf(v, gx * gy, hxy);
+        hxz = fmaf(v, gx * gz, hxz);
+        hyz = fmaf(v, gy * gz, hyz);
+    }
+    if (P.n_poly > 0) {
+        float xp[5], yp[5], zp[5];
+        xp[0] = yp[0] = zp[0] = 1.f;
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+            xp[k] = xp[k - 1] * p.x;
+            yp[k] = yp[k - 1] * p.y;
+            zp[k] = zp[k - 1] * p.z;
+        }
+        for (int i = 0; i < P.n_poly; ++i) {
+            const DevPoly& t = P.poly[i];
+            const int a = t.a, b = t.b, c = t.c;
+            const float xa = xp[a], yb = yp[b], zc = zp[c];
+            const float xa1 = a > 0 ? xp[a - 1] : 0.f, yb1 = b > 0 ? yp[b - 1] : 0.f;
+            const float zc1 = c > 0 ? zp[c - 1] : 0.f;
+            const float xa2 = a > 1 ? xp[a - 2] : 0.f, yb2 = b > 1 ? yp[b - 2] : 0.f;
+            const float zc2 = c > 1 ? zp[c - 2] : 0.f;
+            fx = fmaf(t.coef * a, xa1 * yb * zc, fx);
+            fy = fmaf(t.coef * b, xa * yb1 * zc, fy);
+            fz = fmaf(t.coef * c, xa * yb * zc1, fz);
+            hxx = fmaf(t.coef * (a * (a - 1)), xa2 * yb * zc, hxx);
+            hyy = fmaf(t.coef * (b * (b - 1)), xa * yb2 * zc, hyy);
+            hzz = fmaf(t.coef * (c * (c - 1)), xa * yb * zc2, hzz);
+            hxy = fmaf(t.coef * (a * b), xa1 * yb1 * zc, hxy);
+            hxz = fmaf(t.coef * (a * c), xa1 * yb * zc1, hxz);
+            hyz = fmaf(t.coef * (b * c), xa * yb1 * zc1, hyz);
+        }
+    }
+    // Q = y^T H y;  a = -(Q / (1 + |grad f|^2)) grad f   (metric.hpp:74-83)
+    const float Q = hxx * y.x * y.x + hyy * y.y * y.y + hzz * y.z * y.z +
+                    2.f * (hxy * y.x * y.y + hxz * y.x * y.z + hyz * y.y * y.z);
+    const float w = 1.f + fx * fx + fy * fy + fz * fz;
+    const float r = -__fdividef(Q, w);
+    return f3(r * fx, r * fy, r * fz);
+}
+
+// ---------------------------------------------------------------------------
+// Diffeo pull-back metric: directional jet folded innermost-first.
+__device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float& valid) {
+    float x0 = p.x, x1 = p.y, x2 = p.z;          // current point
+    float w0 = y.x, w1 = y.y, w2 = y.z;          // J_inner y
+    float q0 = 0.f, q1 = 0.f, q2 = 0.f;          // D^2 Phi_inner[y, y]
+    float J[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+    float vmin = 3.0e38f, dprod = 1.f;
+    for (int s = 0; s < P.n_stages; ++s) {
+        const DevStage& st = P.stages[s];
+        float det;
+        if (st.kind == kStageAffine) {                       // diffeo.hpp:133-141
+            const float* m = st.v;
+            const float n0 = m[0] * x0 + m[1] * x1 + m[2] * x2 + m[9];
+            const float n1 = m[3] * x0 + m[4] * x1 + m[5] * x2 + m[10];
+            const float n2 = m[6] * x0 + m[7] * x1 + m[8] * x2 + m[11];
+            const float a0 = m[0] * q0 + m[1] * q1 + m[2] * q2;
+            const float a1 = m[3] * q0 + m[4] * q1 + m[5] * q2;
+            const float a2 = m[6] * q0 + m[7] * q1 + m[8] * q2;
+            q0 = a0; q1 = a1; q2 = a2;
+            const float b0 = m[0] * w0 + m[1] * w1 + m[2] * w2;
+            const float b1 = m[3] * w0 + m[4] * w1 + m[5] * w2;
+            const float b2 = m[6] * w0 + m[7] * w1 + m[8] * w2;
+            w0 = b0; w1 = b1; w2 = b2;
+            float R[9];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                R[c] = m[0] * J[c] + m[1] * J[3 + c] + m[2] * J[6 + c];
+                R[3 + c] = m[3] * J[c] + m[4] * J[3 + c] + m[5] * J[6 + c];
+                R[6 + c] = m[6] * J[c] + m[7] * J[3 + c] + m[8] * J[6 + c];
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) J[k] = R[k];
+            x0 = n0; x1 = n1; x2 = n2;
+            det = st.det;
+        } else if (st.kind == kStageTwist) {                 // diffeo.hpp:143-173
+            float sn, cs;
+            sincosf(x2, &sn, &cs);
+            const float j02 = -(x0 * sn) - x1 * cs;          // d(image_0)/dz
+            const float j12 = x0 * cs - x1 * sn;             // d(image_1)/dz
+            // w^T H[0] w and w^T H[1] w (H[2] = 0)
+            const float d0 = -w2 * (2.f * (w0 * sn + w1 * cs) + w2 * j12);
+            const float d1 = w2 * (2.f * (w0 * cs - w1 * sn) + w2 * j02);
+            const float a0 = d0 + cs * q0 - sn * q1 + j02 * q2;
+            const float a1 = d1 + sn * q0 + cs * q1 + j12 * q2;
+            q0 = a0; q1 = a1;
+            const float b0 = cs * w0 - sn * w1 + j02 * w2;
+            const float b1 = sn * w0 + cs * w1 + j12 * w2;
+            w0 = b0; w1 = b1;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float r0 = cs * J[c] - sn * J[3 + c] + j02 * J[6 + c];
+                const float r1 = sn * J[c] + cs * J[3 + c] + j12 * J[6 + c];
+                J[c] = r0;
+                J[3 + c] = r1;
+            }
+            x0 = j12;                                         // x c - y s
+            x1 = -j02;                                        // x s + y c
+            det = cs * cs + sn * sn;
+        } else {                                              // diffeo.hpp:175-193
+            const float* b = st.v;
+            const float ux = (x0 - b[0]) * b[3], uy = (x1 - b[1]) * b[4], uz = (x2 - b[2]) * b[5];
+            const float e = b[6] * __expf(-0.5f * (ux * ux + uy * uy + uz * uz));
+            const float gx = ux * b[3], gy = uy * b[4], gz = uz * b[5];   // grad f = -e g
+            const float wg = w0 * gx + w1 * gy + w2 * gz;
+            const float ws = w0 * w0 * b[3] * b[3] + w1 * w1 * b[4] * b[4] + w2 * w2 * b[5] * b[5];
+            const float whw = e * (wg * wg - ws);                           // w^T Hess f w
+            const float fq = -e * (gx * q0 + gy * q1 + gz * q2);          // grad f . q
+            const float fw = -e * wg;                                       // grad f . w
+            q0 = fmaf(b[7], whw + fq, q0);
+            q1 = fmaf(b[8], whw + fq, q1);
+            q2 = fmaf(b[9], whw + fq, q2);
+            w0 = fmaf(b[7], fw, w0);
+            w1 = fmaf(b[8], fw, w1);
+            w2 = fmaf(b[9], fw, w2);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float r = -e * (gx * J[c] + gy * J[3 + c] + gz * J[6 + c]);
+                J[c] = fmaf(b[7], r, J[c]);
+                J[3 + c] = fmaf(b[8], r, J[3 + c]);
+                J[6 + c] = fmaf(b[9], r, J[6 + c]);
+            }
+            x0 = fmaf(e, b[7], x0);
+            x1 = fmaf(e, b[8], x1);
+            x2 = fmaf(e, b[9], x2);
+            det = 1.f - e * (b[7] * gx + b[8] * gy + b[9] * gz);
+        }
+        vmin = fminf(vmin, fabsf(det));
+        dprod *= det;
+        vmin = fminf(vmin, fabsf(dprod));
+    }
+    // a = -J^-1 q via the adjugate (linalg.hpp:223-236)
+    const float c00 = J[4] * J[8] - J[5] * J[7];
+    const float c01 = J[2] * J[7] - J[1] * J[8];
+    const float c02 = J[1] * J[5] - J[2] * J[4];
+    const float c10 = J[5] * J[6] - J[3] * J[8];
+    const float c11 = J[0] * J[8] - J[2] * J[6];
+    const float c12 = J[2] * J[3] - J[0] * J[5];
+    const float c20 = J[3] * J[7] - J[4] * J[6];
+    const float c21 = J[1] * J[6] - J[0] * J[7];
+    const float c22 = J[0] * J[4] - J[1] * J[3];
+    const float d = J[0] * c00 + J[1] * c10 + J[2] * c20;
+    valid = fminf(valid, fminf(vmin, fabsf(d)));
+    const float id = -1.f / d;
+    return f3(id * (c00 * q0 + c01 * q1 + c02 * q2), id * (c10 * q0 + c11 * q1 + c12 * q2),
+              id * (c20 * q0 + c21 * q1 + c22 * q2));
+}
+
+template <int KIND, int NB>
+__device__ __forceinline__ F3 accel(const DevParams& P, uint32_t um, F3 p, F3 y, float& valid) {
+    if constexpr (KIND == kEuclid) {
+        return f3(0.f, 0.f, 0.f);
+    } else if constexpr (KIND == kBumps) {
+        return accel_bumps<NB>(P, um, p, y);
+    } else if constexpr (KIND == kGraphGeneral) {
+        return accel_graph_general(P, p, y);
+    } else {
+        return accel_diffeo(P, p, y, valid);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chord-vs-primitive intersection (scene.cpp:15-109), FP32.
+__device__ __forceinline__ bool slab(float a, float d, float lo, float hi, float& smin, float& smax) {
+    if (d == 0.f) return !(a < lo || a > hi);
+    float s1 = (lo - a) / d;
+    float s2 = (hi - a) / d;
+    if (s1 > s2) {
+        const float t = s1;
+        s1 = s2;
+        s2 = t;
+    }
+    smin = fmaxf(smin, s1);
+    smax = fminf(smax, s2);
+    return !(smin > smax);
+}
+
+// chord_box_entry (scene.cpp:15-34) for a box given per axis.
+__device__ __forceinline__ bool chord_box_entry(F3 a, F3 d, F3 lo, F3 hi, float& s_out) {
+    float smin = 0.f, smax = 1.f;
+    if (!slab(a.x, d.x, lo.x, hi.x, smin, smax)) return false;
+    if (!slab(a.y, d.y, lo.y, hi.y, smin, smax)) return false;
+    if (!slab(a.z, d.z, lo.z, hi.z, smin, smax)) return false;
+    s_out = smin;
+    return true;
+}
+
+__device__ __forceinline__ float comp(F3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+__device__ __forceinline__ void set_comp(F3& v, int i, float x) {
+    if (i == 0) v.x = x;
+    else if (i == 1) v.y = x;
+    else v.z = x;
+}
+
+// hit_grid (scene.cpp:36-54): slabs around x_dim = k*spacing clipped to bounds.
+template <int DIM>
+__device__ __forceinline__ void hit_grid_dim(const DevPrim& g, F3 a, F3 b, F3 d, bool& have,
+                                             float& best) {
+    const float ad = comp(a, DIM), bd = comp(b, DIM);
+    const float clo = fminf(ad, bd), chi = fmaxf(ad, bd);
+    const int kmin = (int)ceilf((clo - g.hw) / g.spacing);
+    const int kmax = (int)floorf((chi + g.hw) / g.spacing);
+    for (int k = kmin; k <= kmax; ++k) {
+        F3 lo = f3(g.lo[0], g.lo[1], g.lo[2]), hi = f3(g.hi[0], g.hi[1], g.hi[2]);
+        const float plane = (float)k * g.spacing;
+        set_comp(lo, DIM, fmaxf(comp(lo, DIM), plane - g.hw));
+        set_comp(hi, DIM, fminf(comp(hi, DIM), plane + g.hw));
+        if (comp(lo, DIM) > comp(hi, DIM)) continue;
+        float s;
+        if (chord_box_entry(a, d, lo, hi, s) && (!have || s < best)) {
+            best = s;
+            have = true;
+        }
+    }
+}
+
+__device__ __forceinline__ bool hit_grid(const DevPrim& g, F3 a, F3 b, F3 d, float& s_out) {
+    bool have = false;
+    float best = 0.f;
+    hit_grid_dim<0>(g, a, b, d, have, best);
+    hit_grid_dim<1>(g, a, b, d, have, best);
+    hit_grid_dim<2>(g, a, b, d, have, best);
+    s_out = best;
+    return have;
+}
+
+__device__ __forceinline__ bool hit_sphere(const DevPrim& sp, F3 a, F3 d, float qa, float& s_out) {
+    const float ox = a.x - sp.c[0], oy = a.y - sp.c[1], oz = a.z - sp.c[2];
+    const float c = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -sp.r * sp.r)));
+    if (c <= 0.f) {
+        s_out = 0.f;
+        return true;
+    }
+    const float qb = 2.f * (ox * d.x + oy * d.y + oz * d.z);
+    if (qb >= 0.f) return false;
+    const float disc = qb * qb - 4.f * qa * c;
+    if (disc < 0.f) return false;
+    const float q = 0.5f * (sqrtf(disc) - qb);
+    const float s = c / q;
+    if (s > 1.f) return false;
+    s_out = s;
+    return true;
+}
+
+__device__ __forceinline__ bool hit_half_space(const DevPrim& hs, F3 a, F3 d, float& s_out) {
+    const float e0 = hs.n[0] * a.x + hs.n[1] * a.y + hs.n[2] * a.z - hs.off;
+    if (e0 <= 0.f) {
+        s_out = 0.f;
+        return true;
+    }
+    const float de = hs.n[0] * d.x + hs.n[1] * d.y + hs.n[2] * d.z;
+    if (de >= 0.f) return false;
+    const float s = -e0 / de;
+    if (s > 1.f) return false;
+    s_out = s;
+    return true;
+}
+
+__device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
+                                          int& prim) {
+    const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
+    const float qa = d.x * d.x + d.y * d.y + d.z * d.z;
+    bool have = false;
+    for (int i = 0; i < P.n_prims; ++i) {
+        const DevPrim& pr = P.prims[i];
+        float s = 0.f;
+        bool h;
+        if (pr.kind == kPrimSphere) h = hit_sphere(pr, a, d, qa, s);
+        else if (pr.kind == kPrimHalfSpace) h = hit_half_space(pr, a, d, s);
+        else h = hit_grid(pr, a, b, d, s);
+        if (h && (!have || s < s_best)) {
+            s_best = s;
+            prim = i;
+            have = true;
+        }
+    }
+    return have;
+}
+
+__device__ __forceinline__ bool inside_bounds(const DevParams& P, F3 p) {
+    return p.x >= P.lo[0] && p.x <= P.hi[0] && p.y >= P.lo[1] && p.y <= P.hi[1] &&
+           p.z >= P.lo[2] && p.z <= P.hi[2];
+}
+
+__device__ __forceinline__ uint32_t cell_mask(const DevParams& P, F3 p) {
+    const int g = P.grid;
+    const int ix = min(max((int)floorf((p.x - P.grid_lo[0]) * P.grid_inv[0]), 0), g - 1);
+    const int iy = min(max((int)floorf((p.y - P.grid_lo[1]) * P.grid_inv[1]), 0), g - 1);
+    const int iz = min(max((int)floorf((p.z - P.grid_lo[2]) * P.grid_inv[2]), 0), g - 1);
+    return __ldg(P.cull_masks + ((size_t)iz * g + iy) * g + ix);
+}
+
+struct RayResult {
+    int status;    // 0 miss 1 hit 2 failed
+    int prim;
+    int steps;
+    float t;
+    F3 point;
+};
+
+struct LaneCounters {
+    unsigned steps_integrated;
+    unsigned bump_evals;
+};
+
+// ---------------------------------------------------------------------------
+// March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
+// until every live lane has terminated; retired lanes keep computing (their
+// results are locked in), exactly as the reference's retired pack lanes.
+template <int KIND, int NB, int SCHEME>
+__device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
+                                                LaneCounters& cnt) {
+    RayResult res{0, -1, 0, 0.f, f3(0.f, 0.f, 0.f)};
+    bool active = live;
+    float cx = 0.f, cy = 0.f, cz = 0.f;       // Kahan compensation of the position sum
+    const float h = P.h;
+    const float half = 0.5f * h;
+    const float sixth = h / 6.f;
+    int step = 0;
+    for (; step < P.max_steps; ++step) {
+        if (!__any_sync(kFull, active)) break;
+        uint32_t um = 0;
+        if constexpr (KIND == kBumps) {
+            uint32_t lm = 0;
+            if (active) lm = P.cull ? cell_mask(P, p) : P.all_mask;
+            um = __reduce_or_sync(kFull, lm);
+            if (active) cnt.bump_evals += (SCHEME == 0 ? 1u : 4u) * __popc(um);
+        }
+        float valid = 3.0e38f;
+        F3 dp, vn;
+        if (SCHEME == 0) {                                   // Euler (integrate.hpp:55-61)
+            const F3 a = accel<KIND, NB>(P, um, p, v, valid);
+            dp = f3(h * v.x, h * v.y, h * v.z);
+            vn = f3(fmaf(h, a.x, v.x), fmaf(h, a.y, v.y), fmaf(h, a.z, v.z));
+        } else {                                             // RK4 (integrate.hpp:63-93)
+            F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
+            F3 ps = p, vs = v;
+#pragma unroll 1
+            for (int st = 0; st < 4; ++st) {
+                const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
+                const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
+                sx = f3(fmaf(wgt, vs.x, sx.x), fmaf(wgt, vs.y, sx.y), fmaf(wgt, vs.z, sx.z));
+                sv = f3(fmaf(wgt, a.x, sv.x), fmaf(wgt, a.y, sv.y), fmaf(wgt, a.z, sv.z));
+                const float c = st < 2 ? half : h;
+                ps = f3(fmaf(c, vs.x, p.x), fmaf(c, vs.y, p.y), fmaf(c, vs.z, p.z));
+                vs = f3(fmaf(c, a.x, v.x), fmaf(c, a.y, v.y), fmaf(c, a.z, v.z));
+            }
+            dp = f3(sixth * sx.x, sixth * sx.y, sixth * sx.z);
+            vn = f3(fmaf(sixth, sv.x, v.x), fmaf(sixth, sv.y, v.y), fmaf(sixth, sv.z, v.z));
+        }
+        // Compensated position update: pn = p + dp carrying the rounding error.
+        F3 pn;
+        {
+            const float yx = dp.x - cx, yy = dp.y - cy, yz = dp.z - cz;
+            pn = f3(p.x + yx, p.y + yy, p.z + yz);
+            cx = (pn.x - p.x) - yx;
+            cy = (pn.y - p.y) - yy;
+            cz = (pn.z - p.z) - yz;
+        }
+        if (active) {
+            cnt.steps_integrated += 1;
+            float s = 0.f;
+            int prim = -1;
+            if (KIND == kDiffeo && !(valid > 1e-14f)) {     // kernel_impl.hpp:54-61
+                res.status = 2;
+                res.steps = step;
+                active = false;
+            } else if (intersect(P, p, pn, s, prim)) {      // kernel_impl.hpp:63-76
+                res.status = 1;
+                res.prim = prim;
+                res.point = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
+                               fmaf(s, pn.z - p.z, p.z));
+                res.t = ((float)step + s) * h;
+                res.steps = step + 1;
+                active = false;
+            } else if (!inside_bounds(P, pn)) {             // kernel_impl.hpp:77-82
+                res.status = 0;
+                res.steps = step + 1;
+                active = false;
+            }
+        }
+        p = pn;
+        v = vn;
+    }
+    if (active) {                                            // kernel_impl.hpp:87-91
+        res.status = 0;
+        res.steps = P.max_steps;
+    }
+    return res;
+}
+
+// Pseudo-colour + fog (render.cpp:14-25); failures magenta (render.cpp:39).
+__device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, uint8_t* rgb) {
+    if (r.status == 2) {
+        rgb[0] = 255; rgb[1] = 0; rgb[2] = 255;
+        return;
+    }
+    if (r.status != 1) {
+        rgb[0] = rgb[1] = rgb[2] = 0;
+        return;
+    }
+    const float atten = expf(-P.fog * r.t);
+    const float pv[3] = {r.point.x, r.point.y, r.point.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float frac = pv[k] - floorf(pv[k]);
+        long v = lroundf(255.f * (frac * atten));
+        v = v < 0 ? 0 : (v > 255 ? 255 : v);
+        rgb[k] = (uint8_t)v;
+    }
+}
+
+// Primary ray of pixel (px, py) (camera.cpp:22-29), computed in FP64.
+__device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w, int h, F3& pos,
+                                       F3& dir) {
+    const double sx = (2.0 * (px + 0.5) / w - 1.0) * c.tan_half * c.aspect;
+    const double sy = (1.0 - 2.0 * (py + 0.5) / h) * c.tan_half;
+    const double dx = c.f0[0] + sx * c.f2[0] + sy * c.f1[0];
+    const double dy = c.f0[1] + sx * c.f2[1] + sy * c.f1[1];
+    const double dz = c.f0[2] + sx * c.f2[2] + sy * c.f1[2];
+    const double n2 = c.g[0] * dx * dx + c.g[3] * dy * dy + c.g[5] * dz * dz +
+                      2.0 * (c.g[1] * dx * dy + c.g[2] * dx * dz + c.g[4] * dy * dz);
+    const double inv = 1.0 / sqrt(n2);
+    pos = f3((float)c.pos[0], (float)c.pos[1], (float)c.pos[2]);
+    dir = f3((float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
+}
+
+template <int KIND, int NB, int SCHEME>
+__global__ void __launch_bounds__(kThreads, 1)
+march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long acc_steps = 0, acc_err = 0, acc_int = 0, acc_evals = 0, acc_rays = 0;
+    for (;;) {
+        unsigned unit = 0;
+        if (lane == 0) unit = atomicAdd(L.counter, 1u);
+        unit = __shfl_sync(kFull, unit, 0);
+        if (unit >= L.n_units) break;
+
+        bool live;
+        F3 pos, dir;
+        int px = 0, py = 0, lx = 0, ly = 0;
+        unsigned long long ray_index = 0, tile_k = 0;
+        if (L.mode == kModeRays) {
+            ray_index = (unsigned long long)unit * kUnit + lane;
+            live = ray_index < L.n_rays;
+            if (live) {
+                const double* r = L.rays + 6 * ray_index;
+                pos = f3((float)r[0], (float)r[1], (float)r[2]);
+                dir = f3((float)r[3], (float)r[4], (float)r[5]);
+            } else {
+                pos = dir = f3(0.f, 0.f, 0.f);
+            }
+        } else {
+            tile_k = unit / L.micro_per_tile;
+            const unsigned micro = unit % L.micro_per_tile;
+            const unsigned tile = L.shard + (unsigned)tile_k * L.n_shards;
+            const int tx = tile % L.tiles_x, ty = tile / L.tiles_x;
+            const int mpr = L.tile_w / kMicroW;
+            lx = (micro % mpr) * kMicroW + (lane & 7);
+            ly = (micro / mpr) * kMicroH + (lane >> 3);
+            px = tx * L.tile_w + lx;
+            py = ty * L.tile_h + ly;
+            live = px < L.width && py < L.height;
+            if (live) raygen(L.cam, px, py, L.width, L.height, pos, dir);
+            else pos = dir = f3(0.f, 0.f, 0.f);
+        }
+
+        LaneCounters cnt{0u, 0u};
+        const RayResult r = march_unit<KIND, NB, SCHEME>(P, live, pos, dir, cnt);
+
+        if (live) {
+            acc_steps += (unsigned)r.steps;
+            acc_err += r.status == 2 ? 1u : 0u;
+            acc_int += cnt.steps_integrated;
+            acc_evals += cnt.bump_evals;
+            acc_rays += 1;
+            if (L.mode == kModeRays) {
+                uint8_t* o = L.outcomes + 48 * ray_index;      // render::PixelOutcome
+                o[0] = (uint8_t)r.status;
+                *reinterpret_cast<int*>(o + 4) = r.status == 1 ? r.prim : -1;
+                double* pt = reinterpret_cast<double*>(o + 8);
+                pt[0] = r.status == 1 ? (double)r.point.x : 0.0;
+                pt[1] = r.status == 1 ? (double)r.point.y : 0.0;
+                pt[2] = r.status == 1 ? (double)r.point.z : 0.0;
+                *reinterpret_cast<double*>(o + 32) = r.status == 1 ? (double)r.t : 0.0;
+                *reinterpret_cast<int*>(o + 40) = r.steps;
+            } else {
+                uint8_t* dst;
+                if (L.mode == kModeFrame) {
+                    dst = L.rgb + 3 * ((size_t)py * L.width + px);
+                } else {
+                    dst = L.rgb + 3 * ((size_t)tile_k * L.tile_w * L.tile_h +
+                                       (size_t)ly * L.tile_w + lx);
+                }
+                shade(P, r, dst);
+            }
+        } else if (L.mode == kModeTiles) {
+            // zero the padding of partial edge tiles
+            uint8_t* dst = L.rgb + 3 * ((size_t)tile_k * L.tile_w * L.tile_h +
+                                        (size_t)ly * L.tile_w + lx);
+            dst[0] = dst[1] = dst[2] = 0;
+        }
+    }
+    // warp-reduce the counters, one atomic per counter per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_steps += __shfl_xor_sync(kFull, acc_steps, o);
+        acc_err += __shfl_xor_sync(kFull, acc_err, o);
+        acc_int += __shfl_xor_sync(kFull, acc_int, o);
+        acc_evals += __shfl_xor_sync(kFull, acc_evals, o);
+        acc_rays += __shfl_xor_sync(kFull, acc_rays, o);
+    }
+    if (lane == 0 && acc_rays) {
+        atomicAdd(L.stats + 0, acc_steps);
+        atomicAdd(L.stats + 1, acc_err);
+        atomicAdd(L.stats + 2, acc_int);
+        atomicAdd(L.stats + 3, acc_evals);
+        atomicAdd(L.stats + 4, acc_rays);
+    }
+}
+
+__global__ void detile_kernel(const uint8_t* __restrict__ g, int width, int height, int tw, int th,
+                              int n_shards, int max_k, int tiles_x, uint8_t* __restrict__ rgb) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x;
+    const int py = blockIdx.y;
+    if (px >= width) return;
+    const int tile = (py / th) * tiles_x + px / tw;
+    const int shard = tile % n_shards, k = tile / n_shards;
+    const size_t src = 3 * (((size_t)shard * max_k + k) * tw * th + (size_t)(py % th) * tw + px % tw);
+    const size_t dst = 3 * ((size_t)py * width + px);
+    rgb[dst] = g[src];
+    rgb[dst + 1] = g[src + 1];
+    rgb[dst + 2] = g[src + 2];
+}
+
+// FFMA throughput probe: 8 independent FMA chains per thread, imm-free.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678f) out[0] = s;   // keep the chains alive
+}
+
+template <int KIND, int NB, int SCHEME>
+int occupancy_of() {
+    static int occ = [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME>, kThreads, 0);
+        return n > 0 ? n : 1;
+    }();
+    return occ;
+}
+
+template <int KIND, int NB, int SCHEME>
+cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
+    const unsigned warps_needed = L.n_units;
+    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME>());
+    const unsigned max_useful = (warps_needed + 3) / 4;
+    if (blocks > max_useful) blocks = max_useful;
+    if (blocks == 0) blocks = 1;
+    march_kernel<KIND, NB, SCHEME><<<blocks, kThreads, 0, s>>>(P, L);
+    return cudaGetLastError();
+}
+
+template <int SCHEME>
+cudaError_t dispatch_scheme(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                            const char** name) {
+    switch (P.kind) {
+        case kEuclid:
+            *name = "march_kernel<euclid>";
+            return launch_variant<kEuclid, 0, SCHEME>(P, L, s, sms);
+        case kBumps:
+            if (P.n_bumps <= 8) {
+                *name = "march_kernel<bumps8>";
+                return launch_variant<kBumps, 8, SCHEME>(P, L, s, sms);
+            }
+            if (P.n_bumps <= 16) {
+                *name = "march_kernel<bumps16>";
+                return launch_variant<kBumps, 16, SCHEME>(P, L, s, sms);
+            }
+            *name = "march_kernel<bumps32>";
+            return launch_variant<kBumps, 32, SCHEME>(P, L, s, sms);
+        case kGraphGeneral:
+            *name = "march_kernel<graph>";
+            return launch_variant<kGraphGeneral, 0, SCHEME>(P, L, s, sms);
+        default:
+            *name = "march_kernel<diffeo>";
+            return launch_variant<kDiffeo, 0, SCHEME>(P, L, s, sms);
+    }
+}
+
+} // namespace
+
+cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream, int num_sms,
+                         const char** kernel_name) {
+    const char* dummy;
+    if (!kernel_name) kernel_name = &dummy;
+    if (L.n_units == 0) return cudaSuccess;
+    return P.scheme == 0 ? dispatch_scheme<0>(P, L, stream, num_sms, kernel_name)
+                         : dispatch_scheme<1>(P, L, stream, num_sms, kernel_name);
+}
+
+cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int tile_w, int tile_h,
+                          int n_shards, int max_k, uint8_t* rgb, cudaStream_t stream) {
+    const int tiles_x = (width + tile_w - 1) / tile_w;
+    dim3 grid((width + 255) / 256, height);
+    detile_kernel<<<grid, 256, 0, stream>>>(gathered, width, height, tile_w, tile_h, n_shards, max_k,
+                                            tiles_x, rgb);
+    return cudaGetLastError();
+}
+
+cudaError_t measure_fp32_peak(int num_sms, double* tflops) {
+    float* out = nullptr;
+    cudaError_t e = cudaMalloc(&out, sizeof(float));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    const int blocks = num_sms * 8, iters = 4096;
+    ffma_peak_kernel<<<blocks, 256>>>(out, 64, 1.0000001f, 1e-7f);   // warm-up
+    cudaEventRecord(t0);
+    ffma_peak_kernel<<<blocks, 256>>>(out, iters, 1.0000001f, 1e-7f);
+    cudaEventRecord(t1);
+    e = cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 256;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFree(out);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e;
+}
+
+} // namespace rr
