@@ -54,6 +54,8 @@ def parse_args():
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
+    p.add_argument("--opt", action="append", default=[],
+                   help="renderer option key=value (rr_options field), e.g. cull_grid=64")
     return p.parse_args()
 
 
@@ -202,6 +204,8 @@ def run_b200(args, cfg):
     w, h = cfg.output.width, cfg.output.height
     integ = cfg.integrator
     r = Renderer(local)
+    if args.opt:
+        r.set_options(**{k: type(r.options()[k])(v) for k, v in (o.split("=", 1) for o in args.opt)})
     r.set_config(cfg)
     cam = r.build_camera(cfg.camera)
     # a dedicated (non-NULL) stream: NULL selects the context's own stream in the C-ABI

@@ -195,8 +195,8 @@ typedef struct rr_stats {
 /* ---- tuning knobs (extension; defaults are parity-safe) ------------------- */
 typedef struct rr_options {
     int32_t cull;                     /* 1: per-warp bump culling on a voxel grid (default 1) */
-    int32_t cull_grid;                /* voxels per axis of the culling grid (default 32) */
-    double cull_radius_sigma;         /* bump support radius in sigmas (default 7.0) */
+    int32_t cull_grid;                /* voxels per axis of the culling grid (default 64) */
+    double cull_radius_sigma;         /* bump support radius in sigmas (default 6.0) */
     int32_t block_x, block_y;         /* pixel tile of one CTA (default 16 x 8) */
     int32_t persistent;               /* 1: persistent-thread ray queue (default 0) */
     int32_t pad_;

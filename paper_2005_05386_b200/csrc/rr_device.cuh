@@ -36,6 +36,8 @@ constexpr int kMaxBumps = 64;     // Gaussian terms of a graph field
 constexpr int kMaxPoly = 32;      // polynomial terms of a graph field
 constexpr int kMaxStages = 16;    // stages of a linearised diffeo chain
 constexpr int kMaxPrims = 32;     // scene primitives
+constexpr int kStaticSpheres = 4; // sphere slots evaluated with constant operands
+constexpr int kStaticHalves = 2;  // half-space slots evaluated with constant operands
 constexpr int kMaxLights = 8;     // point lights (EXTENSION)
 constexpr int kUnit = 32;         // rays per warp unit
 constexpr int kMicroW = 8, kMicroH = 4;   // pixel micro-tile of one warp
@@ -52,7 +54,7 @@ enum Mode : int { kModeFrame = 0, kModeTiles = 1, kModeRays = 2 };
 struct DevBump {          // one Gaussian term in factored form
     float cx, cy, cz;     // centre
     float kx, ky, kz;     // K = -(1/2) log2(e) / sigma^2
-    float la;             // log2 |amplitude|
+    float la;             // log2 |amplitude|  (-inf for an empty slot)
     float sgn;            // sign(amplitude)
 };
 
@@ -68,14 +70,27 @@ struct DevStage {         // one stage of a diffeo chain (identity stages droppe
                           // BUMP:   cx,cy,cz, sx,sy,sz (=1/sigma), amp, dx,dy,dz
 };
 
-struct DevPrim {
-    int kind;             // kPrim*
-    float spacing, hw, r; // GRID: spacing, half_width; SPHERE: radius
-    float lo[3], hi[3];   // GRID: clip bounds
-    float c[3];           // SPHERE: centre
-    float n[3];           // HALF_SPACE: normal
-    float off;            // HALF_SPACE: offset
-    float pad;
+struct DevSphere {        // scene.cpp:56-71
+    float c[3];
+    float r;
+    float r2;             // r*r
+    float two_r;          // 2r (early-out bound)
+    int index;            // position in Scene::primitives (tie-break)
+    int pad;
+};
+
+struct DevHalf {          // scene.cpp:73-81: region dot(n, p) <= off
+    float n[3];
+    float off;
+    int index;
+    int pad[3];
+};
+
+struct DevGrid {          // scene.cpp:36-54
+    float spacing, hw;
+    float lo[3], hi[3];
+    int index;
+    int pad;
 };
 
 struct DevLight {
@@ -87,18 +102,21 @@ struct DevParams {
     int kind;             // Kind
     int n_bumps, n_poly, n_stages;
     int n_prims, n_lights, scheme, max_steps;
+    int n_spheres, n_halves, n_grids;
+    int nb_slot;          // kBumps: bump slots of the kernel variant (4/8/16/32)
     float h, fog;
     float lo[3], hi[3];   // scene bounds
     int cull;             // 1: cull_masks valid
     int grid;             // culling voxels per axis
     float grid_lo[3], grid_inv[3];
-    uint32_t all_mask;    // bits of every live bump
-    uint32_t pad0;
+    uint32_t all_mask;    // bits of every live bump (slot bits for kBumps)
     const uint32_t* cull_masks;   // grid^3 bump masks (device)
     DevBump bumps[kMaxBumps];
     DevPoly poly[kMaxPoly];
     DevStage stages[kMaxStages];
-    DevPrim prims[kMaxPrims];
+    DevSphere spheres[kMaxPrims];
+    DevHalf halves[kMaxPrims];
+    DevGrid grids[kMaxPrims];
     DevLight lights[kMaxLights];
 };
 

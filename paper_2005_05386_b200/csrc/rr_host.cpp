@@ -54,8 +54,8 @@ struct Options {
     Options() {
         std::memset(&o, 0, sizeof o);
         o.cull = 1;
-        o.cull_grid = 32;
-        o.cull_radius_sigma = 7.0;
+        o.cull_grid = 64;            // 1 MB mask table; measured best
+        o.cull_radius_sigma = 6.0;   // parity-neutral (profiles/r1_cull_radius_sweep.log)
         o.block_x = 32;
         o.block_y = 32;
         o.persistent = 1;
@@ -74,6 +74,7 @@ struct rr_ctx {
     Options opt;
     bool has_scene = false;
     Compiled prog;
+    std::vector<int> slots;                  // device bump slot of each Gaussian term
     DevParams* P = nullptr;                  // host copy of the kernel parameter block
     // culling grid (built lazily for the integrator step length in use)
     uint32_t* d_masks = nullptr;
@@ -196,7 +197,8 @@ double det3(const double* a) {
            a[2] * (a[3] * a[7] - a[4] * a[6]);
 }
 
-void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
+void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::vector<int>& slots_out) {
+    slots_out.assign(c.gauss.size(), -1);
     std::memset(&P, 0, sizeof P);
     if (c.metric_kind == RR_METRIC_EUCLIDEAN) {
         P.kind = rr::kEuclid;
@@ -208,9 +210,14 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
         P.kind = c.stages.empty() ? rr::kEuclid : rr::kDiffeo;
     }
     P.n_bumps = (int)c.gauss.size();
+    // kBumps: slot = term index; nb_slot = smallest of 4/8/16/32 holding them
+    const int nterms = (int)c.gauss.size();
+    P.nb_slot = nterms <= 4 ? 4 : (nterms <= 8 ? 8 : (nterms <= 16 ? 16 : 32));
+    for (int j = 0; j < rr::kMaxBumps; ++j) P.bumps[j].la = -INFINITY;
     for (size_t j = 0; j < c.gauss.size(); ++j) {
         const HostGauss& g = c.gauss[j];
-        rr::DevBump& b = P.bumps[j];
+        const int slot = (int)j;
+        rr::DevBump& b = P.bumps[slot];
         b.cx = (float)g.c[0];
         b.cy = (float)g.c[1];
         b.cz = (float)g.c[2];
@@ -219,7 +226,8 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
         b.kz = (float)(-rr::kHalfLog2e / (g.s[2] * g.s[2]));
         b.la = (float)std::log2(std::fabs(g.a));
         b.sgn = g.a < 0.0 ? -1.f : 1.f;
-        P.all_mask |= j < 32 ? (1u << j) : 0u;
+        if (slot < 32) P.all_mask |= 1u << slot;
+        slots_out[j] = slot;
     }
     P.n_poly = (int)c.poly.size();
     for (size_t i = 0; i < c.poly.size(); ++i)
@@ -243,26 +251,37 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
         }
     }
     P.n_prims = sc->n_primitives;
+    P.n_spheres = P.n_halves = P.n_grids = 0;
     for (int i = 0; i < sc->n_primitives; ++i) {
         const rr_primitive& q = sc->primitives[i];
-        rr::DevPrim& d = P.prims[i];
-        d.kind = q.kind == RR_PRIM_GRID_PLANES ? rr::kPrimGrid
-                 : q.kind == RR_PRIM_SPHERE    ? rr::kPrimSphere
-                                               : rr::kPrimHalfSpace;
-        d.spacing = (float)q.spacing;
-        d.hw = (float)q.half_width;
-        d.r = (float)q.radius;
-        const double lo[3] = {q.bounds.min.x, q.bounds.min.y, q.bounds.min.z};
-        const double hi[3] = {q.bounds.max.x, q.bounds.max.y, q.bounds.max.z};
-        const double cc[3] = {q.center.x, q.center.y, q.center.z};
-        const double nn[3] = {q.normal.x, q.normal.y, q.normal.z};
-        for (int k = 0; k < 3; ++k) {
-            d.lo[k] = (float)lo[k];
-            d.hi[k] = (float)hi[k];
-            d.c[k] = (float)cc[k];
-            d.n[k] = (float)nn[k];
+        if (q.kind == RR_PRIM_SPHERE) {
+            rr::DevSphere& d = P.spheres[P.n_spheres++];
+            d.c[0] = (float)q.center.x;
+            d.c[1] = (float)q.center.y;
+            d.c[2] = (float)q.center.z;
+            d.r = (float)q.radius;
+            d.r2 = d.r * d.r;
+            d.two_r = 2.f * d.r;
+            d.index = i;
+        } else if (q.kind == RR_PRIM_HALF_SPACE) {
+            rr::DevHalf& d = P.halves[P.n_halves++];
+            d.n[0] = (float)q.normal.x;
+            d.n[1] = (float)q.normal.y;
+            d.n[2] = (float)q.normal.z;
+            d.off = (float)q.offset;
+            d.index = i;
+        } else {
+            rr::DevGrid& d = P.grids[P.n_grids++];
+            d.spacing = (float)q.spacing;
+            d.hw = (float)q.half_width;
+            d.lo[0] = (float)q.bounds.min.x;
+            d.lo[1] = (float)q.bounds.min.y;
+            d.lo[2] = (float)q.bounds.min.z;
+            d.hi[0] = (float)q.bounds.max.x;
+            d.hi[1] = (float)q.bounds.max.y;
+            d.hi[2] = (float)q.bounds.max.z;
+            d.index = i;
         }
-        d.off = (float)q.offset;
     }
     P.n_lights = sc->n_lights;
     for (int i = 0; i < sc->n_lights; ++i) {
@@ -284,8 +303,8 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P) {
 // h of the step's start because unit g-speed implies |y| <= 1 for graph
 // metrics).  Nearest point of an axis-aligned box to the centre, measured in
 // sigma units, decides (exact for axis-aligned ellipsoids).
-std::vector<uint32_t> build_masks(const Compiled& c, const DevParams& P, int G, double R,
-                                  double dil) {
+std::vector<uint32_t> build_masks(const Compiled& c, const std::vector<int>& slots,
+                                  const DevParams& P, int G, double R, double dil) {
     std::vector<uint32_t> masks((size_t)G * G * G, 0u);
     double lo[3], cell[3];
     for (int k = 0; k < 3; ++k) {
@@ -298,7 +317,8 @@ std::vector<uint32_t> build_masks(const Compiled& c, const DevParams& P, int G, 
             for (int ix = 0; ix < G; ++ix) {
                 const int idx[3] = {ix, iy, iz};
                 uint32_t m = 0;
-                for (size_t j = 0; j < c.gauss.size() && j < 32; ++j) {
+                for (size_t j = 0; j < c.gauss.size(); ++j) {
+                    if (slots[j] < 0 || slots[j] >= 32) continue;
                     const HostGauss& g = c.gauss[j];
                     double u2 = 0.0;
                     for (int k = 0; k < 3; ++k) {
@@ -309,7 +329,7 @@ std::vector<uint32_t> build_masks(const Compiled& c, const DevParams& P, int G, 
                         const double u = (n - g.c[k]) / g.s[k];
                         u2 += u * u;
                     }
-                    if (u2 < R2) m |= 1u << j;
+                    if (u2 < R2) m |= 1u << slots[j];
                 }
                 masks[((size_t)iz * G + iy) * G + ix] = m;
             }
@@ -318,18 +338,18 @@ std::vector<uint32_t> build_masks(const Compiled& c, const DevParams& P, int G, 
 
 int ensure_masks(rr_ctx* c, double h) {
     DevParams& P = *c->P;
-    if (P.kind != rr::kBumps || !c->opt.o.cull || c->prog.gauss.size() > 32) {
+    if (P.kind != rr::kBumps || !c->opt.o.cull) {
         P.cull = 0;
         return RR_OK;
     }
     const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));
-    const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 7.0;
+    const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 6.0;
     const double dil = 1.5 * h;
     if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil) {
         P.cull = 1;
         return RR_OK;
     }
-    const std::vector<uint32_t> m = build_masks(c->prog, P, G, R, dil);
+    const std::vector<uint32_t> m = build_masks(c->prog, c->slots, P, G, R, dil);
     if (c->d_masks && c->masks_grid != G) {
         cudaFree(c->d_masks);
         c->d_masks = nullptr;
@@ -667,7 +687,7 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
         }
     }
     c->prog = prog;
-    fill_params(c->prog, sc, *c->P);
+    fill_params(c->prog, sc, *c->P, c->slots);
     c->masks_dilation = -1.0;
     c->has_scene = true;
     return RR_OK;

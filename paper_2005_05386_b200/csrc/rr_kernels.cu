@@ -21,6 +21,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 128;   // 4 warps per CTA
+#ifndef RR_MIN_BLOCKS
+#define RR_MIN_BLOCKS 7   // <= 72 registers: 7 CTAs = 28 warps per SM (measured best)
+#endif
 
 struct F3 {
     float x, y, z;
@@ -34,9 +37,24 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // ---------------------------------------------------------------------------
 // Graph metric, Gaussian bumps only (factored form, rr_device.cuh header).
-// `um` is warp-uniform: bit j set <=> bump j is evaluated by the whole warp.
+// `um` is warp-uniform: bit j set <=> bump slot j is evaluated by the whole
+// warp this step.  Slot tests cost 2 issue slots each, so NB is the smallest
+// of 4/8/16/32 holding the field (a sign-split slot layout was measured
+// slower: it doubles the slots tested per evaluation).
 template <int NB>
 __device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p, F3 y) {
     float Gx = 0.f, Gy = 0.f, Gz = 0.f, Q1 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f;
@@ -47,22 +65,22 @@ __device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p,
             const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
             const float gx = dx * b.kx, gy = dy * b.ky, gz = dz * b.kz;
             const float q = fmaf(dx, gx, fmaf(dy, gy, fmaf(dz, gz, b.la)));
-            const float vs = ex2(q) * b.sgn;
-            Gx = fmaf(vs, gx, Gx);
-            Gy = fmaf(vs, gy, Gy);
-            Gz = fmaf(vs, gz, Gz);
+            const float v = ex2(q) * b.sgn;
+            Gx = fmaf(v, gx, Gx);
+            Gy = fmaf(v, gy, Gy);
+            Gz = fmaf(v, gz, Gz);
             const float t = fmaf(y.x, gx, fmaf(y.y, gy, y.z * gz));
-            Q1 = fmaf(vs * t, t, Q1);
-            Sx = fmaf(vs, b.kx, Sx);
-            Sy = fmaf(vs, b.ky, Sy);
-            Sz = fmaf(vs, b.kz, Sz);
+            Q1 = fmaf(v * t, t, Q1);
+            Sx = fmaf(v, b.kx, Sx);
+            Sy = fmaf(v, b.ky, Sy);
+            Sz = fmaf(v, b.kz, Sz);
         }
     }
     // G = beta G';  Q = beta^2 Q1 - beta (Y . S');  a = (Q / (1 + |G|^2)) G
     const float ys = fmaf(y.x * y.x, Sx, fmaf(y.y * y.y, Sy, y.z * y.z * Sz));
     const float Q = fmaf(kBeta * kBeta, Q1, -kBeta * ys);
     const float w = fmaf(kBeta * kBeta, fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)), 1.f);
-    const float r = __fdividef(Q, w) * kBeta;
+    const float r = Q * rcp_approx(w) * kBeta;
     return f3(r * Gx, r * Gy, r * Gz);
 }
 
@@ -119,7 +137,7 @@ __device__ __forceinline__ F3 accel_graph_general(const DevParams& P, F3 p, F3 y
     const float Q = hxx * y.x * y.x + hyy * y.y * y.y + hzz * y.z * y.z +
                     2.f * (hxy * y.x * y.y + hxz * y.x * y.z + hyz * y.y * y.z);
     const float w = 1.f + fx * fx + fy * fy + fz * fz;
-    const float r = -__fdividef(Q, w);
+    const float r = -Q * rcp_approx(w);
     return f3(r * fx, r * fy, r * fz);
 }
 
@@ -279,7 +297,7 @@ __device__ __forceinline__ void set_comp(F3& v, int i, float x) {
 
 // hit_grid (scene.cpp:36-54): slabs around x_dim = k*spacing clipped to bounds.
 template <int DIM>
-__device__ __forceinline__ void hit_grid_dim(const DevPrim& g, F3 a, F3 b, F3 d, bool& have,
+__device__ __forceinline__ void hit_grid_dim(const DevGrid& g, F3 a, F3 b, F3 d, bool& have,
                                              float& best) {
     const float ad = comp(a, DIM), bd = comp(b, DIM);
     const float clo = fminf(ad, bd), chi = fmaxf(ad, bd);
@@ -299,7 +317,7 @@ __device__ __forceinline__ void hit_grid_dim(const DevPrim& g, F3 a, F3 b, F3 d,
     }
 }
 
-__device__ __forceinline__ bool hit_grid(const DevPrim& g, F3 a, F3 b, F3 d, float& s_out) {
+__device__ __forceinline__ bool hit_grid(const DevGrid& g, F3 a, F3 b, F3 d, float& s_out) {
     bool have = false;
     float best = 0.f;
     hit_grid_dim<0>(g, a, b, d, have, best);
@@ -309,13 +327,18 @@ __device__ __forceinline__ bool hit_grid(const DevPrim& g, F3 a, F3 b, F3 d, flo
     return have;
 }
 
-__device__ __forceinline__ bool hit_sphere(const DevPrim& sp, F3 a, F3 d, float qa, float& s_out) {
+// hit_sphere (scene.cpp:56-71) with a conservative early-out: a chord of
+// length L starting outside cannot reach the sphere when |oc| > r + L, i.e.
+// c = |oc|^2 - r^2 > (2r + L) L.
+__device__ __forceinline__ bool hit_sphere(const DevSphere& sp, F3 a, F3 d, float qa, float len,
+                                           float& s_out) {
     const float ox = a.x - sp.c[0], oy = a.y - sp.c[1], oz = a.z - sp.c[2];
-    const float c = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -sp.r * sp.r)));
+    const float c = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -sp.r2)));
     if (c <= 0.f) {
         s_out = 0.f;
         return true;
     }
+    if (fmaf(-len, sp.two_r + len, c) > 0.f) return false;
     const float qb = 2.f * (ox * d.x + oy * d.y + oz * d.z);
     if (qb >= 0.f) return false;
     const float disc = qb * qb - 4.f * qa * c;
@@ -327,7 +350,7 @@ __device__ __forceinline__ bool hit_sphere(const DevPrim& sp, F3 a, F3 d, float 
     return true;
 }
 
-__device__ __forceinline__ bool hit_half_space(const DevPrim& hs, F3 a, F3 d, float& s_out) {
+__device__ __forceinline__ bool hit_half_space(const DevHalf& hs, F3 a, F3 d, float& s_out) {
     const float e0 = hs.n[0] * a.x + hs.n[1] * a.y + hs.n[2] * a.z - hs.off;
     if (e0 <= 0.f) {
         s_out = 0.f;
@@ -341,23 +364,47 @@ __device__ __forceinline__ bool hit_half_space(const DevPrim& hs, F3 a, F3 d, fl
     return true;
 }
 
+// Nearest hit over all primitives; ties keep the lower primitive index
+// (scene.cpp:99-109), i.e. the lexicographic minimum of (s, index).
+__device__ __forceinline__ void consider(bool h, float s, int idx, bool& have, float& best,
+                                         int& prim) {
+    if (h && (!have || s < best || (s == best && idx < prim))) {
+        best = s;
+        prim = idx;
+        have = true;
+    }
+}
+
 __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
                                           int& prim) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
-    const float qa = d.x * d.x + d.y * d.y + d.z * d.z;
+    const float qa = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
+    const float len = fmaf(sqrt_approx(qa), 1.0001f, 1e-30f);   // conservative chord length
     bool have = false;
-    for (int i = 0; i < P.n_prims; ++i) {
-        const DevPrim& pr = P.prims[i];
-        float s = 0.f;
-        bool h;
-        if (pr.kind == kPrimSphere) h = hit_sphere(pr, a, d, qa, s);
-        else if (pr.kind == kPrimHalfSpace) h = hit_half_space(pr, a, d, s);
-        else h = hit_grid(pr, a, b, d, s);
-        if (h && (!have || s < s_best)) {
-            s_best = s;
-            prim = i;
-            have = true;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kStaticSpheres; ++i)
+        if (i < P.n_spheres) {
+            const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
+            consider(h, s, P.spheres[i].index, have, s_best, prim);
         }
+    for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
+        const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
+        consider(h, s, P.spheres[i].index, have, s_best, prim);
+    }
+#pragma unroll
+    for (int i = 0; i < kStaticHalves; ++i)
+        if (i < P.n_halves) {
+            const bool h = hit_half_space(P.halves[i], a, d, s);
+            consider(h, s, P.halves[i].index, have, s_best, prim);
+        }
+    for (int i = kStaticHalves; i < P.n_halves; ++i) {
+        const bool h = hit_half_space(P.halves[i], a, d, s);
+        consider(h, s, P.halves[i].index, have, s_best, prim);
+    }
+    for (int i = 0; i < P.n_grids; ++i) {
+        const bool h = hit_grid(P.grids[i], a, b, d, s);
+        consider(h, s, P.grids[i].index, have, s_best, prim);
     }
     return have;
 }
@@ -421,7 +468,7 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
             F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
             F3 ps = p, vs = v;
 #pragma unroll 1
-            for (int st = 0; st < 4; ++st) {
+            for (int st = 0; st < 4; ++st) {   // one call site: the bump block is inlined once
                 const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
                 const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
                 sx = f3(fmaf(wgt, vs.x, sx.x), fmaf(wgt, vs.y, sx.y), fmaf(wgt, vs.z, sx.z));
@@ -511,10 +558,9 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
 }
 
 template <int KIND, int NB, int SCHEME>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, RR_MIN_BLOCKS)
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
-    unsigned long long acc_steps = 0, acc_err = 0, acc_int = 0, acc_evals = 0, acc_rays = 0;
     for (;;) {
         unsigned unit = 0;
         if (lane == 0) unit = atomicAdd(L.counter, 1u);
@@ -554,11 +600,6 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
         const RayResult r = march_unit<KIND, NB, SCHEME>(P, live, pos, dir, cnt);
 
         if (live) {
-            acc_steps += (unsigned)r.steps;
-            acc_err += r.status == 2 ? 1u : 0u;
-            acc_int += cnt.steps_integrated;
-            acc_evals += cnt.bump_evals;
-            acc_rays += 1;
             if (L.mode == kModeRays) {
                 uint8_t* o = L.outcomes + 48 * ray_index;      // render::PixelOutcome
                 o[0] = (uint8_t)r.status;
@@ -585,22 +626,19 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                                         (size_t)ly * L.tile_w + lx);
             dst[0] = dst[1] = dst[2] = 0;
         }
-    }
-    // warp-reduce the counters, one atomic per counter per warp
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        acc_steps += __shfl_xor_sync(kFull, acc_steps, o);
-        acc_err += __shfl_xor_sync(kFull, acc_err, o);
-        acc_int += __shfl_xor_sync(kFull, acc_int, o);
-        acc_evals += __shfl_xor_sync(kFull, acc_evals, o);
-        acc_rays += __shfl_xor_sync(kFull, acc_rays, o);
-    }
-    if (lane == 0 && acc_rays) {
-        atomicAdd(L.stats + 0, acc_steps);
-        atomicAdd(L.stats + 1, acc_err);
-        atomicAdd(L.stats + 2, acc_int);
-        atomicAdd(L.stats + 3, acc_evals);
-        atomicAdd(L.stats + 4, acc_rays);
+        // per-unit counters: one REDUX per counter, one 64-bit atomic per warp
+        const unsigned steps = __reduce_add_sync(kFull, live ? (unsigned)r.steps : 0u);
+        const unsigned errs = __reduce_add_sync(kFull, (live && r.status == 2) ? 1u : 0u);
+        const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
+        const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
+        const unsigned nr = __reduce_add_sync(kFull, live ? 1u : 0u);
+        if (lane == 0) {
+            atomicAdd(L.stats + 0, (unsigned long long)steps);
+            if (errs) atomicAdd(L.stats + 1, (unsigned long long)errs);
+            atomicAdd(L.stats + 2, (unsigned long long)integ);
+            if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
+            atomicAdd(L.stats + 4, (unsigned long long)nr);
+        }
     }
 }
 
@@ -665,11 +703,15 @@ cudaError_t dispatch_scheme(const DevParams& P, const DevLaunch& L, cudaStream_t
             *name = "march_kernel<euclid>";
             return launch_variant<kEuclid, 0, SCHEME>(P, L, s, sms);
         case kBumps:
-            if (P.n_bumps <= 8) {
+            if (P.nb_slot <= 4) {
+                *name = "march_kernel<bumps4>";
+                return launch_variant<kBumps, 4, SCHEME>(P, L, s, sms);
+            }
+            if (P.nb_slot <= 8) {
                 *name = "march_kernel<bumps8>";
                 return launch_variant<kBumps, 8, SCHEME>(P, L, s, sms);
             }
-            if (P.n_bumps <= 16) {
+            if (P.nb_slot <= 16) {
                 *name = "march_kernel<bumps16>";
                 return launch_variant<kBumps, 16, SCHEME>(P, L, s, sms);
             }

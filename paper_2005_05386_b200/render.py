@@ -28,7 +28,8 @@ from .config import (CameraSpec, IntegratorConfig, MetricDesc, RunConfig, Scene,
                      fov_radians)
 from .errors import DeviceError, IoError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "librray_cuda.so")
+LIB_PATH = os.environ.get("RRAY_CUDA_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "csrc", "librray_cuda.so")
 _lib = None
 _lib_lock = threading.Lock()
 
