@@ -686,9 +686,25 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
             return set_err(c, RR_ERR_CONFIG, "scene.primitives.kind: unknown primitive kind");
         }
     }
-    c->prog = prog;
-    fill_params(c->prog, sc, *c->P, c->slots);
-    c->masks_dilation = -1.0;
+    // Re-uploading an unchanged scene (the reference's per-row MarchFn calls,
+    // render.cpp:124-128) keeps the compiled program and its culling grid.
+    DevParams* np = new DevParams();
+    std::vector<int> slots;
+    fill_params(prog, sc, *np, slots);
+    DevParams cur = *c->P;
+    cur.h = 0.f;
+    cur.max_steps = cur.scheme = cur.cull = cur.grid = 0;
+    std::memset(cur.grid_lo, 0, sizeof cur.grid_lo);
+    std::memset(cur.grid_inv, 0, sizeof cur.grid_inv);
+    cur.cull_masks = nullptr;
+    const bool same = c->has_scene && std::memcmp(&cur, np, sizeof cur) == 0;
+    if (!same) {
+        *c->P = *np;
+        c->prog = prog;
+        c->slots = slots;
+        c->masks_dilation = -1.0;
+    }
+    delete np;
     c->has_scene = true;
     return RR_OK;
 }
