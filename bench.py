@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG = os.path.join(ROOT, "configs", "c3_bumps16_1080p.json")
+SHADOW_CONFIG = os.path.join(ROOT, "configs", "c3_bumps16_shadows_1080p.json")
 WORKLOAD = "c3_bumps16_1080p"
 METRIC = "geodesic RK4 steps/s (1920x1080, 16 Gaussian bumps, RK4 h=0.05)"
 UNIT = "steps/s"
@@ -53,6 +54,7 @@ def parse_args():
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-shadows", action="store_true")
     p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
     p.add_argument("--opt", action="append", default=[],
                    help="renderer option key=value (rr_options field), e.g. cull_grid=64")
@@ -277,6 +279,37 @@ def run_b200(args, cfg):
     achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
     traffic = load_traffic().get(r.last_kernel)
 
+    # ---- EXTENSION: the same frame with shadow geodesics to 2 point lights
+    #      (BASELINE configs[2] headline target), device-timed the same way
+    shadows = None
+    if world == 1 and not args.no_shadows:
+        from paper_2005_05386_b200.config import load_config
+        scfg = load_config(SHADOW_CONFIG)
+        r.set_config(scfg)
+        scam = r.build_camera(scfg.camera)
+        for _ in range(max(2, args.warmup)):
+            r.render_device(scam, scfg.integrator, w, h, frame, stream=sp)
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            sev[i][0].record(stream)
+            r.render_device(scam, scfg.integrator, w, h, frame, stream=sp)
+            sev[i][1].record(stream)
+        torch.cuda.synchronize()
+        sms = [a.elapsed_time(b) for a, b in sev]
+        sst = r.render_device(scam, scfg.integrator, w, h, frame, stream=sp, with_stats=True)
+        sflop = algorithmic_flops(sst, integ.scheme) + \
+            algorithmic_flops({"integrated_steps": sst["shadow_steps"], "bump_evals": 0}, integ.scheme)
+        shadows = {"workload": "c3_bumps16_shadows_1080p", "lights": len(scfg.scene.lights),
+                   "ms_per_frame": statistics.mean(sms), "fps": 1e3 / statistics.mean(sms),
+                   "primary_steps": sst["total_steps"], "shadow_steps": sst["shadow_steps"],
+                   "steps_per_s": (sst["integrated_steps"] + sst["shadow_steps"]) /
+                                  (statistics.mean(sms) * 1e-3),
+                   "launches_per_frame": sst["kernel_launches"]}
+        r.set_config(cfg)
+
     # ---- e2e through the public API with host buffers (rank 0 only, N=1 path)
     e2e = None
     if world == 1:
@@ -328,6 +361,7 @@ def run_b200(args, cfg):
                          "peak_nominal": NOMINAL_FP32_TFLOPS,
                          "flop_per_launch": flop_launch, "kernel": r.last_kernel},
             "e2e": e2e,
+            "shadows": shadows,
             "gpu_launches": args.steps * (1 if world == 1 else (2 if rank == 0 else 1)),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

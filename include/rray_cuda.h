@@ -128,7 +128,16 @@ typedef struct rr_primitive {
 } rr_primitive;
 
 /* Point light (EXTENSION: shadow geodesics; no reference counterpart,
- * SPEC.md:491,494).  n_lights == 0 selects the reference shading exactly. */
+ * SPEC.md:491,494).  n_lights == 0 selects the reference shading exactly.
+ * With lights, a hit at q with outward unit normal n is shaded
+ *     I = ambient + sum_l intensity_l * lambert_l * lit_l,
+ *     lambert_l = n . (L_l - q) / |L_l - q|   (no shadow ray when <= 0),
+ *     channel = lround(255 * frac(x) * exp(-kappa t) * I)  clamped to [0,255],
+ * where lit_l comes from a shadow geodesic started at q + 1e-4 n with unit
+ * g-speed along L_l - q, marched with the frame's integrator: blocked when a
+ * primitive is hit closer to q than |L_l - q|, lit when it crosses that
+ * sphere, leaves the bounds or exhausts max_steps (oracle/rro.c
+ * shadow_march is the FP64 definition). */
 typedef struct rr_light {
     rr_vec3 position;
     double intensity;
@@ -141,6 +150,7 @@ typedef struct rr_scene_desc {
     const rr_light* lights;
     rr_aabb bounds;                   /* rays terminate once they leave it */
     double fog_density;               /* kappa of exp(-kappa t) (render.cpp:14-25) */
+    double ambient;                   /* EXTENSION: ambient term of the lit shading (n_lights > 0) */
 } rr_scene_desc;
 
 /* ---- integrator (integrate.hpp:30-36) ------------------------------------ */

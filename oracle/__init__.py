@@ -26,6 +26,7 @@ REF_SO = os.path.join(HERE, "_ref", "librray_ref.so")
 
 FLAG_GRAZING, FLAG_WRAP, FLAG_LIMIT = 1, 2, 4
 FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z = 8, 16, 32
+FLAG_SHADOW = 64
 
 
 def _ptr(a: np.ndarray):

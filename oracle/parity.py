@@ -13,7 +13,8 @@ Flags come from oracle.Oracle.render(with_flags=True) (rro.c rro_flags):
 GRAZING = status/prim changes under +-1e-4 rad direction perturbations,
 WRAP = a hit coordinate within 1e-4 of an integer (frac() discontinuity of
 render.cpp:18; WRAP_X/Y/Z name the channel), LIMIT = a hit on the last step
-or an exhausted miss that one more step would turn into a hit.
+or an exhausted miss that one more step would turn into a hit, SHADOW = a
+light's visibility flips under +-1e-4 rad shadow-ray perturbations (EXT).
 """
 from __future__ import annotations
 
@@ -21,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import FLAG_GRAZING, FLAG_LIMIT, FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z
+from . import FLAG_GRAZING, FLAG_LIMIT, FLAG_SHADOW, FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z
 
 ENDPOINT_RTOL = 1e-4
 RGB_TOL = 1
@@ -90,7 +91,7 @@ def compare_rgb(gpu_rgb: np.ndarray, ref_rgb: np.ndarray, flags: np.ndarray | No
     g = gpu_rgb.reshape(-1, 3).astype(np.int32)
     r = ref_rgb.reshape(-1, 3).astype(np.int32)
     flags = np.zeros(len(r), np.uint8) if flags is None else flags
-    keep = (flags & (FLAG_GRAZING | FLAG_LIMIT)) == 0
+    keep = (flags & (FLAG_GRAZING | FLAG_LIMIT | FLAG_SHADOW)) == 0
     diff = np.abs(g - r)
     # a channel whose coordinate sits on an integer wraps frac() (render.cpp:18)
     for ch, bit in enumerate((FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z)):

@@ -456,8 +456,9 @@ void rro_step(const rr_metric_desc* m, const double s[6], double h, int scheme, 
 
 /* ---- scene intersection (src/render/scene.cpp) --------------------------- */
 /* chord_box_entry :15-34; returns 1 and *s when the chord enters the box */
-static int chord_box_entry(V3 a, V3 b, V3 lo, V3 hi, double* s_out) {
+static int chord_box_entry(V3 a, V3 b, V3 lo, V3 hi, double* s_out, int* axis) {
     double smin = 0.0, smax = 1.0;
+    int ax = -1;   /* EXT (normals): axis whose slab bound set smin; -1 = inside start */
     for (int e = 0; e < 3; ++e) {
         const double ae = vcomp(a, e), be = vcomp(b, e);
         const double l = vcomp(lo, e), h = vcomp(hi, e);
@@ -473,17 +474,22 @@ static int chord_box_entry(V3 a, V3 b, V3 lo, V3 hi, double* s_out) {
             s1 = s2;
             s2 = t;
         }
-        if (s1 > smin) smin = s1;
+        if (s1 > smin) {
+            smin = s1;
+            ax = e;
+        }
         if (s2 < smax) smax = s2;
         if (smin > smax) return 0;
     }
     *s_out = smin;
+    *axis = ax;
     return 1;
 }
 
-static int hit_grid(const rr_primitive* g, V3 a, V3 b, double* s_out) {    /* :36-54 */
+static int hit_grid(const rr_primitive* g, V3 a, V3 b, double* s_out, int* axis) { /* :36-54 */
     int have = 0;
     double best = 0.0;
+    int best_ax = -1;
     for (int d = 0; d < 3; ++d) {
         const double ad = vcomp(a, d), bd = vcomp(b, d);
         const double clo = ad < bd ? ad : bd, chi = ad < bd ? bd : ad;  /* std::min / std::max */
@@ -498,13 +504,16 @@ static int hit_grid(const rr_primitive* g, V3 a, V3 b, double* s_out) {    /* :3
             vset(&hi, d, ph < h0 ? ph : h0);   /* std::min(hi, plane + hw) */
             if (vcomp(lo, d) > vcomp(hi, d)) continue;
             double s;
-            if (chord_box_entry(a, b, lo, hi, &s) && (!have || s < best)) {
+            int ax;
+            if (chord_box_entry(a, b, lo, hi, &s, &ax) && (!have || s < best)) {
                 best = s;
+                best_ax = ax;
                 have = 1;
             }
         }
     }
     *s_out = best;
+    *axis = best_ax;
     return have;
 }
 
@@ -542,27 +551,55 @@ static int hit_half_space(const rr_primitive* hs, V3 a, V3 b, double* s_out) { /
     return 1;
 }
 
-static int intersect_segment(const rr_scene_desc* sc, V3 a, V3 b, V3* point, double* s_out,
-                             int* prim) {                                      /* :99-109 */
+/* intersect_segment; `normal` (EXTENSION, may be NULL) receives the outward
+ * unit normal of the hit face: sphere radial, half-space n/|n|, grid slab
+ * entry face; -chord direction for a chord that starts inside (s = 0). */
+static int intersect_segment_n(const rr_scene_desc* sc, V3 a, V3 b, V3* point, double* s_out,
+                               int* prim, V3* normal) {                          /* :99-109 */
     int have = 0;
     double best = 0.0;
+    int best_ax = -1;
     for (int i = 0; i < sc->n_primitives; ++i) {
         const rr_primitive* p = &sc->primitives[i];
         double s;
-        int h;
-        if (p->kind == RR_PRIM_GRID_PLANES) h = hit_grid(p, a, b, &s);
+        int h, ax = -1;
+        if (p->kind == RR_PRIM_GRID_PLANES) h = hit_grid(p, a, b, &s, &ax);
         else if (p->kind == RR_PRIM_SPHERE) h = hit_sphere(p, a, b, &s);
         else h = hit_half_space(p, a, b, &s);
         if (h && (!have || s < best)) {
             const V3 d = vsub(b, a);
             *point = vadd(a, vscale(s, d));
             best = s;
+            best_ax = ax;
             *prim = i;
             have = 1;
         }
     }
     *s_out = best;
+    if (have && normal) {
+        const V3 d = vsub(b, a);
+        const double dl = sqrt(vdot(d, d));
+        const rr_primitive* p = &sc->primitives[*prim];
+        if (best == 0.0 || (p->kind == RR_PRIM_GRID_PLANES && best_ax < 0)) {
+            *normal = vscale(-1.0 / dl, d);
+        } else if (p->kind == RR_PRIM_SPHERE) {
+            const V3 r = vsub(*point, vfrom(p->center));
+            *normal = vscale(1.0 / sqrt(vdot(r, r)), r);
+        } else if (p->kind == RR_PRIM_HALF_SPACE) {
+            const V3 n = vfrom(p->normal);
+            *normal = vscale(1.0 / sqrt(vdot(n, n)), n);
+        } else {
+            V3 n = v3(0.0, 0.0, 0.0);
+            vset(&n, best_ax, vcomp(d, best_ax) > 0.0 ? -1.0 : 1.0);
+            *normal = n;
+        }
+    }
     return have;
+}
+
+static int intersect_segment(const rr_scene_desc* sc, V3 a, V3 b, V3* point, double* s_out,
+                             int* prim) {
+    return intersect_segment_n(sc, a, b, point, s_out, prim, NULL);
 }
 
 int rro_intersect(const rr_scene_desc* sc, const double a[3], const double b[3], double point[3],
@@ -581,8 +618,8 @@ static int aabb_contains(const rr_aabb* bx, V3 p) {                          /* 
 }
 
 /* ---- march (include/rray/render/detail/kernel_impl.hpp:22-94) ------------ */
-static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
-                      const rr_ray_start* ray, rr_pixel_outcome* res) {
+static void march_one_n(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                        const rr_ray_start* ray, rr_pixel_outcome* res, V3* normal) {
     memset(res, 0, sizeof *res);
     res->status = RR_MISS;
     res->prim = -1;
@@ -601,7 +638,7 @@ static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr
         V3 point;
         double hs;
         int prim;
-        if (intersect_segment(sc, s.position, next.position, &point, &hs, &prim)) { /* :63-76 */
+        if (intersect_segment_n(sc, s.position, next.position, &point, &hs, &prim, normal)) { /* :63-76 */
             res->status = RR_HIT;
             res->prim = prim;
             res->point.x = point.x;
@@ -624,6 +661,11 @@ static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr
         res->status = RR_MISS;
         res->steps = in->max_steps;
     }
+}
+
+static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                      const rr_ray_start* ray, rr_pixel_outcome* res) {
+    march_one_n(m, sc, in, ray, res, NULL);
 }
 
 typedef struct {
@@ -715,15 +757,74 @@ void rro_shade_outcome(const rr_pixel_outcome* o, double kappa, uint8_t rgb[3]) 
     }
 }
 
+/* ---- EXTENSION: shadow geodesics + point lights (include/rray_cuda.h) ------
+ * No reference counterpart; this is the FP64 definition the
+ * GPU pass is checked against. */
+static const double kShadowEps = 1e-4;
+
+/* Returns 1 when the light is reached (lit), 0 when blocked. */
+static int shadow_march(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                        V3 q, V3 n, V3 dir, double dist, long long* steps) {
+    const V3 x0 = vadd(q, vscale(kShadowEps, n));
+    S3 g;
+    if (metric_tensor_checked(m, x0, &g)) return 0;
+    State s = {x0, vdiv(dir, sqrt(quad_form(g, dir, dir)))};
+    for (int step = 0; step < in->max_steps; ++step) {
+        double validity;
+        const State next = flow_step(m, s, in->h, in->scheme, &validity);
+        ++*steps;
+        if (!(validity > kSingularDetEps)) return 0;
+        V3 pt;
+        double hs;
+        int prim;
+        if (intersect_segment(sc, s.position, next.position, &pt, &hs, &prim)) {
+            const V3 r = vsub(pt, q);
+            return sqrt(vdot(r, r)) < dist ? 0 : 1;
+        }
+        const V3 rb = vsub(next.position, q);
+        if (sqrt(vdot(rb, rb)) >= dist) return 1;
+        if (!aabb_contains(&sc->bounds, next.position)) return 1;
+        s = next;
+    }
+    return 1;
+}
+
+/* Lit shading of an outcome with hit normal n (lights present). */
+static void shade_lit(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                      const rr_pixel_outcome* o, V3 n, uint8_t rgb[3], long long* shadow_steps) {
+    if (o->status != RR_HIT) {
+        rro_shade_outcome(o, sc->fog_density, rgb);
+        return;
+    }
+    const V3 q = vfrom(o->point);
+    double I = sc->ambient;
+    for (int l = 0; l < sc->n_lights; ++l) {
+        const V3 D = vsub(vfrom(sc->lights[l].position), q);
+        const double dist = sqrt(vdot(D, D));
+        const double lam = vdot(n, D) / dist;
+        if (lam > 0.0 && shadow_march(m, sc, in, q, n, D, dist, shadow_steps))
+            I += sc->lights[l].intensity * lam;
+    }
+    const double atten = exp(-sc->fog_density * o->t);
+    const double pv[3] = {o->point.x, o->point.y, o->point.z};
+    for (int k = 0; k < 3; ++k) {
+        const double frac = pv[k] - floor(pv[k]);
+        long v = lround(255.0 * (frac * atten * I));
+        if (v < 0) v = 0;
+        if (v > 255) v = 255;
+        rgb[k] = (uint8_t)v;
+    }
+}
+
 typedef struct {
     const rr_metric_desc* m; const rr_scene_desc* sc; const rr_camera* cam;
     const rr_integrator* in; int w, h; uint8_t* rgb; rr_pixel_outcome* outcomes;
-    atomic_llong total_steps, errors;
+    atomic_llong total_steps, errors, shadow_steps;
 } RenderArgs;
 
 static void render_rows(void* p, long lo, long hi) {
     RenderArgs* a = (RenderArgs*)p;
-    long long steps = 0, errors = 0;
+    long long steps = 0, errors = 0, sh_steps = 0;
     for (long py = lo; py < hi; ++py) {
         for (int px = 0; px < a->w; ++px) {
             rr_ray_start ray;
@@ -734,16 +835,19 @@ static void render_rows(void* p, long lo, long hi) {
             ray.direction.y = d[1];
             ray.direction.z = d[2];
             rr_pixel_outcome o;
-            march_one(a->m, a->sc, a->in, &ray, &o);
+            V3 n = v3(0.0, 0.0, 0.0);
+            march_one_n(a->m, a->sc, a->in, &ray, &o, &n);
             const size_t i = (size_t)py * a->w + px;
             if (a->outcomes) a->outcomes[i] = o;
             steps += o.steps;
             if (o.status == RR_FAILED) ++errors;
-            rro_shade_outcome(&o, a->sc->fog_density, a->rgb + 3 * i);
+            if (a->sc->n_lights > 0) shade_lit(a->m, a->sc, a->in, &o, n, a->rgb + 3 * i, &sh_steps);
+            else rro_shade_outcome(&o, a->sc->fog_density, a->rgb + 3 * i);
         }
     }
     atomic_fetch_add(&a->total_steps, steps);
     atomic_fetch_add(&a->errors, errors);
+    atomic_fetch_add(&a->shadow_steps, sh_steps);
 }
 
 void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
@@ -754,6 +858,7 @@ void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camer
     a.rgb = rgb; a.outcomes = outcomes;
     atomic_init(&a.total_steps, 0);
     atomic_init(&a.errors, 0);
+    atomic_init(&a.shadow_steps, 0);
     parallel_for(h, 1, threads, render_rows, &a);
     if (stats) {
         memset(stats, 0, sizeof *stats);
@@ -761,6 +866,7 @@ void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camer
         stats->total_steps = atomic_load(&a.total_steps);
         stats->pixel_errors = atomic_load(&a.errors);
         stats->integrated_steps = stats->total_steps;
+        stats->shadow_steps = atomic_load(&a.shadow_steps);
     }
 }
 
@@ -827,6 +933,41 @@ static void flag_rows(void* p, long lo, long hi) {
                         f |= RRO_FLAG_GRAZING;
                         break;
                     }
+                }
+            }
+            /* SHADOW: a light's visibility flips under +-perturb of the shadow
+             * geodesic's initial direction (penumbra edge in FP64 terms). */
+            if (a->sc->n_lights > 0 && o->status == RR_HIT) {
+                rr_ray_start r0;
+                r0.position = cam->position;
+                r0.direction.x = d.x;
+                r0.direction.y = d.y;
+                r0.direction.z = d.z;
+                rr_pixel_outcome oo;
+                V3 n = v3(0.0, 0.0, 0.0);
+                march_one_n(a->m, a->sc, a->in, &r0, &oo, &n);
+                const V3 q = vfrom(o->point);
+                long long dummy = 0;
+                for (int l = 0; l < a->sc->n_lights && !(f & RRO_FLAG_SHADOW); ++l) {
+                    const V3 D = vsub(vfrom(a->sc->lights[l].position), q);
+                    const double dist = sqrt(vdot(D, D));
+                    const double lam = vdot(n, D) / dist;
+                    if (!(lam > 0.0)) continue;
+                    const int base = shadow_march(a->m, a->sc, a->in, q, n, D, dist, &dummy);
+                    const V3 Dh = vscale(1.0 / dist, D);
+                    V3 u1 = vcross(Dh, fabs(Dh.x) < 0.9 ? v3(1, 0, 0) : v3(0, 1, 0));
+                    u1 = vscale(1.0 / sqrt(vdot(u1, u1)), u1);
+                    const V3 u2 = vcross(Dh, u1);
+                    const V3 us[2] = {u1, u2};
+                    for (int k = 0; k < 2 && !(f & RRO_FLAG_SHADOW); ++k)
+                        for (int sg = -1; sg <= 1; sg += 2) {
+                            const double ang = sg * a->perturb;
+                            const V3 Dp = vadd(vscale(cos(ang), Dh), vscale(sin(ang), us[k]));
+                            if (shadow_march(a->m, a->sc, a->in, q, n, vscale(dist, Dp), dist, &dummy) != base) {
+                                f |= RRO_FLAG_SHADOW;
+                                break;
+                            }
+                        }
                 }
             }
             a->flags[i] = f;

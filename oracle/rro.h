@@ -31,7 +31,8 @@ enum {
     RRO_FLAG_LIMIT = 4,     /* outcome flips if the march were one step longer / shorter */
     RRO_FLAG_WRAP_X = 8,    /* per-channel wrap bits: R, G, B individually */
     RRO_FLAG_WRAP_Y = 16,
-    RRO_FLAG_WRAP_Z = 32
+    RRO_FLAG_WRAP_Z = 32,
+    RRO_FLAG_SHADOW = 64    /* EXT: a light's visibility flips under shadow-ray perturbation */
 };
 
 const char* rro_last_error(void);

@@ -80,7 +80,7 @@ class rr_light(C.Structure):
 class rr_scene_desc(C.Structure):
     _fields_ = [("n_primitives", C.c_int32), ("n_lights", C.c_int32),
                 ("primitives", C.POINTER(rr_primitive)), ("lights", C.POINTER(rr_light)),
-                ("bounds", rr_aabb), ("fog_density", C.c_double)]
+                ("bounds", rr_aabb), ("fog_density", C.c_double), ("ambient", C.c_double)]
 
 
 class rr_integrator(C.Structure):
@@ -130,7 +130,7 @@ OUTCOME_DTYPE = np.dtype({
 EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
     "rr_field_node": 72, "rr_diffeo_node": 192, "rr_metric_desc": 56,
-    "rr_primitive": 136, "rr_light": 32, "rr_scene_desc": 80, "rr_integrator": 16,
+    "rr_primitive": 136, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 16,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 72,
     "rr_options": 32,
 }

@@ -150,6 +150,7 @@ class Scene:                          # scene.hpp:45-51 (+ lights EXT)
     bounds: Aabb = field(default_factory=Aabb)
     fog_density: float = 0.05
     lights: List[Light] = field(default_factory=list)
+    ambient: float = 0.2              # EXTENSION: used only when lights are present
 
 
 @dataclass
@@ -390,7 +391,7 @@ def _parse_scene(o, path, allow_ext: bool) -> Scene:              # :277-338
     s = Scene()
     s.bounds = Aabb()
     if o is not None:
-        keys = {"primitives", "bounds", "fog_density"} | ({"lights"} if allow_ext else set())
+        keys = {"primitives", "bounds", "fog_density"} | ({"lights", "ambient"} if allow_ext else set())
         _check_keys(o, path, keys)
         if "bounds" in o:
             s.bounds = _parse_aabb(o["bounds"], path + ".bounds")
@@ -399,6 +400,10 @@ def _parse_scene(o, path, allow_ext: bool) -> Scene:              # :277-338
             _fail(path + ".fog_density", "must be >= 0")
         if allow_ext and "lights" in o:
             s.lights = _parse_lights(o["lights"], path + ".lights")
+        if allow_ext:
+            s.ambient = _get_double_or(o, path, "ambient", 0.2)
+            if not (s.ambient >= 0.0):
+                _fail(path + ".ambient", "must be >= 0")
     prims = o.get("primitives") if o is not None else None
     if o is None or "primitives" not in o:
         s.primitives.append(GridPlanes(1.0, 0.02, Aabb(list(s.bounds.min), list(s.bounds.max))))
@@ -595,6 +600,7 @@ def config_to_dict(cfg: RunConfig, include_ext: bool = True) -> dict:
     if include_ext and cfg.scene.lights:
         scene["lights"] = [{"position": list(l.position), "intensity": l.intensity}
                            for l in cfg.scene.lights]
+        scene["ambient"] = cfg.scene.ambient
     return {
         "metric": _metric_json(cfg.metric),
         "scene": scene,
@@ -720,7 +726,7 @@ class SceneDesc:
         self.desc = abi.rr_scene_desc(
             len(prims), len(lights), self._pr, self._li,
             abi.rr_aabb(abi.rr_vec3.of(scene.bounds.min), abi.rr_vec3.of(scene.bounds.max)),
-            float(scene.fog_density))
+            float(scene.fog_density), float(scene.ambient))
 
 
 def fov_radians(cam: CameraSpec) -> float:

@@ -98,6 +98,15 @@ struct DevLight {
     float intensity;
 };
 
+constexpr float kShadowEps = 1e-4f;   // shadow-ray origin offset along the normal
+
+struct HitRec {           // EXTENSION: primary hit for the shadow pass (32 B)
+    float p[3];
+    float t;
+    float n[3];           // outward unit normal
+    int status;           // 0 miss, 1 hit, 2 failed
+};
+
 struct DevParams {
     int kind;             // Kind
     int n_bumps, n_poly, n_stages;
@@ -105,6 +114,7 @@ struct DevParams {
     int n_spheres, n_halves, n_grids;
     int nb_slot;          // kBumps: bump slots of the kernel variant (4/8/16/32)
     float h, fog;
+    float ambient;        // EXTENSION: lit shading ambient term
     float lo[3], hi[3];   // scene bounds
     int cull;             // 1: cull_masks valid
     int grid;             // culling voxels per axis
@@ -140,8 +150,9 @@ struct DevLaunch {
     const double* rays;           // RAYS: 6 doubles per ray (RayStart)
     uint8_t* outcomes;            // RAYS: 48-byte PixelOutcome records
     unsigned long long n_rays;
-    unsigned* counter;            // unit dispenser (zeroed per launch)
-    unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays
+    unsigned* counter;            // unit dispensers [2] (zeroed per launch)
+    unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays [5] shadow steps
+    HitRec* hits;                 // EXTENSION: hit records (lights present)
 };
 
 } // namespace rr

@@ -90,6 +90,8 @@ struct rr_ctx {
     size_t out_cap = 0;
     uint8_t* d_rgb = nullptr;
     size_t rgb_cap = 0;
+    void* d_hits = nullptr;                  // EXTENSION: hit records of the shadow pass
+    size_t hits_cap = 0;
     const char* last_kernel = "";
 };
 
@@ -296,6 +298,7 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
         P.hi[k] = (float)bhi[k];
     }
     P.fog = (float)sc->fog_density;
+    P.ambient = (float)sc->ambient;
 }
 
 // Culling grid: bit j of cell c is set when bump j's R-sigma ellipsoid
@@ -502,8 +505,15 @@ int check_ready(rr_ctx* c, const rr_integrator* integ) {
     return ensure_masks(c, integ->h);
 }
 
-// Launch one march over `units` warp units; zeroes counter+stats first.
+// Launch one march over `units` warp units; zeroes counters+stats first.
 int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
+    if (c->P->n_lights > 0 && L.mode != rr::kModeRays) {
+        const size_t pixels = L.mode == rr::kModeFrame ? (size_t)L.width * L.height
+                                                       : (size_t)L.n_units * rr::kUnit;
+        const int rc = ensure_device_buffer(c, &c->d_hits, &c->hits_cap, pixels * sizeof(rr::HitRec));
+        if (rc) return rc;
+        L.hits = reinterpret_cast<rr::HitRec*>(c->d_hits);
+    }
     RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * 8, s));
     L.counter = reinterpret_cast<unsigned*>(c->d_aux);
     L.stats = reinterpret_cast<unsigned long long*>(c->d_aux + 8);
@@ -526,7 +536,8 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->integrated_steps = (int64_t)c->h_stats[2];
         st->bump_evals = (int64_t)c->h_stats[3];
         st->rays = (int64_t)c->h_stats[4];
-        st->kernel_launches = 1;
+        st->shadow_steps = (int64_t)c->h_stats[5];
+        st->kernel_launches = c->P->n_lights > 0 ? 2 : 1;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
         st->wall_seconds = now - wall0_s;
@@ -626,6 +637,7 @@ void rr_destroy(rr_ctx* c) {
     if (c->d_rays) cudaFree(c->d_rays);
     if (c->d_out) cudaFree(c->d_out);
     if (c->d_rgb) cudaFree(c->d_rgb);
+    if (c->d_hits) cudaFree(c->d_hits);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -366,17 +366,18 @@ __device__ __forceinline__ bool hit_half_space(const DevHalf& hs, F3 a, F3 d, fl
 
 // Nearest hit over all primitives; ties keep the lower primitive index
 // (scene.cpp:99-109), i.e. the lexicographic minimum of (s, index).
-__device__ __forceinline__ void consider(bool h, float s, int idx, bool& have, float& best,
-                                         int& prim) {
+__device__ __forceinline__ void consider(bool h, float s, int idx, int id, bool& have, float& best,
+                                         int& prim, int& hid) {
     if (h && (!have || s < best || (s == best && idx < prim))) {
         best = s;
         prim = idx;
+        hid = id;   // (kind << 8) | slot, for the hit normal (EXT shading)
         have = true;
     }
 }
 
 __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
-                                          int& prim) {
+                                          int& prim, int& hid) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
     const float qa = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
     const float len = fmaf(sqrt_approx(qa), 1.0001f, 1e-30f);   // conservative chord length
@@ -386,27 +387,100 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
     for (int i = 0; i < kStaticSpheres; ++i)
         if (i < P.n_spheres) {
             const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
-            consider(h, s, P.spheres[i].index, have, s_best, prim);
+            consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
         }
     for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
         const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
-        consider(h, s, P.spheres[i].index, have, s_best, prim);
+        consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
     }
 #pragma unroll
     for (int i = 0; i < kStaticHalves; ++i)
         if (i < P.n_halves) {
             const bool h = hit_half_space(P.halves[i], a, d, s);
-            consider(h, s, P.halves[i].index, have, s_best, prim);
+            consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
         }
     for (int i = kStaticHalves; i < P.n_halves; ++i) {
         const bool h = hit_half_space(P.halves[i], a, d, s);
-        consider(h, s, P.halves[i].index, have, s_best, prim);
+        consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
     }
     for (int i = 0; i < P.n_grids; ++i) {
         const bool h = hit_grid(P.grids[i], a, b, d, s);
-        consider(h, s, P.grids[i].index, have, s_best, prim);
+        consider(h, s, P.grids[i].index, (kPrimGrid << 8) | i, have, s_best, prim, hid);
     }
     return have;
+}
+
+// Outward unit normal of a hit (EXTENSION shading; oracle/rro.c
+// intersect_segment_n): sphere radial, half-space n/|n|, grid entry face,
+// -chord direction for a chord that starts inside (s == 0).
+__device__ F3 hit_normal(const DevParams& P, int hid, float s, F3 a, F3 b, F3 point) {
+    const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
+    const float kind = hid >> 8;
+    const int slot = hid & 0xff;
+    F3 n;
+    int grid_axis = -1;
+    if (s > 0.f && hid >> 8 == kPrimGrid) {
+        // re-run the winning slab entry with axis tracking
+        const DevGrid& g = P.grids[slot];
+        float best = 2.f;
+        const float av[3] = {a.x, a.y, a.z}, bv[3] = {b.x, b.y, b.z}, dv[3] = {d.x, d.y, d.z};
+        for (int dim = 0; dim < 3; ++dim) {
+            const float clo = fminf(av[dim], bv[dim]), chi = fmaxf(av[dim], bv[dim]);
+            const int kmin = (int)ceilf((clo - g.hw) / g.spacing);
+            const int kmax = (int)floorf((chi + g.hw) / g.spacing);
+            for (int k = kmin; k <= kmax; ++k) {
+                float lo[3] = {g.lo[0], g.lo[1], g.lo[2]}, hi[3] = {g.hi[0], g.hi[1], g.hi[2]};
+                const float plane = (float)k * g.spacing;
+                lo[dim] = fmaxf(lo[dim], plane - g.hw);
+                hi[dim] = fminf(hi[dim], plane + g.hw);
+                if (lo[dim] > hi[dim]) continue;
+                float smin = 0.f, smax = 1.f;
+                int ax = -1;
+                bool ok = true;
+                for (int e = 0; e < 3 && ok; ++e) {
+                    if (dv[e] == 0.f) {
+                        ok = !(av[e] < lo[e] || av[e] > hi[e]);
+                        continue;
+                    }
+                    float s1 = (lo[e] - av[e]) / dv[e], s2 = (hi[e] - av[e]) / dv[e];
+                    if (s1 > s2) {
+                        const float t = s1;
+                        s1 = s2;
+                        s2 = t;
+                    }
+                    if (s1 > smin) {
+                        smin = s1;
+                        ax = e;
+                    }
+                    smax = fminf(smax, s2);
+                    ok = !(smin > smax);
+                }
+                if (ok && smin < best) {
+                    best = smin;
+                    grid_axis = ax;
+                }
+            }
+        }
+    }
+    (void)kind;
+    if (s == 0.f || (hid >> 8 == kPrimGrid && grid_axis < 0)) {
+        const float il = rsqrtf(fmaxf(d.x * d.x + d.y * d.y + d.z * d.z, 1e-30f));
+        n = f3(-d.x * il, -d.y * il, -d.z * il);
+    } else if (hid >> 8 == kPrimSphere) {
+        const DevSphere& sp = P.spheres[slot];
+        const F3 r = f3(point.x - sp.c[0], point.y - sp.c[1], point.z - sp.c[2]);
+        const float il = rsqrtf(r.x * r.x + r.y * r.y + r.z * r.z);
+        n = f3(r.x * il, r.y * il, r.z * il);
+    } else if (hid >> 8 == kPrimHalfSpace) {
+        const DevHalf& hs = P.halves[slot];
+        const float il = rsqrtf(hs.n[0] * hs.n[0] + hs.n[1] * hs.n[1] + hs.n[2] * hs.n[2]);
+        n = f3(hs.n[0] * il, hs.n[1] * il, hs.n[2] * il);
+    } else {
+        const float dc = grid_axis == 0 ? d.x : (grid_axis == 1 ? d.y : d.z);
+        const float sg = dc > 0.f ? -1.f : 1.f;
+        n = f3(grid_axis == 0 ? sg : 0.f, grid_axis == 1 ? sg : 0.f, grid_axis == 2 ? sg : 0.f);
+    }
+    return n;
 }
 
 __device__ __forceinline__ bool inside_bounds(const DevParams& P, F3 p) {
@@ -423,11 +497,12 @@ __device__ __forceinline__ uint32_t cell_mask(const DevParams& P, F3 p) {
 }
 
 struct RayResult {
-    int status;    // 0 miss 1 hit 2 failed
+    int status;    // primary: 0 miss 1 hit 2 failed; shadow: 1 lit 0 blocked
     int prim;
     int steps;
     float t;
     F3 point;
+    F3 normal;     // NORMAL passes only
 };
 
 struct LaneCounters {
@@ -435,14 +510,21 @@ struct LaneCounters {
     unsigned bump_evals;
 };
 
+enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2 };
+
 // ---------------------------------------------------------------------------
 // March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
 // until every live lane has terminated; retired lanes keep computing (their
 // results are locked in), exactly as the reference's retired pack lanes.
-template <int KIND, int NB, int SCHEME>
+// PASS == kPassShadow marches a shadow geodesic (EXTENSION, oracle/rro.c
+// shadow_march): lit (1) when it crosses the sphere |x - q| = sqrt(dist2),
+// leaves the bounds or runs out of steps; blocked (0) on a nearer hit or a
+// metric failure.
+template <int KIND, int NB, int SCHEME, int PASS>
 __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
-                                                LaneCounters& cnt) {
-    RayResult res{0, -1, 0, 0.f, f3(0.f, 0.f, 0.f)};
+                                                LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
+                                                float dist2 = 0.f) {
+    RayResult res{PASS == kPassShadow ? 1 : 0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
     bool active = live;
     float cx = 0.f, cy = 0.f, cz = 0.f;       // Kahan compensation of the position sum
     const float h = P.h;
@@ -492,21 +574,34 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
         if (active) {
             cnt.steps_integrated += 1;
             float s = 0.f;
-            int prim = -1;
+            int prim = -1, hid = 0;
             if (KIND == kDiffeo && !(valid > 1e-14f)) {     // kernel_impl.hpp:54-61
-                res.status = 2;
+                res.status = PASS == kPassShadow ? 0 : 2;
                 res.steps = step;
                 active = false;
-            } else if (intersect(P, p, pn, s, prim)) {      // kernel_impl.hpp:63-76
-                res.status = 1;
-                res.prim = prim;
-                res.point = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
-                               fmaf(s, pn.z - p.z, p.z));
-                res.t = ((float)step + s) * h;
+            } else if (intersect(P, p, pn, s, prim, hid)) { // kernel_impl.hpp:63-76
+                const F3 pt = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
+                                 fmaf(s, pn.z - p.z, p.z));
+                if constexpr (PASS == kPassShadow) {
+                    const F3 r = f3(pt.x - q.x, pt.y - q.y, pt.z - q.z);
+                    res.status = (r.x * r.x + r.y * r.y + r.z * r.z) < dist2 ? 0 : 1;
+                } else {
+                    res.status = 1;
+                    res.prim = prim;
+                    res.point = pt;
+                    res.t = ((float)step + s) * h;
+                    if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, pn, pt);
+                }
+                res.steps = step + 1;
+                active = false;
+            } else if (PASS == kPassShadow &&
+                       (pn.x - q.x) * (pn.x - q.x) + (pn.y - q.y) * (pn.y - q.y) +
+                               (pn.z - q.z) * (pn.z - q.z) >= dist2) {
+                res.status = 1;                              // reached the light's sphere
                 res.steps = step + 1;
                 active = false;
             } else if (!inside_bounds(P, pn)) {             // kernel_impl.hpp:77-82
-                res.status = 0;
+                res.status = PASS == kPassShadow ? 1 : 0;
                 res.steps = step + 1;
                 active = false;
             }
@@ -515,14 +610,96 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
         v = vn;
     }
     if (active) {                                            // kernel_impl.hpp:87-91
-        res.status = 0;
+        res.status = PASS == kPassShadow ? 1 : 0;
         res.steps = P.max_steps;
     }
     return res;
 }
 
+// g at x (metric.cpp:12-15 / :40-42), for the shadow ray's unit g-speed.
+__device__ void metric_at(const DevParams& P, F3 x, float g[6], bool& ok) {
+    float gx = 0.f, gy = 0.f, gz = 0.f;   // grad f (graph) ; J (diffeo) below
+    ok = true;
+    g[0] = g[3] = g[5] = 1.f;
+    g[1] = g[2] = g[4] = 0.f;
+    if (P.kind == kBumps || P.kind == kGraphGeneral) {
+        for (int j = 0; j < (P.kind == kBumps ? P.nb_slot : P.n_bumps); ++j) {
+            const DevBump& b = P.bumps[j];
+            const float dx = x.x - b.cx, dy = x.y - b.cy, dz = x.z - b.cz;
+            const float v = ex2(fmaf(dx * b.kx, dx, fmaf(dy * b.ky, dy, fmaf(dz * b.kz, dz, b.la)))) * b.sgn;
+            gx = fmaf(-v * kBeta, dx * b.kx, gx);
+            gy = fmaf(-v * kBeta, dy * b.ky, gy);
+            gz = fmaf(-v * kBeta, dz * b.kz, gz);
+        }
+        float xp[5], yp[5], zp[5];
+        xp[0] = yp[0] = zp[0] = 1.f;
+        for (int k = 1; k < 5; ++k) {
+            xp[k] = xp[k - 1] * x.x;
+            yp[k] = yp[k - 1] * x.y;
+            zp[k] = zp[k - 1] * x.z;
+        }
+        for (int i = 0; i < P.n_poly; ++i) {
+            const DevPoly& t = P.poly[i];
+            if (t.a > 0) gx = fmaf(t.coef * t.a, xp[t.a - 1] * yp[t.b] * zp[t.c], gx);
+            if (t.b > 0) gy = fmaf(t.coef * t.b, xp[t.a] * yp[t.b - 1] * zp[t.c], gy);
+            if (t.c > 0) gz = fmaf(t.coef * t.c, xp[t.a] * yp[t.b] * zp[t.c - 1], gz);
+        }
+        g[0] += gx * gx; g[1] = gx * gy; g[2] = gx * gz;
+        g[3] += gy * gy; g[4] = gy * gz; g[5] += gz * gz;
+    } else if (P.kind == kDiffeo) {
+        float J[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+        float x0 = x.x, x1 = x.y, x2 = x.z;
+        for (int s = 0; s < P.n_stages; ++s) {
+            const DevStage& st = P.stages[s];
+            float Js[9], n0, n1, n2;
+            if (st.kind == kStageAffine) {
+                for (int k = 0; k < 9; ++k) Js[k] = st.v[k];
+                n0 = st.v[0] * x0 + st.v[1] * x1 + st.v[2] * x2 + st.v[9];
+                n1 = st.v[3] * x0 + st.v[4] * x1 + st.v[5] * x2 + st.v[10];
+                n2 = st.v[6] * x0 + st.v[7] * x1 + st.v[8] * x2 + st.v[11];
+            } else if (st.kind == kStageTwist) {
+                float sn, cs;
+                sincosf(x2, &sn, &cs);
+                Js[0] = cs; Js[1] = -sn; Js[2] = -(x0 * sn) - x1 * cs;
+                Js[3] = sn; Js[4] = cs; Js[5] = x0 * cs - x1 * sn;
+                Js[6] = 0.f; Js[7] = 0.f; Js[8] = 1.f;
+                n0 = x0 * cs - x1 * sn;
+                n1 = x0 * sn + x1 * cs;
+                n2 = x2;
+            } else {
+                const float* b = st.v;
+                const float ux = (x0 - b[0]) * b[3], uy = (x1 - b[1]) * b[4], uz = (x2 - b[2]) * b[5];
+                const float e = b[6] * __expf(-0.5f * (ux * ux + uy * uy + uz * uz));
+                const float fg[3] = {-e * ux * b[3], -e * uy * b[4], -e * uz * b[5]};
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) Js[3 * i + j] = (i == j ? 1.f : 0.f) + b[7 + i] * fg[j];
+                n0 = fmaf(e, b[7], x0);
+                n1 = fmaf(e, b[8], x1);
+                n2 = fmaf(e, b[9], x2);
+            }
+            float R[9];
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j)
+                    R[3 * i + j] = Js[3 * i] * J[j] + Js[3 * i + 1] * J[3 + j] + Js[3 * i + 2] * J[6 + j];
+            for (int k = 0; k < 9; ++k) J[k] = R[k];
+            x0 = n0; x1 = n1; x2 = n2;
+        }
+        const float d = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+                        J[2] * (J[3] * J[7] - J[4] * J[6]);
+        ok = fabsf(d) > 1e-14f;
+        g[0] = J[0] * J[0] + J[3] * J[3] + J[6] * J[6];
+        g[1] = J[0] * J[1] + J[3] * J[4] + J[6] * J[7];
+        g[2] = J[0] * J[2] + J[3] * J[5] + J[6] * J[8];
+        g[3] = J[1] * J[1] + J[4] * J[4] + J[7] * J[7];
+        g[4] = J[1] * J[2] + J[4] * J[5] + J[7] * J[8];
+        g[5] = J[2] * J[2] + J[5] * J[5] + J[8] * J[8];
+    }
+}
+
 // Pseudo-colour + fog (render.cpp:14-25); failures magenta (render.cpp:39).
-__device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, uint8_t* rgb) {
+// `light` scales the colour (EXTENSION lit shading; 1 = reference shading).
+__device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, uint8_t* rgb,
+                                      float light = 1.f) {
     if (r.status == 2) {
         rgb[0] = 255; rgb[1] = 0; rgb[2] = 255;
         return;
@@ -536,7 +713,7 @@ __device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, ui
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const float frac = pv[k] - floorf(pv[k]);
-        long v = lroundf(255.f * (frac * atten));
+        long v = lroundf(255.f * (frac * atten * light));
         v = v < 0 ? 0 : (v > 255 ? 255 : v);
         rgb[k] = (uint8_t)v;
     }
@@ -557,7 +734,7 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
     dir = f3((float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
 }
 
-template <int KIND, int NB, int SCHEME>
+template <int KIND, int NB, int SCHEME, int PASS>
 __global__ void __launch_bounds__(kThreads, RR_MIN_BLOCKS)
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
@@ -570,7 +747,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
         bool live;
         F3 pos, dir;
         int px = 0, py = 0, lx = 0, ly = 0;
-        unsigned long long ray_index = 0, tile_k = 0;
+        unsigned long long ray_index = 0, tile_k = 0, pix = 0;
         if (L.mode == kModeRays) {
             ray_index = (unsigned long long)unit * kUnit + lane;
             live = ray_index < L.n_rays;
@@ -592,52 +769,104 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             px = tx * L.tile_w + lx;
             py = ty * L.tile_h + ly;
             live = px < L.width && py < L.height;
-            if (live) raygen(L.cam, px, py, L.width, L.height, pos, dir);
-            else pos = dir = f3(0.f, 0.f, 0.f);
+            // output index: row-major frame, or tile-major shard buffer
+            pix = L.mode == kModeFrame ? (unsigned long long)py * L.width + px
+                                       : tile_k * L.tile_w * L.tile_h + (unsigned long long)ly * L.tile_w + lx;
+            if (PASS != kPassShadow) {
+                if (live) raygen(L.cam, px, py, L.width, L.height, pos, dir);
+                else pos = dir = f3(0.f, 0.f, 0.f);
+            }
         }
 
         LaneCounters cnt{0u, 0u};
-        const RayResult r = march_unit<KIND, NB, SCHEME>(P, live, pos, dir, cnt);
-
-        if (live) {
-            if (L.mode == kModeRays) {
-                uint8_t* o = L.outcomes + 48 * ray_index;      // render::PixelOutcome
-                o[0] = (uint8_t)r.status;
-                *reinterpret_cast<int*>(o + 4) = r.status == 1 ? r.prim : -1;
-                double* pt = reinterpret_cast<double*>(o + 8);
-                pt[0] = r.status == 1 ? (double)r.point.x : 0.0;
-                pt[1] = r.status == 1 ? (double)r.point.y : 0.0;
-                pt[2] = r.status == 1 ? (double)r.point.z : 0.0;
-                *reinterpret_cast<double*>(o + 32) = r.status == 1 ? (double)r.t : 0.0;
-                *reinterpret_cast<int*>(o + 40) = r.steps;
-            } else {
-                uint8_t* dst;
-                if (L.mode == kModeFrame) {
-                    dst = L.rgb + 3 * ((size_t)py * L.width + px);
-                } else {
-                    dst = L.rgb + 3 * ((size_t)tile_k * L.tile_w * L.tile_h +
-                                       (size_t)ly * L.tile_w + lx);
+        unsigned ref_steps = 0, errs = 0, shadow_steps = 0;
+        if constexpr (PASS == kPassShadow) {
+            // ---- EXTENSION: shadow geodesics for this unit's hits, light by light
+            HitRec hr{};
+            if (live) hr = L.hits[pix];
+            const bool hit = live && (hr.status == 1);
+            const F3 q = f3(hr.p[0], hr.p[1], hr.p[2]);
+            const F3 n = f3(hr.n[0], hr.n[1], hr.n[2]);
+            float light = P.ambient;
+            for (int l = 0; l < P.n_lights; ++l) {
+                const DevLight& Lt = P.lights[l];
+                const F3 D = f3(Lt.pos[0] - q.x, Lt.pos[1] - q.y, Lt.pos[2] - q.z);
+                const float dist2 = D.x * D.x + D.y * D.y + D.z * D.z;
+                const float lam = (n.x * D.x + n.y * D.y + n.z * D.z) * rsqrtf(dist2);
+                bool want = hit && lam > 0.f;
+                F3 x0 = f3(0.f, 0.f, 0.f), v0 = f3(0.f, 0.f, 0.f);
+                if (want) {
+                    x0 = f3(fmaf(kShadowEps, n.x, q.x), fmaf(kShadowEps, n.y, q.y),
+                            fmaf(kShadowEps, n.z, q.z));
+                    float g[6];
+                    bool ok;
+                    metric_at(P, x0, g, ok);
+                    const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
+                                     2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
+                    const float inv = rsqrtf(n2);
+                    v0 = f3(D.x * inv, D.y * inv, D.z * inv);
+                    want = ok;
                 }
-                shade(P, r, dst);
+                const RayResult sr = march_unit<KIND, NB, SCHEME, kPassShadow>(P, want, x0, v0, cnt, q, dist2);
+                if (want && sr.status == 1) light = fmaf(Lt.intensity, lam, light);
             }
-        } else if (L.mode == kModeTiles) {
-            // zero the padding of partial edge tiles
-            uint8_t* dst = L.rgb + 3 * ((size_t)tile_k * L.tile_w * L.tile_h +
-                                        (size_t)ly * L.tile_w + lx);
+            shadow_steps = cnt.steps_integrated;
+            if (live) {
+                RayResult r{hr.status, 0, 0, hr.t, q, n};
+                shade(P, r, L.rgb + 3 * pix, light);
+            }
+        } else {
+            const RayResult r = march_unit<KIND, NB, SCHEME, PASS>(P, live, pos, dir, cnt);
+            ref_steps = live ? (unsigned)r.steps : 0u;
+            errs = (live && r.status == 2) ? 1u : 0u;
+            if (live) {
+                if (L.mode == kModeRays) {
+                    uint8_t* o = L.outcomes + 48 * ray_index;      // render::PixelOutcome
+                    o[0] = (uint8_t)r.status;
+                    *reinterpret_cast<int*>(o + 4) = r.status == 1 ? r.prim : -1;
+                    double* pt = reinterpret_cast<double*>(o + 8);
+                    pt[0] = r.status == 1 ? (double)r.point.x : 0.0;
+                    pt[1] = r.status == 1 ? (double)r.point.y : 0.0;
+                    pt[2] = r.status == 1 ? (double)r.point.z : 0.0;
+                    *reinterpret_cast<double*>(o + 32) = r.status == 1 ? (double)r.t : 0.0;
+                    *reinterpret_cast<int*>(o + 40) = r.steps;
+                } else if constexpr (PASS == kPassHits) {
+                    HitRec hr;
+                    hr.p[0] = r.point.x;
+                    hr.p[1] = r.point.y;
+                    hr.p[2] = r.point.z;
+                    hr.t = r.t;
+                    hr.n[0] = r.normal.x;
+                    hr.n[1] = r.normal.y;
+                    hr.n[2] = r.normal.z;
+                    hr.status = r.status;
+                    L.hits[pix] = hr;
+                } else {
+                    shade(P, r, L.rgb + 3 * pix);
+                }
+            } else if (L.mode == kModeTiles && PASS == kPassShade) {
+                uint8_t* dst = L.rgb + 3 * pix;                    // zero partial-tile padding
+                dst[0] = dst[1] = dst[2] = 0;
+            }
+        }
+        if (PASS == kPassShadow && !live && L.mode == kModeTiles) {
+            uint8_t* dst = L.rgb + 3 * pix;
             dst[0] = dst[1] = dst[2] = 0;
         }
         // per-unit counters: one REDUX per counter, one 64-bit atomic per warp
-        const unsigned steps = __reduce_add_sync(kFull, live ? (unsigned)r.steps : 0u);
-        const unsigned errs = __reduce_add_sync(kFull, (live && r.status == 2) ? 1u : 0u);
-        const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
+        const unsigned steps = __reduce_add_sync(kFull, ref_steps);
+        const unsigned nerr = __reduce_add_sync(kFull, errs);
+        const unsigned integ = __reduce_add_sync(kFull, PASS == kPassShadow ? 0u : cnt.steps_integrated);
         const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
-        const unsigned nr = __reduce_add_sync(kFull, live ? 1u : 0u);
+        const unsigned nr = __reduce_add_sync(kFull, (live && PASS != kPassShadow) ? 1u : 0u);
+        const unsigned shs = __reduce_add_sync(kFull, shadow_steps);
         if (lane == 0) {
-            atomicAdd(L.stats + 0, (unsigned long long)steps);
-            if (errs) atomicAdd(L.stats + 1, (unsigned long long)errs);
-            atomicAdd(L.stats + 2, (unsigned long long)integ);
+            if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
+            if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
+            if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
             if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
-            atomicAdd(L.stats + 4, (unsigned long long)nr);
+            if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
+            if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
         }
     }
 }
@@ -674,25 +903,38 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
     if (s == 12345.678f) out[0] = s;   // keep the chains alive
 }
 
-template <int KIND, int NB, int SCHEME>
+template <int KIND, int NB, int SCHEME, int PASS>
 int occupancy_of() {
     static int occ = [] {
         int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME, PASS>, kThreads, 0);
         return n > 0 ? n : 1;
     }();
     return occ;
 }
 
-template <int KIND, int NB, int SCHEME>
-cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
+template <int KIND, int NB, int SCHEME, int PASS>
+cudaError_t launch_pass(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
     const unsigned warps_needed = L.n_units;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME>());
+    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME, PASS>());
     const unsigned max_useful = (warps_needed + 3) / 4;
     if (blocks > max_useful) blocks = max_useful;
     if (blocks == 0) blocks = 1;
-    march_kernel<KIND, NB, SCHEME><<<blocks, kThreads, 0, s>>>(P, L);
+    march_kernel<KIND, NB, SCHEME, PASS><<<blocks, kThreads, 0, s>>>(P, L);
     return cudaGetLastError();
+}
+
+// Without lights: one fused launch.  With lights (EXTENSION): a hit-record
+// pass and a shadow+shade pass over the same units (each with its own unit
+// counter: L.counter[0] and L.counter[1]).
+template <int KIND, int NB, int SCHEME>
+cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
+    if (P.n_lights == 0 || L.mode == kModeRays) return launch_pass<KIND, NB, SCHEME, kPassShade>(P, L, s, num_sms);
+    cudaError_t e = launch_pass<KIND, NB, SCHEME, kPassHits>(P, L, s, num_sms);
+    if (e != cudaSuccess) return e;
+    DevLaunch L2 = L;
+    L2.counter = L.counter + 1;
+    return launch_pass<KIND, NB, SCHEME, kPassShadow>(P, L2, s, num_sms);
 }
 
 template <int SCHEME>
