@@ -115,7 +115,7 @@ class rr_stats(C.Structure):
 class rr_options(C.Structure):
     _fields_ = [("cull", C.c_int32), ("cull_grid", C.c_int32),
                 ("cull_radius_sigma", C.c_double), ("block_x", C.c_int32),
-                ("block_y", C.c_int32), ("persistent", C.c_int32), ("pad_", C.c_int32)]
+                ("block_y", C.c_int32), ("persistent", C.c_int32), ("skip", C.c_int32)]
 
 
 RAY_DTYPE = np.dtype([("position", "<f8", (3,)), ("direction", "<f8", (3,))])

@@ -121,6 +121,9 @@ struct DevParams {
     float grid_lo[3], grid_inv[3];
     uint32_t all_mask;    // bits of every live bump (slot bits for kBumps)
     const uint32_t* cull_masks;   // grid^3 bump masks (device)
+    const uint8_t* skip_k;        // grid^3 Chebyshev distance (cells) to the nearest non-empty cell
+    int skip;                     // 1: empty-space skipping enabled
+    float cell_min;               // smallest culling-cell edge (world units)
     DevBump bumps[kMaxBumps];
     DevPoly poly[kMaxPoly];
     DevStage stages[kMaxStages];

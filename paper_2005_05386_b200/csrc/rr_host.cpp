@@ -59,6 +59,7 @@ struct Options {
         o.block_x = 32;
         o.block_y = 32;
         o.persistent = 1;
+        o.skip = 1;
     }
 };
 
@@ -78,6 +79,7 @@ struct rr_ctx {
     DevParams* P = nullptr;                  // host copy of the kernel parameter block
     // culling grid (built lazily for the integrator step length in use)
     uint32_t* d_masks = nullptr;
+    uint8_t* d_skip = nullptr;               // Chebyshev distance grid for empty-space skipping
     double masks_dilation = -1.0;
     int masks_grid = 0;
     double masks_radius = 0.0;
@@ -339,6 +341,37 @@ std::vector<uint32_t> build_masks(const Compiled& c, const std::vector<int>& slo
     return masks;
 }
 
+// Chebyshev (26-neighbourhood) distance in cells from every cell to the
+// nearest cell with a non-empty bump mask, capped at 255 (multi-source BFS).
+std::vector<uint8_t> chebyshev_distance(const std::vector<uint32_t>& masks, int G) {
+    std::vector<uint8_t> k(masks.size(), 255);
+    std::vector<int> frontier;
+    for (size_t i = 0; i < masks.size(); ++i)
+        if (masks[i]) {
+            k[i] = 0;
+            frontier.push_back((int)i);
+        }
+    for (int d = 1; d < 255 && !frontier.empty(); ++d) {
+        std::vector<int> next;
+        for (int i : frontier) {
+            const int x = i % G, y = (i / G) % G, z = i / (G * G);
+            for (int dz = -1; dz <= 1; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int X = x + dx, Y = y + dy, Z = z + dz;
+                        if (X < 0 || Y < 0 || Z < 0 || X >= G || Y >= G || Z >= G) continue;
+                        const int j = (Z * G + Y) * G + X;
+                        if (k[j] == 255) {
+                            k[j] = (uint8_t)d;
+                            next.push_back(j);
+                        }
+                    }
+        }
+        frontier.swap(next);
+    }
+    return k;
+}
+
 int ensure_masks(rr_ctx* c, double h) {
     DevParams& P = *c->P;
     if (P.kind != rr::kBumps || !c->opt.o.cull) {
@@ -350,6 +383,7 @@ int ensure_masks(rr_ctx* c, double h) {
     const double dil = 1.5 * h;
     if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil) {
         P.cull = 1;
+        P.skip = c->opt.o.skip ? 1 : 0;
         return RR_OK;
     }
     const std::vector<uint32_t> m = build_masks(c->prog, c->slots, P, G, R, dil);
@@ -360,6 +394,13 @@ int ensure_masks(rr_ctx* c, double h) {
     if (!c->d_masks) RR_CUDA(c, cudaMalloc(&c->d_masks, m.size() * sizeof(uint32_t)));
     RR_CUDA(c, cudaMemcpyAsync(c->d_masks, m.data(), m.size() * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, c->stream));
+    const std::vector<uint8_t> k = chebyshev_distance(m, G);
+    if (c->d_skip && c->masks_grid != G) {
+        cudaFree(c->d_skip);
+        c->d_skip = nullptr;
+    }
+    if (!c->d_skip) RR_CUDA(c, cudaMalloc(&c->d_skip, k.size()));
+    RR_CUDA(c, cudaMemcpyAsync(c->d_skip, k.data(), k.size(), cudaMemcpyHostToDevice, c->stream));
     RR_CUDA(c, cudaStreamSynchronize(c->stream));
     c->masks_grid = G;
     c->masks_radius = R;
@@ -367,6 +408,10 @@ int ensure_masks(rr_ctx* c, double h) {
     P.cull = 1;
     P.grid = G;
     P.cull_masks = c->d_masks;
+    P.skip_k = c->d_skip;
+    P.skip = c->opt.o.skip ? 1 : 0;
+    P.cell_min = (float)std::min({((double)P.hi[0] - P.lo[0]) / G, ((double)P.hi[1] - P.lo[1]) / G,
+                                  ((double)P.hi[2] - P.lo[2]) / G});
     for (int k = 0; k < 3; ++k) {
         P.grid_lo[k] = P.lo[k];
         P.grid_inv[k] = (float)(G / ((double)P.hi[k] - P.lo[k]));
@@ -632,6 +677,7 @@ void rr_destroy(rr_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->d_masks) cudaFree(c->d_masks);
+    if (c->d_skip) cudaFree(c->d_skip);
     if (c->d_aux) cudaFree(c->d_aux);
     if (c->h_stats) cudaFreeHost(c->h_stats);
     if (c->d_rays) cudaFree(c->d_rays);

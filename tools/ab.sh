@@ -25,7 +25,8 @@ import json, sys
 name = sys.argv[1]
 try:
     d = json.loads(open(f"gpurun_out/ab_{name}.log").read().strip().splitlines()[-1])
-    print(f"{name:28s} ms/frame {d['ms_per_step']:8.3f} fps {d['fps']:7.2f} frac {d['roofline']['frac']:.3f} neff {d['n_eff_bumps']:.2f} clk {d['clocks']['sm_mhz']}")
+    sh = d.get("shadows") or {}
+    print(f"{name:28s} ms/frame {d['ms_per_step']:8.3f} fps {d['fps']:7.2f} frac {d['roofline']['frac']:.3f} neff {d['n_eff_bumps']:.2f} clk {d['clocks']['sm_mhz']} | shadows ms {sh.get('ms_per_frame', 0):.3f} fps {sh.get('fps', 0):.1f}")
 except Exception as e:
     print(name, "FAILED", e)
 PY
