@@ -21,6 +21,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 128;   // 4 warps per CTA
+#ifndef RR_GROUP_TESTS
+#define RR_GROUP_TESTS 1
+#endif
 #ifndef RR_MIN_BLOCKS
 #define RR_MIN_BLOCKS 7   // <= 72 registers: 7 CTAs = 28 warps per SM (measured best)
 #endif
@@ -59,21 +62,29 @@ template <int NB>
 __device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p, F3 y) {
     float Gx = 0.f, Gy = 0.f, Gz = 0.f, Q1 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-        if (um & (1u << j)) {
-            const DevBump& b = P.bumps[j];
-            const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
-            const float gx = dx * b.kx, gy = dy * b.ky, gz = dz * b.kz;
-            const float q = fmaf(dx, gx, fmaf(dy, gy, fmaf(dz, gz, b.la)));
-            const float v = ex2(q) * b.sgn;
-            Gx = fmaf(v, gx, Gx);
-            Gy = fmaf(v, gy, Gy);
-            Gz = fmaf(v, gz, Gz);
-            const float t = fmaf(y.x, gx, fmaf(y.y, gy, y.z * gz));
-            Q1 = fmaf(v * t, t, Q1);
-            Sx = fmaf(v, b.kx, Sx);
-            Sy = fmaf(v, b.ky, Sy);
-            Sz = fmaf(v, b.kz, Sz);
+    for (int g = 0; g < NB; g += 4) {
+#if RR_GROUP_TESTS
+        // slots are sorted by centre x on the host, so a ray's active bumps
+        // cluster and whole groups of 4 are skipped with one test
+        if (!((um >> g) & 0xFu)) continue;
+#endif
+#pragma unroll
+        for (int j = g; j < g + 4; ++j) {
+            if (um & (1u << j)) {
+                const DevBump& b = P.bumps[j];
+                const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
+                const float gx = dx * b.kx, gy = dy * b.ky, gz = dz * b.kz;
+                const float q = fmaf(dx, gx, fmaf(dy, gy, fmaf(dz, gz, b.la)));
+                const float v = ex2(q) * b.sgn;
+                Gx = fmaf(v, gx, Gx);
+                Gy = fmaf(v, gy, Gy);
+                Gz = fmaf(v, gz, Gz);
+                const float t = fmaf(y.x, gx, fmaf(y.y, gy, y.z * gz));
+                Q1 = fmaf(v * t, t, Q1);
+                Sx = fmaf(v, b.kx, Sx);
+                Sy = fmaf(v, b.ky, Sy);
+                Sz = fmaf(v, b.kz, Sz);
+            }
         }
     }
     // G = beta G';  Q = beta^2 Q1 - beta (Y . S');  a = (Q / (1 + |G|^2)) G
