@@ -114,7 +114,8 @@ typedef struct rr_metric_desc {
 } rr_metric_desc;
 
 /* ---- scene (scene.hpp:18-51) --------------------------------------------- */
-enum { RR_PRIM_GRID_PLANES = 0, RR_PRIM_SPHERE = 1, RR_PRIM_HALF_SPACE = 2 };
+enum { RR_PRIM_GRID_PLANES = 0, RR_PRIM_SPHERE = 1, RR_PRIM_HALF_SPACE = 2,
+       RR_PRIM_MESH = 3 /* EXTENSION: triangle mesh (SPEC.md:491 lists it as a non-goal) */ };
 
 typedef struct rr_primitive {
     int32_t kind;                     /* RR_PRIM_* */
@@ -125,6 +126,13 @@ typedef struct rr_primitive {
     double radius;
     rr_vec3 normal;                   /* HALF_SPACE: region dot(normal,p) <= offset (scene.hpp:35-41) */
     double offset;
+    /* MESH (EXTENSION): a triangle soup, hit like the other primitives by
+     * the chord [a, b] of each step (nearest s in [0, 1]; ties between
+     * triangles keep the lower triangle index); no inside-start rule (a
+     * surface, not a solid).  The library builds and owns its BVH. */
+    int32_t n_vertices, n_triangles;
+    const double* vertices;           /* n_vertices * 3 */
+    const int32_t* triangles;         /* n_triangles * 3 vertex indices */
 } rr_primitive;
 
 /* Point light (EXTENSION: shadow geodesics; no reference counterpart,

@@ -60,8 +60,12 @@ class Oracle:
         lib.rro_flags.argtypes = [C.POINTER(abi.rr_metric_desc), C.POINTER(abi.rr_scene_desc),
                                   C.POINTER(abi.rr_camera), C.POINTER(abi.rr_integrator),
                                   C.c_int, C.c_int, P, C.c_double, C.c_double, P, C.c_int]
+        lib.rro_set_mesh_bruteforce.argtypes = [C.c_int]
         self.lib = lib
         self.threads = os.cpu_count() or 1
+
+    def set_mesh_bruteforce(self, on: bool):
+        self.lib.rro_set_mesh_bruteforce(1 if on else 0)
 
     @staticmethod
     def _d3(v):

@@ -13,6 +13,7 @@
 #include <pthread.h>
 #include <stdatomic.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 static _Thread_local char g_err[256];
@@ -551,6 +552,223 @@ static int hit_half_space(const rr_primitive* hs, V3 a, V3 b, double* s_out) { /
     return 1;
 }
 
+/* ---- EXTENSION: triangle meshes (rr_primitive kind RR_PRIM_MESH) ---------
+ * FP64 definition the GPU BVH traversal is checked against: the chord [a, b]
+ * hits the nearest triangle (Moller-Trumbore, s in [0, 1], barycentrics
+ * inclusive); equal s keeps the lower triangle index.  The oracle's own BVH
+ * (median split) only prunes: tests/test_oracle_mesh.py checks it against a
+ * brute-force scan. */
+typedef struct { double lo[3], hi[3]; int left, right, first, count; } MNode;
+typedef struct MeshBVH_ {
+    const double* verts; const int32_t* tris; int n_tris, n_verts;
+    uint64_t fingerprint;          /* content hash: arrays may be reallocated at the same address */
+    MNode* nodes; int n_nodes; int* order;
+} MeshBVH;
+
+static uint64_t mesh_fingerprint(const rr_primitive* p) {
+    uint64_t h = 1469598103934665603ULL;
+    const unsigned char* b = (const unsigned char*)p->vertices;
+    for (size_t i = 0; i < (size_t)p->n_vertices * 3 * sizeof(double); ++i) h = (h ^ b[i]) * 1099511628211ULL;
+    b = (const unsigned char*)p->triangles;
+    for (size_t i = 0; i < (size_t)p->n_triangles * 3 * sizeof(int32_t); ++i) h = (h ^ b[i]) * 1099511628211ULL;
+    return h;
+}
+
+static pthread_mutex_t g_mesh_mu = PTHREAD_MUTEX_INITIALIZER;
+static MeshBVH g_mesh_cache[16];
+static int g_mesh_n = 0;
+static int g_mesh_brute = 0;   /* 1: scan every triangle (test hook) */
+/* Meshes of the scene of the current entry-point call, resolved once per call
+ * (fingerprinting 100k-triangle arrays per chord would dominate the march). */
+static const rr_primitive* g_prep_prim[16];
+static const struct MeshBVH_* g_prep_bvh[16];
+static int g_prep_n = 0;
+
+void rro_set_mesh_bruteforce(int on) { g_mesh_brute = on; }
+
+static V3 mvert(const MeshBVH* m, int t, int k) {
+    return vload(m->verts + 3 * m->tris[3 * t + k]);
+}
+
+static int mesh_build_rec(MeshBVH* m, int first, int count) {
+    const int idx = m->n_nodes++;
+    MNode* nd = &m->nodes[idx];
+    for (int k = 0; k < 3; ++k) { nd->lo[k] = 1e300; nd->hi[k] = -1e300; }
+    double clo[3] = {1e300, 1e300, 1e300}, chi[3] = {-1e300, -1e300, -1e300};
+    for (int i = first; i < first + count; ++i) {
+        const int t = m->order[i];
+        double c[3] = {0, 0, 0};
+        for (int v = 0; v < 3; ++v) {
+            const V3 p = mvert(m, t, v);
+            const double pv[3] = {p.x, p.y, p.z};
+            for (int k = 0; k < 3; ++k) {
+                if (pv[k] < nd->lo[k]) nd->lo[k] = pv[k];
+                if (pv[k] > nd->hi[k]) nd->hi[k] = pv[k];
+                c[k] += pv[k] / 3.0;
+            }
+        }
+        for (int k = 0; k < 3; ++k) {
+            if (c[k] < clo[k]) clo[k] = c[k];
+            if (c[k] > chi[k]) chi[k] = c[k];
+        }
+    }
+    if (count <= 8) {
+        nd->left = nd->right = -1;
+        nd->first = first;
+        nd->count = count;
+        return idx;
+    }
+    int ax = 0;
+    for (int k = 1; k < 3; ++k)
+        if (chi[k] - clo[k] > chi[ax] - clo[ax]) ax = k;
+    const double mid = 0.5 * (clo[ax] + chi[ax]);
+    int i = first, j = first + count - 1;
+    while (i <= j) {
+        const int t = m->order[i];
+        const double c = (mvert(m, t, 0).x * (ax == 0) + mvert(m, t, 0).y * (ax == 1) + mvert(m, t, 0).z * (ax == 2) +
+                          mvert(m, t, 1).x * (ax == 0) + mvert(m, t, 1).y * (ax == 1) + mvert(m, t, 1).z * (ax == 2) +
+                          mvert(m, t, 2).x * (ax == 0) + mvert(m, t, 2).y * (ax == 1) + mvert(m, t, 2).z * (ax == 2)) / 3.0;
+        if (c < mid) ++i;
+        else {
+            const int tmp = m->order[i];
+            m->order[i] = m->order[j];
+            m->order[j] = tmp;
+            --j;
+        }
+    }
+    int nl = i - first;
+    if (nl == 0 || nl == count) nl = count / 2;   /* degenerate split */
+    nd->first = nd->count = 0;
+    const int l = mesh_build_rec(m, first, nl);
+    const int r = mesh_build_rec(m, first + nl, count - nl);
+    m->nodes[idx].left = l;
+    m->nodes[idx].right = r;
+    return idx;
+}
+
+static const MeshBVH* mesh_bvh_resolve(const rr_primitive* p);
+
+static const MeshBVH* mesh_bvh(const rr_primitive* p) {
+    for (int i = 0; i < g_prep_n; ++i)
+        if (g_prep_prim[i] == p) return (const MeshBVH*)g_prep_bvh[i];
+    return mesh_bvh_resolve(p);
+}
+
+/* Entry points call this once: validate/build every mesh's BVH. */
+static void prepare_meshes(const rr_scene_desc* sc) {
+    g_prep_n = 0;
+    for (int i = 0; i < sc->n_primitives && g_prep_n < 16; ++i)
+        if (sc->primitives[i].kind == RR_PRIM_MESH) {
+            g_prep_prim[g_prep_n] = &sc->primitives[i];
+            g_prep_bvh[g_prep_n] = (const struct MeshBVH_*)mesh_bvh_resolve(&sc->primitives[i]);
+            ++g_prep_n;
+        }
+}
+
+static const MeshBVH* mesh_bvh_resolve(const rr_primitive* p) {
+    pthread_mutex_lock(&g_mesh_mu);
+    for (int i = 0; i < g_mesh_n; ++i)
+        if (g_mesh_cache[i].verts == p->vertices && g_mesh_cache[i].tris == p->triangles &&
+            g_mesh_cache[i].n_tris == p->n_triangles && g_mesh_cache[i].n_verts == p->n_vertices) {
+            /* same address: confirm the content (cheap relative to a march) */
+            if (g_mesh_cache[i].fingerprint == mesh_fingerprint(p)) {
+                pthread_mutex_unlock(&g_mesh_mu);
+                return &g_mesh_cache[i];
+            }
+        }
+    MeshBVH* m;
+    if (g_mesh_n < 16) {
+        m = &g_mesh_cache[g_mesh_n++];
+    } else {   /* evict the oldest entry */
+        free(g_mesh_cache[0].order);
+        free(g_mesh_cache[0].nodes);
+        memmove(&g_mesh_cache[0], &g_mesh_cache[1], 15 * sizeof(MeshBVH));
+        m = &g_mesh_cache[15];
+    }
+    m->fingerprint = mesh_fingerprint(p);
+    m->verts = p->vertices;
+    m->tris = p->triangles;
+    m->n_tris = p->n_triangles;
+    m->n_verts = p->n_vertices;
+    m->order = (int*)malloc(sizeof(int) * (size_t)(p->n_triangles > 0 ? p->n_triangles : 1));
+    for (int i = 0; i < p->n_triangles; ++i) m->order[i] = i;
+    m->nodes = (MNode*)malloc(sizeof(MNode) * (size_t)(2 * (p->n_triangles > 0 ? p->n_triangles : 1)));
+    m->n_nodes = 0;
+    if (p->n_triangles > 0) mesh_build_rec(m, 0, p->n_triangles);
+    pthread_mutex_unlock(&g_mesh_mu);
+    return m;
+}
+
+/* Moller-Trumbore on the chord a + s d. */
+static int hit_triangle(V3 v0, V3 v1, V3 v2, V3 a, V3 d, double* s_out) {
+    const V3 e1 = vsub(v1, v0), e2 = vsub(v2, v0);
+    const V3 pv = vcross(d, e2);
+    const double det = vdot(e1, pv);
+    if (det == 0.0) return 0;
+    const double inv = 1.0 / det;
+    const V3 tv = vsub(a, v0);
+    const double u = vdot(tv, pv) * inv;
+    if (u < 0.0 || u > 1.0) return 0;
+    const V3 qv = vcross(tv, e1);
+    const double v = vdot(d, qv) * inv;
+    if (v < 0.0 || u + v > 1.0) return 0;
+    const double s = vdot(e2, qv) * inv;
+    if (s < 0.0 || s > 1.0) return 0;
+    *s_out = s;
+    return 1;
+}
+
+static int box_overlap(const MNode* n, const double lo[3], const double hi[3]) {
+    for (int k = 0; k < 3; ++k)
+        if (n->hi[k] < lo[k] || n->lo[k] > hi[k]) return 0;
+    return 1;
+}
+
+static int hit_mesh(const rr_primitive* p, V3 a, V3 b, double* s_out, int* tri_out) {
+    const MeshBVH* m = mesh_bvh(p);
+    const V3 d = vsub(b, a);
+    int have = 0, best_t = -1;
+    double best = 0.0;
+    if (g_mesh_brute || m->n_nodes == 0) {
+        for (int t = 0; t < p->n_triangles; ++t) {
+            double s;
+            if (hit_triangle(mvert(m, t, 0), mvert(m, t, 1), mvert(m, t, 2), a, d, &s) &&
+                (!have || s < best || (s == best && t < best_t))) {
+                best = s;
+                best_t = t;
+                have = 1;
+            }
+        }
+    } else {
+        const double lo[3] = {a.x < b.x ? a.x : b.x, a.y < b.y ? a.y : b.y, a.z < b.z ? a.z : b.z};
+        const double hi[3] = {a.x < b.x ? b.x : a.x, a.y < b.y ? b.y : a.y, a.z < b.z ? b.z : a.z};
+        int stack[128], sp = 0;
+        stack[sp++] = 0;
+        while (sp) {
+            const MNode* n = &m->nodes[stack[--sp]];
+            if (!box_overlap(n, lo, hi)) continue;
+            if (n->left < 0) {
+                for (int i = n->first; i < n->first + n->count; ++i) {
+                    const int t = m->order[i];
+                    double s;
+                    if (hit_triangle(mvert(m, t, 0), mvert(m, t, 1), mvert(m, t, 2), a, d, &s) &&
+                        (!have || s < best || (s == best && t < best_t))) {
+                        best = s;
+                        best_t = t;
+                        have = 1;
+                    }
+                }
+            } else {
+                stack[sp++] = n->left;
+                stack[sp++] = n->right;
+            }
+        }
+    }
+    *s_out = best;
+    *tri_out = best_t;
+    return have;
+}
+
 /* intersect_segment; `normal` (EXTENSION, may be NULL) receives the outward
  * unit normal of the hit face: sphere radial, half-space n/|n|, grid slab
  * entry face; -chord direction for a chord that starts inside (s = 0). */
@@ -558,19 +776,21 @@ static int intersect_segment_n(const rr_scene_desc* sc, V3 a, V3 b, V3* point, d
                                int* prim, V3* normal) {                          /* :99-109 */
     int have = 0;
     double best = 0.0;
-    int best_ax = -1;
+    int best_ax = -1, best_tri = -1;
     for (int i = 0; i < sc->n_primitives; ++i) {
         const rr_primitive* p = &sc->primitives[i];
         double s;
-        int h, ax = -1;
+        int h, ax = -1, tri = -1;
         if (p->kind == RR_PRIM_GRID_PLANES) h = hit_grid(p, a, b, &s, &ax);
         else if (p->kind == RR_PRIM_SPHERE) h = hit_sphere(p, a, b, &s);
+        else if (p->kind == RR_PRIM_MESH) h = hit_mesh(p, a, b, &s, &tri);
         else h = hit_half_space(p, a, b, &s);
         if (h && (!have || s < best)) {
             const V3 d = vsub(b, a);
             *point = vadd(a, vscale(s, d));
             best = s;
             best_ax = ax;
+            best_tri = tri;
             *prim = i;
             have = 1;
         }
@@ -580,7 +800,13 @@ static int intersect_segment_n(const rr_scene_desc* sc, V3 a, V3 b, V3* point, d
         const V3 d = vsub(b, a);
         const double dl = sqrt(vdot(d, d));
         const rr_primitive* p = &sc->primitives[*prim];
-        if (best == 0.0 || (p->kind == RR_PRIM_GRID_PLANES && best_ax < 0)) {
+        if (p->kind == RR_PRIM_MESH) {   /* geometric normal facing the chord */
+            const MeshBVH* m = mesh_bvh(p);
+            const V3 n = vcross(vsub(mvert(m, best_tri, 1), mvert(m, best_tri, 0)),
+                                vsub(mvert(m, best_tri, 2), mvert(m, best_tri, 0)));
+            const double sg = vdot(n, d) > 0.0 ? -1.0 : 1.0;
+            *normal = vscale(sg / sqrt(vdot(n, n)), n);
+        } else if (best == 0.0 || (p->kind == RR_PRIM_GRID_PLANES && best_ax < 0)) {
             *normal = vscale(-1.0 / dl, d);
         } else if (p->kind == RR_PRIM_SPHERE) {
             const V3 r = vsub(*point, vfrom(p->center));
@@ -604,6 +830,7 @@ static int intersect_segment(const rr_scene_desc* sc, V3 a, V3 b, V3* point, dou
 
 int rro_intersect(const rr_scene_desc* sc, const double a[3], const double b[3], double point[3],
                   double* s, int* prim) {
+    prepare_meshes(sc);
     V3 p;
     if (!intersect_segment(sc, vload(a), vload(b), &p, s, prim)) return 0;
     point[0] = p.x;
@@ -681,6 +908,7 @@ static void march_body(void* p, long lo, long hi) {
 void rro_march(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* integ,
                const rr_ray_start* rays, rr_pixel_outcome* out, size_t n, int threads) {
     MarchArgs a = {m, sc, integ, rays, out};
+    prepare_meshes(sc);
     parallel_for((long)n, 16, threads, march_body, &a);
 }
 
@@ -859,6 +1087,7 @@ void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camer
     atomic_init(&a.total_steps, 0);
     atomic_init(&a.errors, 0);
     atomic_init(&a.shadow_steps, 0);
+    prepare_meshes(sc);
     parallel_for(h, 1, threads, render_rows, &a);
     if (stats) {
         memset(stats, 0, sizeof *stats);
@@ -979,5 +1208,6 @@ void rro_flags(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera
                const rr_integrator* integ, int w, int h, const rr_pixel_outcome* outcomes,
                double perturb_rad, double wrap_eps, uint8_t* flags, int threads) {
     FlagArgs a = {m, sc, cam, integ, w, h, outcomes, perturb_rad, wrap_eps, flags};
+    prepare_meshes(sc);
     parallel_for(h, 1, threads, flag_rows, &a);
 }

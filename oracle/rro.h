@@ -65,6 +65,9 @@ void rro_flags(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera
                const rr_integrator* integ, int w, int h, const rr_pixel_outcome* outcomes,
                double perturb_rad, double wrap_eps, uint8_t* flags, int threads);
 
+/* Test hook: 1 = mesh intersection scans every triangle (no BVH pruning). */
+void rro_set_mesh_bruteforce(int on);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ RR_FIELD_GAUSSIAN, RR_FIELD_POLYNOMIAL, RR_FIELD_SUM = 0, 1, 2
 (RR_DIFFEO_IDENTITY, RR_DIFFEO_AFFINE, RR_DIFFEO_TWIST, RR_DIFFEO_LOCAL_BUMP,
  RR_DIFFEO_COMPOSE) = 0, 1, 2, 3, 4
 RR_METRIC_EUCLIDEAN, RR_METRIC_GRAPH, RR_METRIC_DIFFEO = 0, 1, 2
-RR_PRIM_GRID_PLANES, RR_PRIM_SPHERE, RR_PRIM_HALF_SPACE = 0, 1, 2
+RR_PRIM_GRID_PLANES, RR_PRIM_SPHERE, RR_PRIM_HALF_SPACE, RR_PRIM_MESH = 0, 1, 2, 3
 RR_SCHEME_EULER, RR_SCHEME_RK4 = 0, 1
 RR_MISS, RR_HIT, RR_FAILED = 0, 1, 2
 
@@ -70,7 +70,9 @@ class rr_metric_desc(C.Structure):
 class rr_primitive(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("spacing", C.c_double),
                 ("half_width", C.c_double), ("bounds", rr_aabb), ("center", rr_vec3),
-                ("radius", C.c_double), ("normal", rr_vec3), ("offset", C.c_double)]
+                ("radius", C.c_double), ("normal", rr_vec3), ("offset", C.c_double),
+                ("n_vertices", C.c_int32), ("n_triangles", C.c_int32),
+                ("vertices", C.POINTER(C.c_double)), ("triangles", C.POINTER(C.c_int32))]
 
 
 class rr_light(C.Structure):
@@ -130,7 +132,7 @@ OUTCOME_DTYPE = np.dtype({
 EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
     "rr_field_node": 72, "rr_diffeo_node": 192, "rr_metric_desc": 56,
-    "rr_primitive": 136, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 16,
+    "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 16,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 72,
     "rr_options": 32,
 }

@@ -8,6 +8,10 @@ ValidationError/ParseError naming the same key.  One superset key is accepted
 
     scene.lights: [{"position": [x,y,z], "intensity": I}]   point lights for
                    shadow geodesics; absent/empty = reference shading.
+    scene.ambient: ambient term of the lit shading (default 0.2).
+    scene.primitives[i] = {"kind": "mesh", "vertices": [...], "triangles": [...]}
+                   or {"kind": "mesh", "generator": {"kind": "torus", ...}}
+                   triangle meshes (BVH-accelerated on the GPU).
 
 ``metric_desc`` / ``scene_desc`` flatten the parsed trees into the C-ABI
 descriptors of include/rray_cuda.h.
@@ -136,6 +140,43 @@ class Sphere:                         # scene.hpp:28-33
 class HalfSpace:                      # scene.hpp:35-41
     normal: Vec3 = field(default_factory=lambda: [0.0, 0.0, 1.0])
     offset: float = 0.0
+
+
+@dataclass
+class Mesh:                           # EXTENSION: triangle mesh primitive
+    vertices: object = None           # numpy (n, 3) float64
+    triangles: object = None          # numpy (m, 3) int32
+    generator: Optional[dict] = None  # the procedural spec it came from, if any
+
+    def __eq__(self, o):
+        import numpy as np
+        return (isinstance(o, Mesh) and self.generator == o.generator and
+                np.array_equal(self.vertices, o.vertices) and
+                np.array_equal(self.triangles, o.triangles))
+
+
+def torus_mesh(center, major, minor, nu, nv, wobble=0.0):
+    """Deterministic torus around the z axis: nu*nv*2 triangles.  `wobble`
+    modulates the tube radius by (1 + wobble sin(5u) sin(3v))."""
+    import numpy as np
+    u = 2.0 * np.pi * np.arange(nu) / nu
+    v = 2.0 * np.pi * np.arange(nv) / nv
+    U, V = np.meshgrid(u, v, indexing="ij")
+    r = minor * (1.0 + wobble * np.sin(5.0 * U) * np.sin(3.0 * V))
+    x = (major + r * np.cos(V)) * np.cos(U) + center[0]
+    y = (major + r * np.cos(V)) * np.sin(U) + center[1]
+    z = r * np.sin(V) + center[2]
+    verts = np.stack([x, y, z], -1).reshape(-1, 3)
+    i = np.arange(nu)[:, None]
+    j = np.arange(nv)[None, :]
+    a = i * nv + j
+    b = ((i + 1) % nu) * nv + j
+    c_ = ((i + 1) % nu) * nv + (j + 1) % nv
+    d = i * nv + (j + 1) % nv
+    t1 = np.stack([a, b, c_], -1).reshape(-1, 3)
+    t2 = np.stack([a, c_, d], -1).reshape(-1, 3)
+    tris = np.stack([t1, t2], 1).reshape(-1, 3).astype(np.int32)
+    return verts.astype(np.float64), tris
 
 
 @dataclass
@@ -446,9 +487,45 @@ def _parse_scene(o, path, allow_ext: bool) -> Scene:              # :277-338
             if not (_norm(hs.normal) > 0.0):
                 _fail(pp + ".normal", "must be nonzero")
             s.primitives.append(hs)
+        elif kind == "mesh" and allow_ext:
+            s.primitives.append(_parse_mesh(p, pp))
         else:
             _fail(pp + ".kind", f"must be one of grid_planes|sphere|half_space, got '{kind}'")
     return s
+
+
+def _parse_mesh(p, pp) -> Mesh:                                  # EXTENSION
+    import numpy as np
+    _check_keys(p, pp, {"kind", "vertices", "triangles", "generator"})
+    if "generator" in p:
+        g = p["generator"]
+        _check_keys(g, pp + ".generator", {"kind", "center", "major", "minor", "nu", "nv", "wobble"})
+        if _get_string_or(g, pp + ".generator", "kind", "") != "torus":
+            _fail(pp + ".generator.kind", "must be 'torus'")
+        nu = _get_int_or(g, pp + ".generator", "nu", 64)
+        nv = _get_int_or(g, pp + ".generator", "nv", 32)
+        if nu < 3 or nv < 3:
+            _fail(pp + ".generator", "nu, nv must be >= 3")
+        spec = {"kind": "torus", "center": _get_vec3(g, pp + ".generator", "center"),
+                "major": _get_double(g, pp + ".generator", "major"),
+                "minor": _get_double(g, pp + ".generator", "minor"), "nu": nu, "nv": nv,
+                "wobble": _get_double_or(g, pp + ".generator", "wobble", 0.0)}
+        if not (spec["major"] > spec["minor"] > 0.0):
+            _fail(pp + ".generator", "need major > minor > 0")
+        v, t = torus_mesh(spec["center"], spec["major"], spec["minor"], nu, nv, spec["wobble"])
+        return Mesh(v, t, spec)
+    vs, ts = p.get("vertices"), p.get("triangles")
+    if not isinstance(vs, list) or not isinstance(ts, list) or not ts:
+        _fail(pp, "mesh needs 'vertices' and non-empty 'triangles' (or a 'generator')")
+    v = np.array([_as_vec3(x, f"{pp}.vertices[{i}]") for i, x in enumerate(vs)], np.float64).reshape(-1, 3)
+    tl = []
+    for i, t in enumerate(ts):
+        if not isinstance(t, list) or len(t) != 3 or not all(_is_integer(k) for k in t):
+            _fail(f"{pp}.triangles[{i}]", "must be 3 vertex indices")
+        if not all(0 <= k < len(v) for k in t):
+            _fail(f"{pp}.triangles[{i}]", "vertex index out of range")
+        tl.append(t)
+    return Mesh(v, np.array(tl, np.int32), None)
 
 
 def _parse_lights(o, path) -> List[Light]:                        # EXTENSION
@@ -586,6 +663,10 @@ def _aabb_json(b):
 
 
 def _prim_json(p):
+    if isinstance(p, Mesh):
+        if p.generator is not None:
+            return {"kind": "mesh", "generator": dict(p.generator)}
+        return {"kind": "mesh", "vertices": p.vertices.tolist(), "triangles": p.triangles.tolist()}
     if isinstance(p, GridPlanes):
         return {"kind": "grid_planes", "spacing": p.spacing, "half_width": p.half_width,
                 "bounds": _aabb_json(p.bounds)}
@@ -595,7 +676,8 @@ def _prim_json(p):
 
 
 def config_to_dict(cfg: RunConfig, include_ext: bool = True) -> dict:
-    scene = {"primitives": [_prim_json(p) for p in cfg.scene.primitives],
+    prims = [p for p in cfg.scene.primitives if include_ext or not isinstance(p, Mesh)]
+    scene = {"primitives": [_prim_json(p) for p in prims],
              "bounds": _aabb_json(cfg.scene.bounds), "fog_density": cfg.scene.fog_density}
     if include_ext and cfg.scene.lights:
         scene["lights"] = [{"position": list(l.position), "intensity": l.intensity}
@@ -705,10 +787,20 @@ class SceneDesc:
     """Owns the primitive/light arrays behind an ``rr_scene_desc``."""
 
     def __init__(self, scene: Scene, with_lights: bool = True):
+        import numpy as np
         prims = []
+        self._mesh_arrays = []
         for p in scene.primitives:
             q = abi.rr_primitive()
-            if isinstance(p, GridPlanes):
+            if isinstance(p, Mesh):
+                v = np.ascontiguousarray(p.vertices, np.float64)
+                t = np.ascontiguousarray(p.triangles, np.int32)
+                self._mesh_arrays += [v, t]
+                q.kind = abi.RR_PRIM_MESH
+                q.n_vertices, q.n_triangles = len(v), len(t)
+                q.vertices = v.ctypes.data_as(C.POINTER(C.c_double))
+                q.triangles = t.ctypes.data_as(C.POINTER(C.c_int32))
+            elif isinstance(p, GridPlanes):
                 q.kind = abi.RR_PRIM_GRID_PLANES
                 q.spacing, q.half_width = float(p.spacing), float(p.half_width)
                 q.bounds = abi.rr_aabb(abi.rr_vec3.of(p.bounds.min), abi.rr_vec3.of(p.bounds.max))

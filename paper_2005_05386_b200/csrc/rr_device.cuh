@@ -39,6 +39,7 @@ constexpr int kMaxPrims = 32;     // scene primitives
 constexpr int kStaticSpheres = 4; // sphere slots evaluated with constant operands
 constexpr int kStaticHalves = 2;  // half-space slots evaluated with constant operands
 constexpr int kMaxLights = 8;     // point lights (EXTENSION)
+constexpr int kMaxMeshes = 4;     // triangle-mesh primitives (EXTENSION)
 constexpr int kUnit = 32;         // rays per warp unit
 constexpr int kMicroW = 8, kMicroH = 4;   // pixel micro-tile of one warp
 
@@ -48,7 +49,7 @@ constexpr float kHalfLog2e = 0.7213475204444817f;
 
 enum Kind : int { kEuclid = 0, kBumps = 1, kGraphGeneral = 2, kDiffeo = 3 };
 enum Stage : int { kStageAffine = 0, kStageTwist = 1, kStageBump = 2 };
-enum Prim : int { kPrimGrid = 0, kPrimSphere = 1, kPrimHalfSpace = 2 };
+enum Prim : int { kPrimGrid = 0, kPrimSphere = 1, kPrimHalfSpace = 2, kPrimMesh = 3 };
 enum Mode : int { kModeFrame = 0, kModeTiles = 1, kModeRays = 2 };
 
 struct DevBump {          // one Gaussian term in factored form
@@ -93,6 +94,15 @@ struct DevGrid {          // scene.cpp:36-54
     int pad;
 };
 
+struct DevMesh {          // EXTENSION: BVH over a triangle soup (rr_bvh.h layouts)
+    const float4* nodes;  // 2 float4 per node
+    const float4* tris;   // 3 float4 per triangle
+    int n_nodes, n_tris;
+    int index;            // position in Scene::primitives
+    int pad;
+    unsigned long long fingerprint;   // host: content hash (scene-change detection)
+};
+
 struct DevLight {
     float pos[3];
     float intensity;
@@ -111,7 +121,7 @@ struct DevParams {
     int kind;             // Kind
     int n_bumps, n_poly, n_stages;
     int n_prims, n_lights, scheme, max_steps;
-    int n_spheres, n_halves, n_grids;
+    int n_spheres, n_halves, n_grids, n_meshes;
     int nb_slot;          // kBumps: bump slots of the kernel variant (4/8/16/32)
     float h, fog;
     float ambient;        // EXTENSION: lit shading ambient term
@@ -130,6 +140,7 @@ struct DevParams {
     DevSphere spheres[kMaxPrims];
     DevHalf halves[kMaxPrims];
     DevGrid grids[kMaxPrims];
+    DevMesh meshes[kMaxMeshes];
     DevLight lights[kMaxLights];
 };
 

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "rr_bvh.h"
 #include "rr_device.cuh"
 #include "rr_internal.h"
 #include "rray_cuda.h"
@@ -93,6 +94,7 @@ struct rr_ctx {
     size_t out_cap = 0;
     uint8_t* d_rgb = nullptr;
     size_t rgb_cap = 0;
+    std::vector<void*> d_mesh;               // EXTENSION: BVH nodes + triangles per mesh
     void* d_hits = nullptr;                  // EXTENSION: hit records of the shadow pass
     size_t hits_cap = 0;
     const char* last_kernel = "";
@@ -266,10 +268,20 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
         }
     }
     P.n_prims = sc->n_primitives;
-    P.n_spheres = P.n_halves = P.n_grids = 0;
+    P.n_spheres = P.n_halves = P.n_grids = P.n_meshes = 0;
     for (int i = 0; i < sc->n_primitives; ++i) {
         const rr_primitive& q = sc->primitives[i];
-        if (q.kind == RR_PRIM_SPHERE) {
+        if (q.kind == RR_PRIM_MESH) {
+            rr::DevMesh& d = P.meshes[P.n_meshes++];
+            d.n_tris = q.n_triangles;
+            d.index = i;
+            uint64_t h = 1469598103934665603ULL;   // FNV-1a of the mesh content
+            const unsigned char* b = reinterpret_cast<const unsigned char*>(q.vertices);
+            for (size_t k = 0; k < (size_t)q.n_vertices * 3 * sizeof(double); ++k) h = (h ^ b[k]) * 1099511628211ULL;
+            b = reinterpret_cast<const unsigned char*>(q.triangles);
+            for (size_t k = 0; k < (size_t)q.n_triangles * 3 * sizeof(int32_t); ++k) h = (h ^ b[k]) * 1099511628211ULL;
+            d.fingerprint = h;
+        } else if (q.kind == RR_PRIM_SPHERE) {
             rr::DevSphere& d = P.spheres[P.n_spheres++];
             d.c[0] = (float)q.center.x;
             d.c[1] = (float)q.center.y;
@@ -695,6 +707,7 @@ void rr_destroy(rr_ctx* c) {
     if (c->d_out) cudaFree(c->d_out);
     if (c->d_rgb) cudaFree(c->d_rgb);
     if (c->d_hits) cudaFree(c->d_hits);
+    for (void* p : c->d_mesh) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -745,6 +758,7 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
         return set_err(c, RR_ERR_CONFIG, "scene.primitives: at most 32 primitives");
     if (sc->n_lights < 0 || sc->n_lights > rr::kMaxLights)
         return set_err(c, RR_ERR_CONFIG, "scene.lights: at most 8 lights");
+    int n_mesh = 0;
     for (int i = 0; i < sc->n_primitives; ++i) {
         const rr_primitive& q = sc->primitives[i];
         if (q.kind == RR_PRIM_GRID_PLANES) {
@@ -752,6 +766,14 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
                 return set_err(c, RR_ERR_CONFIG, "scene.primitives: grid needs half_width > 0, spacing > 2*half_width");
         } else if (q.kind == RR_PRIM_SPHERE) {
             if (!(q.radius > 0.0)) return set_err(c, RR_ERR_CONFIG, "scene.primitives: radius must be > 0");
+        } else if (q.kind == RR_PRIM_MESH) {
+            if (q.n_triangles < 1 || q.n_vertices < 3 || !q.vertices || !q.triangles)
+                return set_err(c, RR_ERR_CONFIG, "scene.primitives: mesh needs vertices and triangles");
+            for (int t = 0; t < 3 * q.n_triangles; ++t)
+                if (q.triangles[t] < 0 || q.triangles[t] >= q.n_vertices)
+                    return set_err(c, RR_ERR_CONFIG, "scene.primitives: mesh vertex index out of range");
+            if (++n_mesh > rr::kMaxMeshes)
+                return set_err(c, RR_ERR_CONFIG, "scene.primitives: at most 4 meshes");
         } else if (q.kind != RR_PRIM_HALF_SPACE) {
             return set_err(c, RR_ERR_CONFIG, "scene.primitives.kind: unknown primitive kind");
         }
@@ -765,8 +787,40 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
     fill_params(prog, sc, *np, slots);
     const bool same = c->has_scene && c->P_key && std::memcmp(c->P_key, np, sizeof *np) == 0;
     if (!same) {
+        // meshes: build BVHs on the host, upload to device buffers
+        for (void* p : c->d_mesh) cudaFree(p);
+        c->d_mesh.clear();
+        int m = 0;
+        for (int i = 0; i < sc->n_primitives; ++i) {
+            const rr_primitive& q = sc->primitives[i];
+            if (q.kind != RR_PRIM_MESH) continue;
+            rr::BvhBuild bvh;
+            rr::build_bvh(q.vertices, q.n_vertices, q.triangles, q.n_triangles, bvh);
+            void *dn = nullptr, *dt = nullptr;
+            cudaError_t e = cudaMalloc(&dn, bvh.nodes.size() * sizeof(float));
+            if (e == cudaSuccess) e = cudaMalloc(&dt, bvh.tris.size() * sizeof(float));
+            if (e == cudaSuccess)
+                e = cudaMemcpy(dn, bvh.nodes.data(), bvh.nodes.size() * sizeof(float), cudaMemcpyHostToDevice);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(dt, bvh.tris.data(), bvh.tris.size() * sizeof(float), cudaMemcpyHostToDevice);
+            if (dn) c->d_mesh.push_back(dn);
+            if (dt) c->d_mesh.push_back(dt);
+            if (e != cudaSuccess) {
+                delete np;
+                return cuda_err(c, e, "mesh upload");
+            }
+            np->meshes[m].nodes = reinterpret_cast<const float4*>(dn);
+            np->meshes[m].tris = reinterpret_cast<const float4*>(dt);
+            np->meshes[m].n_nodes = (int)(bvh.nodes.size() / 8);
+            ++m;
+        }
         if (!c->P_key) c->P_key = new DevParams();
         *c->P_key = *np;
+        for (int k = 0; k < rr::kMaxMeshes; ++k) {   // key: content only, not device pointers
+            c->P_key->meshes[k].nodes = nullptr;
+            c->P_key->meshes[k].tris = nullptr;
+            c->P_key->meshes[k].n_nodes = 0;
+        }
         *c->P = *np;
         c->prog = prog;
         c->slots = slots;

@@ -375,20 +375,127 @@ __device__ __forceinline__ bool hit_half_space(const DevHalf& hs, F3 a, F3 d, fl
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// EXTENSION: triangle meshes.  The chord [a, b] of a step is tested against a
+// BVH (slab test per node, Moller-Trumbore per triangle, ties keep the lower
+// original triangle index: oracle/rro.c hit_mesh).  Each lane also keeps a
+// "free distance": the distance from a query point to the nearest leaf box;
+// while the marched path stays inside that ball (sum of chord lengths) no
+// mesh test is needed.  Both are __noinline__ so scenes without meshes keep
+// the march loop's register allocation.
+__device__ __noinline__ bool mesh_chord(const DevMesh& M, F3 a, F3 d, float& best_s, int& best_rec) {
+    const float ix = d.x != 0.f ? 1.f / d.x : 3.0e38f;
+    const float iy = d.y != 0.f ? 1.f / d.y : 3.0e38f;
+    const float iz = d.z != 0.f ? 1.f / d.z : 3.0e38f;
+    bool have = false;
+    float best = 1.f;
+    int best_t = 0x7fffffff;
+    int stack[64];
+    int sp = 0, node = 0;
+    for (;;) {
+        const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
+        float t0 = 0.f, t1 = best;
+        {
+            float u = (n0.x - a.x) * ix, w = (n1.x - a.x) * ix;
+            t0 = fmaxf(t0, fminf(u, w));
+            t1 = fminf(t1, fmaxf(u, w));
+            u = (n0.y - a.y) * iy;
+            w = (n1.y - a.y) * iy;
+            t0 = fmaxf(t0, fminf(u, w));
+            t1 = fminf(t1, fmaxf(u, w));
+            u = (n0.z - a.z) * iz;
+            w = (n1.z - a.z) * iz;
+            t0 = fmaxf(t0, fminf(u, w));
+            t1 = fminf(t1, fmaxf(u, w));
+        }
+        // a zero chord component makes u, w +-inf or NaN: fall back to the
+        // containment test on that axis
+        bool overlap = t0 <= t1;
+        if (d.x == 0.f) overlap = overlap && a.x >= n0.x && a.x <= n1.x;
+        if (d.y == 0.f) overlap = overlap && a.y >= n0.y && a.y <= n1.y;
+        if (d.z == 0.f) overlap = overlap && a.z >= n0.z && a.z <= n1.z;
+        if (overlap) {
+            const int first = __float_as_int(n0.w), cnt = __float_as_int(n1.w);
+            if (cnt > 0) {
+                for (int i = first; i < first + cnt; ++i) {
+                    const float4 r0 = __ldg(M.tris + 3 * i), r1 = __ldg(M.tris + 3 * i + 1),
+                                 r2 = __ldg(M.tris + 3 * i + 2);
+                    const F3 e1 = f3(r1.x, r1.y, r1.z), e2 = f3(r2.x, r2.y, r2.z);
+                    const F3 pv = f3(d.y * e2.z - d.z * e2.y, d.z * e2.x - d.x * e2.z, d.x * e2.y - d.y * e2.x);
+                    const float det = e1.x * pv.x + e1.y * pv.y + e1.z * pv.z;
+                    if (det == 0.f) continue;
+                    const float inv = 1.f / det;
+                    const F3 tv = f3(a.x - r0.x, a.y - r0.y, a.z - r0.z);
+                    const float u = (tv.x * pv.x + tv.y * pv.y + tv.z * pv.z) * inv;
+                    if (u < 0.f || u > 1.f) continue;
+                    const F3 qv = f3(tv.y * e1.z - tv.z * e1.y, tv.z * e1.x - tv.x * e1.z, tv.x * e1.y - tv.y * e1.x);
+                    const float v = (d.x * qv.x + d.y * qv.y + d.z * qv.z) * inv;
+                    if (v < 0.f || u + v > 1.f) continue;
+                    const float s = (e2.x * qv.x + e2.y * qv.y + e2.z * qv.z) * inv;
+                    if (s < 0.f || s > 1.f) continue;
+                    const int t = __float_as_int(r0.w);
+                    if (!have || s < best || (s == best && t < best_t)) {
+                        best = s;
+                        best_t = t;
+                        best_rec = i;
+                        have = true;
+                    }
+                }
+            } else if (sp < 63) {
+                stack[sp++] = first;      // right child
+                node = node + 1;          // left child
+                continue;
+            }
+        }
+        if (sp == 0) break;
+        node = stack[--sp];
+    }
+    if (have) best_s = best;
+    return have;
+}
+
+// Distance from p to the nearest leaf box (capped): no triangle lies closer.
+__device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
+    float best = cap;
+    int stack[64];
+    int sp = 0, node = 0;
+    for (;;) {
+        const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
+        const float dx = fmaxf(fmaxf(n0.x - p.x, p.x - n1.x), 0.f);
+        const float dy = fmaxf(fmaxf(n0.y - p.y, p.y - n1.y), 0.f);
+        const float dz = fmaxf(fmaxf(n0.z - p.z, p.z - n1.z), 0.f);
+        const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+        if (dist < best) {
+            if (__float_as_int(n1.w) > 0) {
+                best = dist;
+            } else if (sp < 63) {
+                stack[sp++] = __float_as_int(n0.w);
+                node = node + 1;
+                continue;
+            }
+        }
+        if (sp == 0) break;
+        node = stack[--sp];
+    }
+    return best;
+}
+
 // Nearest hit over all primitives; ties keep the lower primitive index
 // (scene.cpp:99-109), i.e. the lexicographic minimum of (s, index).
-__device__ __forceinline__ void consider(bool h, float s, int idx, int id, bool& have, float& best,
+__device__ __forceinline__ bool consider(bool h, float s, int idx, int id, bool& have, float& best,
                                          int& prim, int& hid) {
     if (h && (!have || s < best || (s == best && idx < prim))) {
         best = s;
         prim = idx;
         hid = id;   // (kind << 8) | slot, for the hit normal (EXT shading)
         have = true;
+        return true;
     }
+    return false;
 }
 
 __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
-                                          int& prim, int& hid) {
+                                          int& prim, int& hid, float& mfree, int& mrec) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
     const float qa = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
     const float len = fmaf(sqrt_approx(qa), 1.0001f, 1e-30f);   // conservative chord length
@@ -418,14 +525,37 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
         const bool h = hit_grid(P.grids[i], a, b, d, s);
         consider(h, s, P.grids[i].index, (kPrimGrid << 8) | i, have, s_best, prim, hid);
     }
+    if (P.n_meshes > 0) {
+        if (len < mfree) {
+            mfree -= len;                 // the chord stays inside the free ball
+        } else {
+            for (int i = 0; i < P.n_meshes; ++i) {
+                int rec = 0;
+                const bool h = mesh_chord(P.meshes[i], a, d, s, rec);
+                if (consider(h, s, P.meshes[i].index, (kPrimMesh << 8) | i, have, s_best, prim, hid))
+                    mrec = rec;
+            }
+            float fr = 3.0e38f;
+            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, 8.f));
+            mfree = fr;
+        }
+    }
     return have;
 }
 
 // Outward unit normal of a hit (EXTENSION shading; oracle/rro.c
 // intersect_segment_n): sphere radial, half-space n/|n|, grid entry face,
 // -chord direction for a chord that starts inside (s == 0).
-__device__ F3 hit_normal(const DevParams& P, int hid, float s, F3 a, F3 b, F3 point) {
+__device__ F3 hit_normal(const DevParams& P, int hid, float s, F3 a, F3 b, F3 point, int mrec) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
+    if (hid >> 8 == kPrimMesh) {                // geometric normal facing the chord
+        const DevMesh& M = P.meshes[hid & 0xff];
+        const float4 r1 = __ldg(M.tris + 3 * mrec + 1), r2 = __ldg(M.tris + 3 * mrec + 2);
+        F3 n = f3(r1.y * r2.z - r1.z * r2.y, r1.z * r2.x - r1.x * r2.z, r1.x * r2.y - r1.y * r2.x);
+        const float sg = (n.x * d.x + n.y * d.y + n.z * d.z) > 0.f ? -1.f : 1.f;
+        const float il = sg * rsqrtf(n.x * n.x + n.y * n.y + n.z * n.z);
+        return f3(n.x * il, n.y * il, n.z * il);
+    }
     const float kind = hid >> 8;
     const int slot = hid & 0xff;
     F3 n;
@@ -543,6 +673,7 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
     const float sixth = h / 6.f;
     int step = 0;                             // this lane's reference step index
     const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
+    float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
     for (;;) {
         if (!__any_sync(kFull, active)) break;
         uint32_t um = 0;
@@ -631,12 +762,12 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
             const int nsub = nj ? nj : 1;
             cnt.steps_integrated += 1;
             float s = 0.f;
-            int prim = -1, hid = 0;
+            int prim = -1, hid = 0, mrec = 0;
             if (KIND == kDiffeo && !(valid > 1e-14f)) {     // kernel_impl.hpp:54-61
                 res.status = PASS == kPassShadow ? 0 : 2;
                 res.steps = step;
                 active = false;
-            } else if (intersect(P, p, pn, s, prim, hid)) { // kernel_impl.hpp:63-76
+            } else if (intersect(P, p, pn, s, prim, hid, mfree, mrec)) { // kernel_impl.hpp:63-76
                 const F3 pt = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
                                  fmaf(s, pn.z - p.z, p.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
@@ -649,7 +780,7 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
                     res.prim = prim;
                     res.point = pt;
                     res.t = ((float)step + sj) * h;
-                    if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, pn, pt);
+                    if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, pn, pt, mrec);
                 }
                 res.steps = step + sub + 1;
                 active = false;
