@@ -494,6 +494,7 @@ __device__ __forceinline__ bool consider(bool h, float s, int idx, int id, bool&
     return false;
 }
 
+template <bool MESH>
 __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
                                           int& prim, int& hid, float& mfree, int& mrec) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
@@ -525,7 +526,7 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
         const bool h = hit_grid(P.grids[i], a, b, d, s);
         consider(h, s, P.grids[i].index, (kPrimGrid << 8) | i, have, s_best, prim, hid);
     }
-    if (P.n_meshes > 0) {
+    if (MESH) {
         if (len < mfree) {
             mfree -= len;                 // the chord stays inside the free ball
         } else {
@@ -661,7 +662,7 @@ enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2 };
 // shadow_march): lit (1) when it crosses the sphere |x - q| = sqrt(dist2),
 // leaves the bounds or runs out of steps; blocked (0) on a nearer hit or a
 // metric failure.
-template <int KIND, int NB, int SCHEME, int PASS>
+template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
                                                 LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
                                                 float dist2 = 0.f) {
@@ -767,7 +768,7 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
                 res.status = PASS == kPassShadow ? 0 : 2;
                 res.steps = step;
                 active = false;
-            } else if (intersect(P, p, pn, s, prim, hid, mfree, mrec)) { // kernel_impl.hpp:63-76
+            } else if (intersect<MESH>(P, p, pn, s, prim, hid, mfree, mrec)) { // kernel_impl.hpp:63-76
                 const F3 pt = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
                                  fmaf(s, pn.z - p.z, p.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
@@ -926,7 +927,7 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
     dir = f3((float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
 }
 
-template <int KIND, int NB, int SCHEME, int PASS>
+template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 __global__ void __launch_bounds__(kThreads, RR_MIN_BLOCKS)
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
@@ -999,7 +1000,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                     v0 = f3(D.x * inv, D.y * inv, D.z * inv);
                     want = ok;
                 }
-                const RayResult sr = march_unit<KIND, NB, SCHEME, kPassShadow>(P, want, x0, v0, cnt, q, dist2);
+                const RayResult sr = march_unit<KIND, NB, SCHEME, kPassShadow, MESH>(P, want, x0, v0, cnt, q, dist2);
                 if (want) shadow_steps += (unsigned)sr.steps;   // reference-equivalent steps
                 if (want && sr.status == 1) light = fmaf(Lt.intensity, lam, light);
             }
@@ -1008,7 +1009,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                 shade(P, r, L.rgb + 3 * pix, light);
             }
         } else {
-            const RayResult r = march_unit<KIND, NB, SCHEME, PASS>(P, live, pos, dir, cnt);
+            const RayResult r = march_unit<KIND, NB, SCHEME, PASS, MESH>(P, live, pos, dir, cnt);
             ref_steps = live ? (unsigned)r.steps : 0u;
             errs = (live && r.status == 2) ? 1u : 0u;
             if (live) {
@@ -1095,69 +1096,81 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
     if (s == 12345.678f) out[0] = s;   // keep the chains alive
 }
 
-template <int KIND, int NB, int SCHEME, int PASS>
+template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 int occupancy_of() {
     static int occ = [] {
         int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME, PASS>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME, PASS, MESH>,
+                                                      kThreads, 0);
         return n > 0 ? n : 1;
     }();
     return occ;
 }
 
-template <int KIND, int NB, int SCHEME, int PASS>
+template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 cudaError_t launch_pass(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
     const unsigned warps_needed = L.n_units;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME, PASS>());
+    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME, PASS, MESH>());
     const unsigned max_useful = (warps_needed + 3) / 4;
     if (blocks > max_useful) blocks = max_useful;
     if (blocks == 0) blocks = 1;
-    march_kernel<KIND, NB, SCHEME, PASS><<<blocks, kThreads, 0, s>>>(P, L);
+    march_kernel<KIND, NB, SCHEME, PASS, MESH><<<blocks, kThreads, 0, s>>>(P, L);
     return cudaGetLastError();
 }
 
 // Without lights: one fused launch.  With lights (EXTENSION): a hit-record
 // pass and a shadow+shade pass over the same units (each with its own unit
-// counter: L.counter[0] and L.counter[1]).
-template <int KIND, int NB, int SCHEME>
+// counter: L.counter[0] and L.counter[1]).  Scenes with meshes use the MESH
+// variants (BVH traversal compiled in; kept out of the mesh-free kernels).
+template <int KIND, int NB, int SCHEME, bool MESH>
 cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    if (P.n_lights == 0 || L.mode == kModeRays) return launch_pass<KIND, NB, SCHEME, kPassShade>(P, L, s, num_sms);
-    cudaError_t e = launch_pass<KIND, NB, SCHEME, kPassHits>(P, L, s, num_sms);
+    if (P.n_lights == 0 || L.mode == kModeRays)
+        return launch_pass<KIND, NB, SCHEME, kPassShade, MESH>(P, L, s, num_sms);
+    cudaError_t e = launch_pass<KIND, NB, SCHEME, kPassHits, MESH>(P, L, s, num_sms);
     if (e != cudaSuccess) return e;
     DevLaunch L2 = L;
     L2.counter = L.counter + 1;
-    return launch_pass<KIND, NB, SCHEME, kPassShadow>(P, L2, s, num_sms);
+    return launch_pass<KIND, NB, SCHEME, kPassShadow, MESH>(P, L2, s, num_sms);
+}
+
+template <int SCHEME, bool MESH>
+cudaError_t dispatch_kind(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                          const char** name) {
+    switch (P.kind) {
+        case kEuclid:
+            *name = MESH ? "march_kernel<euclid,mesh>" : "march_kernel<euclid>";
+            return launch_variant<kEuclid, 0, SCHEME, MESH>(P, L, s, sms);
+        case kBumps:
+            if constexpr (!MESH) {   // mesh scenes use the 16/32-slot variants only
+                if (P.nb_slot <= 4) {
+                    *name = "march_kernel<bumps4>";
+                    return launch_variant<kBumps, 4, SCHEME, MESH>(P, L, s, sms);
+                }
+                if (P.nb_slot <= 8) {
+                    *name = "march_kernel<bumps8>";
+                    return launch_variant<kBumps, 8, SCHEME, MESH>(P, L, s, sms);
+                }
+            }
+            if (P.nb_slot <= 16) {
+                *name = MESH ? "march_kernel<bumps16,mesh>" : "march_kernel<bumps16>";
+                return launch_variant<kBumps, 16, SCHEME, MESH>(P, L, s, sms);
+            }
+            *name = MESH ? "march_kernel<bumps32,mesh>" : "march_kernel<bumps32>";
+            return launch_variant<kBumps, 32, SCHEME, MESH>(P, L, s, sms);
+        case kGraphGeneral:
+            *name = MESH ? "march_kernel<graph,mesh>" : "march_kernel<graph>";
+            return launch_variant<kGraphGeneral, 0, SCHEME, MESH>(P, L, s, sms);
+        default:
+            *name = MESH ? "march_kernel<diffeo,mesh>" : "march_kernel<diffeo>";
+            return launch_variant<kDiffeo, 0, SCHEME, MESH>(P, L, s, sms);
+    }
 }
 
 template <int SCHEME>
 cudaError_t dispatch_scheme(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
                             const char** name) {
-    switch (P.kind) {
-        case kEuclid:
-            *name = "march_kernel<euclid>";
-            return launch_variant<kEuclid, 0, SCHEME>(P, L, s, sms);
-        case kBumps:
-            if (P.nb_slot <= 4) {
-                *name = "march_kernel<bumps4>";
-                return launch_variant<kBumps, 4, SCHEME>(P, L, s, sms);
-            }
-            if (P.nb_slot <= 8) {
-                *name = "march_kernel<bumps8>";
-                return launch_variant<kBumps, 8, SCHEME>(P, L, s, sms);
-            }
-            if (P.nb_slot <= 16) {
-                *name = "march_kernel<bumps16>";
-                return launch_variant<kBumps, 16, SCHEME>(P, L, s, sms);
-            }
-            *name = "march_kernel<bumps32>";
-            return launch_variant<kBumps, 32, SCHEME>(P, L, s, sms);
-        case kGraphGeneral:
-            *name = "march_kernel<graph>";
-            return launch_variant<kGraphGeneral, 0, SCHEME>(P, L, s, sms);
-        default:
-            *name = "march_kernel<diffeo>";
-            return launch_variant<kDiffeo, 0, SCHEME>(P, L, s, sms);
-    }
+    return P.n_meshes > 0 ? dispatch_kind<SCHEME, true>(P, L, s, sms, name)
+                          : dispatch_kind<SCHEME, false>(P, L, s, sms, name);
 }
 
 } // namespace
