@@ -55,6 +55,8 @@ def parse_args():
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-shadows", action="store_true")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the secondary BASELINE workloads (C1, C2, C4+mesh, C5 4K)")
     p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
     p.add_argument("--opt", action="append", default=[],
                    help="renderer option key=value (rr_options field), e.g. cull_grid=64")
@@ -311,6 +313,38 @@ def run_b200(args, cfg):
                    "launches_per_frame": sst["kernel_launches"]}
         r.set_config(cfg)
 
+    # ---- the other BASELINE.json configs, device-timed the same way (secondary)
+    extras = None
+    if world == 1 and not args.no_extras:
+        from paper_2005_05386_b200.config import load_config
+        extras = {}
+        for name in ("c1_gauss1_512", "c2_flat_1080p", "c4_twist_mesh_1080p", "c5_bumps16_4k"):
+            ecfg = load_config(os.path.join(ROOT, "configs", name + ".json"))
+            ew, eh = ecfg.output.width, ecfg.output.height
+            ebuf = torch.empty((eh, ew, 3), dtype=torch.uint8, device="cuda")
+            r.set_config(ecfg)
+            ecam = r.build_camera(ecfg.camera)
+            r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp)
+            n = 3
+            eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(n)]
+            torch.cuda.synchronize()
+            for i in range(n):
+                flush.zero_()
+                eev[i][0].record(stream)
+                r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp)
+                eev[i][1].record(stream)
+            torch.cuda.synchronize()
+            ems = statistics.mean(a.elapsed_time(b) for a, b in eev)
+            est = r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp, with_stats=True)
+            extras[name] = {"size": f"{ew}x{eh}", "scheme": ecfg.integrator.scheme,
+                            "h": ecfg.integrator.h, "ms_per_frame": ems, "fps": 1e3 / ems,
+                            "steps_per_s": est["total_steps"] / (ems * 1e-3),
+                            "avg_steps_per_ray": est["total_steps"] / (ew * eh),
+                            "kernel": r.last_kernel}
+            del ebuf
+        r.set_config(cfg)
+
     # ---- e2e through the public API with host buffers (rank 0 only, N=1 path)
     e2e = None
     if world == 1:
@@ -363,6 +397,7 @@ def run_b200(args, cfg):
                          "flop_per_launch": flop_launch, "kernel": r.last_kernel},
             "e2e": e2e,
             "shadows": shadows,
+            "workloads": extras,
             "gpu_launches": args.steps * (1 if world == 1 else (2 if rank == 0 else 1)),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

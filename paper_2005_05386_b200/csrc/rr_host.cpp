@@ -397,8 +397,10 @@ std::vector<uint8_t> chebyshev_distance(const std::vector<uint32_t>& masks, int 
 
 int ensure_masks(rr_ctx* c, double h) {
     DevParams& P = *c->P;
+    P.skip = c->opt.o.skip ? 1 : 0;   // Euclid: straight jumps need no grid
     if (P.kind != rr::kBumps || !c->opt.o.cull) {
         P.cull = 0;
+        if (P.kind == rr::kBumps) P.skip = 0;   // no culling grid: no empty cells known
         return RR_OK;
     }
     const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));

@@ -679,6 +679,27 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
         if (!__any_sync(kFull, active)) break;
         uint32_t um = 0;
         int nj = 0;                           // >= 2: this lane jumps nj straight steps
+        if constexpr (KIND == kEuclid) {
+            // Gamma = 0 everywhere: every geodesic is the straight line x + j h y,
+            // so a lane jumps straight to its bounds exit (or its light's
+            // sphere); the chord test finds the hit and its reference step.
+            if (P.skip && active) {
+                const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
+                const float isp = rsqrtf(speed2);
+                float te = 3.0e38f;
+                if (v.x != 0.f) te = fminf(te, ((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x) / v.x);
+                if (v.y != 0.f) te = fminf(te, ((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y) / v.y);
+                if (v.z != 0.f) te = fminf(te, ((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z) / v.z);
+                float L = te * speed2 * isp;
+                if (PASS == kPassShadow) {
+                    const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
+                    L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
+                }
+                const float n = floorf(L * isp / h) - 1.f;
+                nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
+                if (nj < 2) nj = 0;
+            }
+        }
         if constexpr (KIND == kBumps) {
             uint32_t lm = 0;
             unsigned cell = 0;

@@ -164,3 +164,19 @@ def test_march_tail_and_odd_batch_sizes(renderer):
         out = renderer.march(cfg.integrator, z["rays"][:n])
         rep = compare_outcomes(out, z["outcomes"][:n], z["flags"][:n])
         assert rep.ok, (n, rep.summary())
+
+
+@pytest.mark.parametrize("skip", [0, 1])
+def test_straight_jumps_match_stepping(renderer, skip):
+    """Empty-space skipping / Euclidean straight jumps against the golden
+    reference outcomes, with skipping off (every step integrated) and on."""
+    from oracle.parity import compare_outcomes
+    for name in ("ref_grid_euclid", "c2_flat_1080p", "c3_bumps16_1080p", "graph_grid_spheres"):
+        cfg, _, z = load_golden(name)
+        renderer.set_options(skip=skip)
+        renderer.set_config(cfg)
+        out = renderer.march(cfg.integrator, z["rays"])
+        rep = compare_outcomes(out, z["outcomes"], z["flags"])
+        assert rep.ok, (name, skip, rep.summary())
+        assert (out["steps"] == z["outcomes"]["steps"]).mean() > 0.97, name
+    renderer.set_options(skip=1)
