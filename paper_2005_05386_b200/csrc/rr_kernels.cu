@@ -454,30 +454,55 @@ __device__ __noinline__ bool mesh_chord(const DevMesh& M, F3 a, F3 d, float& bes
     return have;
 }
 
+__device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
+    const float dx = fmaxf(fmaxf(n0.x - p.x, p.x - n1.x), 0.f);
+    const float dy = fmaxf(fmaxf(n0.y - p.y, p.y - n1.y), 0.f);
+    const float dz = fmaxf(fmaxf(n0.z - p.z, p.z - n1.z), 0.f);
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
 // Distance from p to the nearest leaf box (capped): no triangle lies closer.
+// Nearest-child-first descent so the bound tightens early.
 __device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
-    float best = cap;
-    int stack[64];
+    float best2 = cap * cap;
+    int stack[48];
+    float sd[48];
     int sp = 0, node = 0;
+    float nd2 = box_dist2(__ldg(M.nodes), __ldg(M.nodes + 1), p);
     for (;;) {
-        const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
-        const float dx = fmaxf(fmaxf(n0.x - p.x, p.x - n1.x), 0.f);
-        const float dy = fmaxf(fmaxf(n0.y - p.y, p.y - n1.y), 0.f);
-        const float dz = fmaxf(fmaxf(n0.z - p.z, p.z - n1.z), 0.f);
-        const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
-        if (dist < best) {
+        if (nd2 < best2) {
+            const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
             if (__float_as_int(n1.w) > 0) {
-                best = dist;
-            } else if (sp < 63) {
-                stack[sp++] = __float_as_int(n0.w);
-                node = node + 1;
+                best2 = nd2;
+            } else {
+                const int l = node + 1, r = __float_as_int(n0.w);
+                const float dl = box_dist2(__ldg(M.nodes + 2 * l), __ldg(M.nodes + 2 * l + 1), p);
+                const float dr = box_dist2(__ldg(M.nodes + 2 * r), __ldg(M.nodes + 2 * r + 1), p);
+                const bool lf = dl <= dr;
+                if (sp < 48) {
+                    stack[sp] = lf ? r : l;
+                    sd[sp] = lf ? dr : dl;
+                    ++sp;
+                }
+                node = lf ? l : r;
+                nd2 = lf ? dl : dr;
                 continue;
             }
         }
-        if (sp == 0) break;
-        node = stack[--sp];
+        // pop the next candidate that can still beat the bound
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (sd[sp] < best2) {
+                node = stack[sp];
+                nd2 = sd[sp];
+                found = true;
+                break;
+            }
+        }
+        if (!found) break;
     }
-    return best;
+    return sqrtf(best2);
 }
 
 // Nearest hit over all primitives; ties keep the lower primitive index
@@ -537,7 +562,7 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
                     mrec = rec;
             }
             float fr = 3.0e38f;
-            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, 8.f));
+            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, 2.f));
             mfree = fr;
         }
     }
