@@ -21,6 +21,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 128;   // 4 warps per CTA
+#ifndef RR_FAST_SINCOS
+#define RR_FAST_SINCOS 1
+#endif
 #ifndef RR_GROUP_TESTS
 #define RR_GROUP_TESTS 1
 #endif
@@ -189,7 +192,11 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
             det = st.det;
         } else if (st.kind == kStageTwist) {                 // diffeo.hpp:143-173
             float sn, cs;
+#if RR_FAST_SINCOS
+            __sincosf(x2, &sn, &cs);   // MUFU.SIN/COS: |z| <= ~10 in chart units
+#else
             sincosf(x2, &sn, &cs);
+#endif
             const float j02 = -(x0 * sn) - x1 * cs;          // d(image_0)/dz
             const float j12 = x0 * cs - x1 * sn;             // d(image_1)/dz
             // w^T H[0] w and w^T H[1] w (H[2] = 0)
