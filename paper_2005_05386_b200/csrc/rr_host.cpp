@@ -82,6 +82,8 @@ struct rr_ctx {
     // culling grid (built lazily for the integrator step length in use)
     uint32_t* d_masks = nullptr;
     uint8_t* d_skip = nullptr;               // Chebyshev distance grid for empty-space skipping
+    uint16_t* d_cull_scratch = nullptr;      // 2 G^3 uint16 for the distance transform passes
+    double* d_cull_gauss = nullptr;          // bump records for the device grid build
     double masks_dilation = -1.0;
     int masks_grid = 0;
     double masks_radius = 0.0;
@@ -326,76 +328,13 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
     P.ambient = (float)sc->ambient;
 }
 
-// Culling grid: bit j of cell c is set when bump j's R-sigma ellipsoid
-// reaches the cell box dilated by `dil` (stage points of a step lie within
-// h of the step's start because unit g-speed implies |y| <= 1 for graph
-// metrics).  Nearest point of an axis-aligned box to the centre, measured in
-// sigma units, decides (exact for axis-aligned ellipsoids).
-std::vector<uint32_t> build_masks(const Compiled& c, const std::vector<int>& slots,
-                                  const DevParams& P, int G, double R, double dil) {
-    std::vector<uint32_t> masks((size_t)G * G * G, 0u);
-    double lo[3], cell[3];
-    for (int k = 0; k < 3; ++k) {
-        lo[k] = P.lo[k];
-        cell[k] = ((double)P.hi[k] - P.lo[k]) / G;
-    }
-    const double R2 = R * R;
-    for (int iz = 0; iz < G; ++iz)
-        for (int iy = 0; iy < G; ++iy)
-            for (int ix = 0; ix < G; ++ix) {
-                const int idx[3] = {ix, iy, iz};
-                uint32_t m = 0;
-                for (size_t j = 0; j < c.gauss.size(); ++j) {
-                    if (slots[j] < 0 || slots[j] >= 32) continue;
-                    const HostGauss& g = c.gauss[j];
-                    double u2 = 0.0;
-                    for (int k = 0; k < 3; ++k) {
-                        // clamp cells at the border extend to infinity (clamped lookups)
-                        const double a = idx[k] == 0 ? -1e30 : lo[k] + idx[k] * cell[k] - dil;
-                        const double b = idx[k] == G - 1 ? 1e30 : lo[k] + (idx[k] + 1) * cell[k] + dil;
-                        const double n = std::min(std::max(g.c[k], a), b);
-                        const double u = (n - g.c[k]) / g.s[k];
-                        u2 += u * u;
-                    }
-                    if (u2 < R2) m |= 1u << slots[j];
-                }
-                masks[((size_t)iz * G + iy) * G + ix] = m;
-            }
-    return masks;
-}
-
-// Chebyshev (26-neighbourhood) distance in cells from every cell to the
-// nearest cell with a non-empty bump mask, capped at 255 (multi-source BFS).
-std::vector<uint8_t> chebyshev_distance(const std::vector<uint32_t>& masks, int G) {
-    std::vector<uint8_t> k(masks.size(), 255);
-    std::vector<int> frontier;
-    for (size_t i = 0; i < masks.size(); ++i)
-        if (masks[i]) {
-            k[i] = 0;
-            frontier.push_back((int)i);
-        }
-    for (int d = 1; d < 255 && !frontier.empty(); ++d) {
-        std::vector<int> next;
-        for (int i : frontier) {
-            const int x = i % G, y = (i / G) % G, z = i / (G * G);
-            for (int dz = -1; dz <= 1; ++dz)
-                for (int dy = -1; dy <= 1; ++dy)
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const int X = x + dx, Y = y + dy, Z = z + dz;
-                        if (X < 0 || Y < 0 || Z < 0 || X >= G || Y >= G || Z >= G) continue;
-                        const int j = (Z * G + Y) * G + X;
-                        if (k[j] == 255) {
-                            k[j] = (uint8_t)d;
-                            next.push_back(j);
-                        }
-                    }
-        }
-        frontier.swap(next);
-    }
-    return k;
-}
-
-int ensure_masks(rr_ctx* c, double h) {
+// Culling grid, built on the device (launch_cull_build) for the integrator
+// step in use: bit j of a cell is set when bump j's R-sigma ellipsoid can reach
+// a stage point of a step starting in the cell (dilation 1.5h: unit g-speed
+// implies |y| <= 1 for graph metrics), plus the Chebyshev distance to the
+// nearest non-empty cell for empty-space skipping.  Rebuilt when the scene or
+// the options change, or h grows; stream-ordered before the march.
+int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
     DevParams& P = *c->P;
     P.skip = c->opt.o.skip ? 1 : 0;   // Euclid: straight jumps need no grid
     if (P.kind != rr::kBumps || !c->opt.o.cull) {
@@ -408,35 +347,52 @@ int ensure_masks(rr_ctx* c, double h) {
     const double dil = 1.5 * h;
     if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil) {
         P.cull = 1;
-        P.skip = c->opt.o.skip ? 1 : 0;
         return RR_OK;
     }
-    const std::vector<uint32_t> m = build_masks(c->prog, c->slots, P, G, R, dil);
-    if (c->d_masks && c->masks_grid != G) {
-        cudaFree(c->d_masks);
+    const size_t cells = (size_t)G * G * G;
+    if (c->masks_grid != G) {
+        if (c->d_masks) cudaFree(c->d_masks);
+        if (c->d_skip) cudaFree(c->d_skip);
+    if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
+    if (c->d_cull_gauss) cudaFree(c->d_cull_gauss);
+        if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
         c->d_masks = nullptr;
-    }
-    if (!c->d_masks) RR_CUDA(c, cudaMalloc(&c->d_masks, m.size() * sizeof(uint32_t)));
-    RR_CUDA(c, cudaMemcpyAsync(c->d_masks, m.data(), m.size() * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, c->stream));
-    const std::vector<uint8_t> k = chebyshev_distance(m, G);
-    if (c->d_skip && c->masks_grid != G) {
-        cudaFree(c->d_skip);
         c->d_skip = nullptr;
+        c->d_cull_scratch = nullptr;
+        RR_CUDA(c, cudaMalloc(&c->d_masks, cells * sizeof(uint32_t)));
+        RR_CUDA(c, cudaMalloc(&c->d_skip, cells));
+        RR_CUDA(c, cudaMalloc(&c->d_cull_scratch, 2 * cells * sizeof(uint16_t)));
+        c->masks_grid = G;
     }
-    if (!c->d_skip) RR_CUDA(c, cudaMalloc(&c->d_skip, k.size()));
-    RR_CUDA(c, cudaMemcpyAsync(c->d_skip, k.data(), k.size(), cudaMemcpyHostToDevice, c->stream));
-    RR_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->masks_grid = G;
+    std::vector<double> g(8 * std::max<size_t>(1, c->prog.gauss.size()), 0.0);
+    int n = 0;
+    for (size_t j = 0; j < c->prog.gauss.size(); ++j) {
+        if (c->slots[j] < 0 || c->slots[j] >= 32) continue;
+        const HostGauss& q = c->prog.gauss[j];
+        double* r = &g[8 * (size_t)n++];
+        for (int k = 0; k < 3; ++k) {
+            r[k] = q.c[k];
+            r[3 + k] = q.s[k];
+        }
+        r[6] = c->slots[j];
+    }
+    if (!c->d_cull_gauss) RR_CUDA(c, cudaMalloc(&c->d_cull_gauss, 8 * 32 * sizeof(double)));
+    RR_CUDA(c, cudaMemcpy(c->d_cull_gauss, g.data(), 8 * (size_t)n * sizeof(double),
+                          cudaMemcpyHostToDevice));
+    double lo[3], cell[3];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = P.lo[k];
+        cell[k] = ((double)P.hi[k] - P.lo[k]) / G;
+    }
+    RR_CUDA(c, rr::launch_cull_build(c->d_cull_gauss, n, G, lo, cell, R, dil, c->d_masks,
+                                     c->d_cull_scratch, c->d_skip, s));
     c->masks_radius = R;
     c->masks_dilation = dil;
     P.cull = 1;
     P.grid = G;
     P.cull_masks = c->d_masks;
     P.skip_k = c->d_skip;
-    P.skip = c->opt.o.skip ? 1 : 0;
-    P.cell_min = (float)std::min({((double)P.hi[0] - P.lo[0]) / G, ((double)P.hi[1] - P.lo[1]) / G,
-                                  ((double)P.hi[2] - P.lo[2]) / G});
+    P.cell_min = (float)std::min({cell[0], cell[1], cell[2]});
     for (int k = 0; k < 3; ++k) {
         P.grid_lo[k] = P.lo[k];
         P.grid_inv[k] = (float)(G / ((double)P.hi[k] - P.lo[k]));
@@ -563,7 +519,7 @@ int ensure_device_buffer(rr_ctx* c, void** buf, size_t* cap, size_t need) {
     return RR_OK;
 }
 
-int check_ready(rr_ctx* c, const rr_integrator* integ) {
+int check_ready(rr_ctx* c, const rr_integrator* integ, cudaStream_t s) {
     if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
     if (!integ || !(integ->h > 0.0)) return set_err(c, RR_ERR_CONFIG, "integrator.h: must be > 0");
     if (integ->max_steps < 1) return set_err(c, RR_ERR_CONFIG, "integrator.max_steps: must be >= 1");
@@ -572,7 +528,7 @@ int check_ready(rr_ctx* c, const rr_integrator* integ) {
     c->P->h = (float)integ->h;
     c->P->max_steps = integ->max_steps;
     c->P->scheme = integ->scheme;
-    return ensure_masks(c, integ->h);
+    return ensure_masks(c, integ->h, s);
 }
 
 // Launch one march over `units` warp units; zeroes counters+stats first.
@@ -703,6 +659,8 @@ void rr_destroy(rr_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->d_masks) cudaFree(c->d_masks);
     if (c->d_skip) cudaFree(c->d_skip);
+    if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
+    if (c->d_cull_gauss) cudaFree(c->d_cull_gauss);
     if (c->d_aux) cudaFree(c->d_aux);
     if (c->h_stats) cudaFreeHost(c->h_stats);
     if (c->d_rays) cudaFree(c->d_rays);
@@ -888,7 +846,7 @@ int rr_march_device(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* d
                     rr_pixel_outcome* d_out, size_t n, void* stream) {
     if (!c) return RR_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(c->mu);
-    int rc = check_ready(c, integ);
+    int rc = check_ready(c, integ, stream ? (cudaStream_t)stream : c->stream);
     if (rc) return rc;
     if (n == 0) return RR_OK;
     if (!d_rays || !d_out) return set_err(c, RR_ERR_CONFIG, "rays/out: required");
@@ -908,7 +866,7 @@ int rr_march(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* rays,
              rr_pixel_outcome* out, size_t n) {
     if (!c) return RR_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(c->mu);
-    int rc = check_ready(c, integ);
+    int rc = check_ready(c, integ, c->stream);
     if (rc) return rc;
     if (n == 0) return RR_OK;
     if (!rays || !out) return set_err(c, RR_ERR_CONFIG, "rays/out: required");
@@ -935,7 +893,7 @@ int rr_render_device(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ
     if (!c) return RR_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(c->mu);
     const double t0 = now_s();
-    int rc = check_ready(c, integ);
+    int rc = check_ready(c, integ, stream ? (cudaStream_t)stream : c->stream);
     if (rc) return rc;
     if (!d_rgb) return set_err(c, RR_ERR_CONFIG, "rgb: required");
     RR_CUDA(c, cudaSetDevice(c->device));
@@ -990,7 +948,7 @@ int rr_render_tiles(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ,
     if (!c) return RR_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(c->mu);
     const double t0 = now_s();
-    int rc = check_ready(c, integ);
+    int rc = check_ready(c, integ, stream ? (cudaStream_t)stream : c->stream);
     if (rc) return rc;
     if (!d_tiles) return set_err(c, RR_ERR_CONFIG, "tiles: required");
     RR_CUDA(c, cudaSetDevice(c->device));

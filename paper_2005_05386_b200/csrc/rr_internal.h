@@ -16,6 +16,13 @@ namespace rr {
 cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream,
                          int num_sms, const char** kernel_name);
 
+// Builds the culling grid (bump masks + Chebyshev distances) on the device:
+// d_gauss holds n records {cx, cy, cz, sigma_x, sigma_y, sigma_z, slot, pad}.
+// scratch needs 2*G^3 uint16.  4 launches on `s`.
+cudaError_t launch_cull_build(const double* d_gauss, int n, int G, const double lo[3],
+                              const double cell[3], double R, double dil, uint32_t* masks,
+                              uint16_t* scratch, uint8_t* skip, cudaStream_t s);
+
 // Reassembles a row-major frame from gathered tile-major shard buffers.
 cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int tile_w,
                           int tile_h, int n_shards, int max_tiles_per_shard, uint8_t* rgb,

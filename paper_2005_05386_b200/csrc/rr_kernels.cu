@@ -1117,6 +1117,61 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Culling grid build on the device (per scene upload, e.g. every animation
+// frame).  Cell c gets bit slot(j) when bump j's R-sigma ellipsoid reaches the
+// cell box dilated by `dil` (nearest point of the box to the centre, in sigma
+// units; border cells extend to infinity because lookups clamp).  FP64, same
+// test as the host reference implementation it replaced.
+__global__ void cull_mask_kernel(const double* __restrict__ g, int n, int G, double lo0, double lo1,
+                                 double lo2, double c0, double c1, double c2, double R2, double dil,
+                                 uint32_t* __restrict__ masks) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * G * G) return;
+    const int ix = idx % G, iy = (idx / G) % G, iz = idx / (G * G);
+    const int id[3] = {ix, iy, iz};
+    const double lo[3] = {lo0, lo1, lo2}, cell[3] = {c0, c1, c2};
+    uint32_t m = 0;
+    for (int j = 0; j < n; ++j) {
+        const double* b = g + 8 * j;   // cx, cy, cz, sx, sy, sz, slot, pad
+        double u2 = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double a = id[k] == 0 ? -1e30 : lo[k] + id[k] * cell[k] - dil;
+            const double e = id[k] == G - 1 ? 1e30 : lo[k] + (id[k] + 1) * cell[k] + dil;
+            const double nr = fmin(fmax(b[k], a), e);
+            const double u = (nr - b[k]) / b[3 + k];
+            u2 += u * u;
+        }
+        if (u2 < R2) m |= 1u << (int)b[6];
+    }
+    masks[idx] = m;
+}
+
+// One separable pass of the Chebyshev (L-inf) distance transform along axis
+// `ax`: out(x) = min_y max(|x - y|, in(y)) over the grid line through x.
+// Pass 0 reads the masks (0 where non-empty, infinity elsewhere).
+__global__ void cheb_pass_kernel(const uint32_t* __restrict__ masks, const uint16_t* __restrict__ in,
+                                 uint16_t* __restrict__ out, uint8_t* __restrict__ out8, int G, int ax) {
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= G * G) return;
+    const int a = line % G, b = line / G;
+    int stride, base;
+    if (ax == 0) { stride = 1; base = (b * G + a) * G; }
+    else if (ax == 1) { stride = G; base = b * G * G + a; }
+    else { stride = G * G; base = b * G + a; }
+    for (int x = 0; x < G; ++x) {
+        int best = 0x7fff;
+        for (int y = 0; y < G; ++y) {
+            const int v = masks ? (masks[base + y * stride] ? 0 : 0x7fff) : in[base + y * stride];
+            const int d = max(abs(x - y), v);
+            best = min(best, d);
+        }
+        if (out8) out8[base + x * stride] = (uint8_t)min(best, 255);
+        else out[base + x * stride] = (uint16_t)best;
+    }
+}
+
 __global__ void detile_kernel(const uint8_t* __restrict__ g, int width, int height, int tw, int th,
                               int n_shards, int max_k, int tiles_x, uint8_t* __restrict__ rgb) {
     const int px = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1235,6 +1290,19 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
     if (L.n_units == 0) return cudaSuccess;
     return P.scheme == 0 ? dispatch_scheme<0>(P, L, stream, num_sms, kernel_name)
                          : dispatch_scheme<1>(P, L, stream, num_sms, kernel_name);
+}
+
+cudaError_t launch_cull_build(const double* d_gauss, int n, int G, const double lo[3],
+                              const double cell[3], double R, double dil, uint32_t* masks,
+                              uint16_t* scratch, uint8_t* skip, cudaStream_t s) {
+    const int cells = G * G * G;
+    cull_mask_kernel<<<(cells + 255) / 256, 256, 0, s>>>(d_gauss, n, G, lo[0], lo[1], lo[2], cell[0],
+                                                          cell[1], cell[2], R * R, dil, masks);
+    const int lines = G * G;
+    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(masks, nullptr, scratch, nullptr, G, 0);
+    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(nullptr, scratch, scratch + cells, nullptr, G, 1);
+    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(nullptr, scratch + cells, nullptr, skip, G, 2);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int tile_w, int tile_h,
