@@ -160,6 +160,7 @@ struct DevLaunch {
     int tiles_x;                  // tiles per frame row
     int micro_per_tile;           // (tile_w/8)*(tile_h/4)
     unsigned n_units;             // warp units of this launch
+    int lpp;                      // shadow pass: lights marched per pixel in one unit (1/2/4)
     uint8_t* rgb;                 // frame (row-major) or tile-major buffer
     const double* rays;           // RAYS: 6 doubles per ray (RayStart)
     uint8_t* outcomes;            // RAYS: 48-byte PixelOutcome records

@@ -1005,13 +1005,18 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                 pos = dir = f3(0.f, 0.f, 0.f);
             }
         } else {
-            tile_k = unit / L.micro_per_tile;
-            const unsigned micro = unit % L.micro_per_tile;
+            // shadow pass: a unit is 32/lpp pixels of a micro-tile x lpp lights
+            const unsigned mt = PASS == kPassShadow ? unit / L.lpp : unit;
+            const int sub = PASS == kPassShadow ? (int)(unit % L.lpp) : 0;
+            const int ppu = PASS == kPassShadow ? kUnit / L.lpp : kUnit;
+            const int idx = sub * ppu + lane % ppu;          // pixel within the micro-tile
+            tile_k = mt / L.micro_per_tile;
+            const unsigned micro = mt % L.micro_per_tile;
             const unsigned tile = L.shard + (unsigned)tile_k * L.n_shards;
             const int tx = tile % L.tiles_x, ty = tile / L.tiles_x;
             const int mpr = L.tile_w / kMicroW;
-            lx = (micro % mpr) * kMicroW + (lane & 7);
-            ly = (micro / mpr) * kMicroH + (lane >> 3);
+            lx = (micro % mpr) * kMicroW + (idx & 7);
+            ly = (micro / mpr) * kMicroH + (idx >> 3);
             px = tx * L.tile_w + lx;
             py = ty * L.tile_h + ly;
             live = px < L.width && py < L.height;
@@ -1026,20 +1031,26 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
 
         LaneCounters cnt{0u, 0u};
         unsigned ref_steps = 0, errs = 0, shadow_steps = 0;
+        bool pad_writer = true;
         if constexpr (PASS == kPassShadow) {
-            // ---- EXTENSION: shadow geodesics for this unit's hits, light by light
+            // ---- EXTENSION: shadow geodesics.  Lane = (pixel, light): lpp lights
+            // of 32/lpp pixels march together; contributions are summed across
+            // the lanes of a pixel; light groups beyond lpp loop.
+            const int ppu = kUnit / L.lpp;
+            const int li = lane / ppu;
             HitRec hr{};
             if (live) hr = L.hits[pix];
             const bool hit = live && (hr.status == 1);
             const F3 q = f3(hr.p[0], hr.p[1], hr.p[2]);
             const F3 n = f3(hr.n[0], hr.n[1], hr.n[2]);
-            float light = P.ambient;
-            for (int l = 0; l < P.n_lights; ++l) {
-                const DevLight& Lt = P.lights[l];
+            float contrib = 0.f;
+            for (int lg = 0; lg < P.n_lights; lg += L.lpp) {
+                const int l = lg + li;
+                const DevLight& Lt = P.lights[l < P.n_lights ? l : 0];
                 const F3 D = f3(Lt.pos[0] - q.x, Lt.pos[1] - q.y, Lt.pos[2] - q.z);
                 const float dist2 = D.x * D.x + D.y * D.y + D.z * D.z;
                 const float lam = (n.x * D.x + n.y * D.y + n.z * D.z) * rsqrtf(dist2);
-                bool want = hit && lam > 0.f;
+                bool want = hit && l < P.n_lights && lam > 0.f;
                 F3 x0 = f3(0.f, 0.f, 0.f), v0 = f3(0.f, 0.f, 0.f);
                 if (want) {
                     x0 = f3(fmaf(kShadowEps, n.x, q.x), fmaf(kShadowEps, n.y, q.y),
@@ -1055,12 +1066,15 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                 }
                 const RayResult sr = march_unit<KIND, NB, SCHEME, kPassShadow, MESH>(P, want, x0, v0, cnt, q, dist2);
                 if (want) shadow_steps += (unsigned)sr.steps;   // reference-equivalent steps
-                if (want && sr.status == 1) light = fmaf(Lt.intensity, lam, light);
+                if (want && sr.status == 1) contrib = fmaf(Lt.intensity, lam, contrib);
             }
-            if (live) {
+            // sum over the lanes of a pixel (same lane % ppu), in light order
+            for (int o = ppu; o < kUnit; o <<= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
+            if (live && li == 0) {
                 RayResult r{hr.status, 0, 0, hr.t, q, n};
-                shade(P, r, L.rgb + 3 * pix, light);
+                shade(P, r, L.rgb + 3 * pix, P.ambient + contrib);
             }
+            pad_writer = li == 0;     // one writer per pixel for the tile padding
         } else {
             const RayResult r = march_unit<KIND, NB, SCHEME, PASS, MESH>(P, live, pos, dir, cnt);
             ref_steps = live ? (unsigned)r.steps : 0u;
@@ -1095,7 +1109,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                 dst[0] = dst[1] = dst[2] = 0;
             }
         }
-        if (PASS == kPassShadow && !live && L.mode == kModeTiles) {
+        if (PASS == kPassShadow && !live && pad_writer && L.mode == kModeTiles) {
             uint8_t* dst = L.rgb + 3 * pix;
             dst[0] = dst[1] = dst[2] = 0;
         }
@@ -1238,6 +1252,11 @@ cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t 
     if (e != cudaSuccess) return e;
     DevLaunch L2 = L;
     L2.counter = L.counter + 1;
+    // lights per pixel marched in one unit: 1.  Pairing 2 lights x 16 pixels per
+    // warp was measured slower on C3 (27.2 vs 23.7 ms/frame): two light
+    // directions in one warp widen the culling union and split coherence.
+    L2.lpp = 1;
+    L2.n_units = L.n_units * L2.lpp;
     return launch_pass<KIND, NB, SCHEME, kPassShadow, MESH>(P, L2, s, num_sms);
 }
 
