@@ -353,8 +353,6 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
     if (c->masks_grid != G) {
         if (c->d_masks) cudaFree(c->d_masks);
         if (c->d_skip) cudaFree(c->d_skip);
-    if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
-    if (c->d_cull_gauss) cudaFree(c->d_cull_gauss);
         if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
         c->d_masks = nullptr;
         c->d_skip = nullptr;
