@@ -375,6 +375,9 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
         r[6] = c->slots[j];
     }
     if (!c->d_cull_gauss) RR_CUDA(c, cudaMalloc(&c->d_cull_gauss, 8 * 32 * sizeof(double)));
+    // a previous grid build on `s` may still read the records: order the copy
+    // after it (scene changes only; static scenes never get here)
+    RR_CUDA(c, cudaStreamSynchronize(s));
     RR_CUDA(c, cudaMemcpy(c->d_cull_gauss, g.data(), 8 * (size_t)n * sizeof(double),
                           cudaMemcpyHostToDevice));
     double lo[3], cell[3];
