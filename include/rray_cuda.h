@@ -83,7 +83,8 @@ enum {
     RR_DIFFEO_AFFINE = 1,
     RR_DIFFEO_TWIST = 2,
     RR_DIFFEO_LOCAL_BUMP = 3,
-    RR_DIFFEO_COMPOSE = 4
+    RR_DIFFEO_COMPOSE = 4,
+    RR_DIFFEO_BEND = 5      /* EXTENSION: Barr bend about z, angle = curvature * x (see rro.c) */
 };
 
 typedef struct rr_diffeo_node {       /* one DiffeoExpr node */
@@ -95,6 +96,7 @@ typedef struct rr_diffeo_node {       /* one DiffeoExpr node */
     rr_vec3 offset;                   /* AFFINE */
     rr_gaussian bump;                 /* LOCAL_BUMP: Phi(p) = p + f(p) * direction */
     rr_vec3 direction;                /* LOCAL_BUMP */
+    double curvature;                 /* BEND (EXTENSION) */
 } rr_diffeo_node;
 
 /* ---- metric fields (metric.hpp:20-49) ------------------------------------ */

@@ -300,6 +300,25 @@ static DiffeoEval eval_diffeo(const rr_metric_desc* m, int node, V3 p) {
             ev.validity = fabs(m3_det(&o->jacobian));
             return ev;
         }
+        case RR_DIFFEO_BEND: {   /* EXTENSION: Barr bend, theta = k x, c = 1/k (no reference counterpart)
+                                  * Phi = (-sin(theta)(y - c), cos(theta)(y - c) + c, z), det J = 1 - k y */
+            const double k = d->curvature, cc = 1.0 / k, th = k * p.x;
+            const double sn = sin(th), cs = cos(th), yc = p.y - cc;
+            DiffeoSample* o = &ev.sample;
+            o->image = v3(-sn * yc, cs * yc + cc, p.z);
+            o->jacobian = m3_identity();
+            o->jacobian.m[0][0] = -k * cs * yc;
+            o->jacobian.m[0][1] = -sn;
+            o->jacobian.m[1][0] = -k * sn * yc;
+            o->jacobian.m[1][1] = cs;
+            o->second = t3_zero();
+            o->second.s[0].xx = k * k * sn * yc;
+            o->second.s[0].xy = -k * cs;
+            o->second.s[1].xx = -k * k * cs * yc;
+            o->second.s[1].xy = -k * sn;
+            ev.validity = fabs(m3_det(&o->jacobian));
+            return ev;
+        }
         case RR_DIFFEO_LOCAL_BUMP: {                                            /* :175-193 */
             const ScalarSample f = eval_gaussian(&d->bump, p);
             const V3 v = vfrom(d->direction);

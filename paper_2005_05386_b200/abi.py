@@ -16,7 +16,7 @@ RR_OK, RR_ERR_CONFIG, RR_ERR_NUMERIC, RR_ERR_IO, RR_ERR_DEVICE = 0, 1, 2, 3, 4
 
 RR_FIELD_GAUSSIAN, RR_FIELD_POLYNOMIAL, RR_FIELD_SUM = 0, 1, 2
 (RR_DIFFEO_IDENTITY, RR_DIFFEO_AFFINE, RR_DIFFEO_TWIST, RR_DIFFEO_LOCAL_BUMP,
- RR_DIFFEO_COMPOSE) = 0, 1, 2, 3, 4
+ RR_DIFFEO_COMPOSE, RR_DIFFEO_BEND) = 0, 1, 2, 3, 4, 5
 RR_METRIC_EUCLIDEAN, RR_METRIC_GRAPH, RR_METRIC_DIFFEO = 0, 1, 2
 RR_PRIM_GRID_PLANES, RR_PRIM_SPHERE, RR_PRIM_HALF_SPACE, RR_PRIM_MESH = 0, 1, 2, 3
 RR_SCHEME_EULER, RR_SCHEME_RK4 = 0, 1
@@ -54,7 +54,7 @@ class rr_field_node(C.Structure):
 class rr_diffeo_node(C.Structure):
     _fields_ = [("kind", C.c_int32), ("first", C.c_int32), ("count", C.c_int32),
                 ("pad_", C.c_int32), ("matrix", (C.c_double * 3) * 3), ("offset", rr_vec3),
-                ("bump", rr_gaussian), ("direction", rr_vec3)]
+                ("bump", rr_gaussian), ("direction", rr_vec3), ("curvature", C.c_double)]
 
 
 class rr_metric_desc(C.Structure):
@@ -131,7 +131,7 @@ OUTCOME_DTYPE = np.dtype({
 # Expected C sizes (checked against the header in tests/test_abi.py).
 EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
-    "rr_field_node": 72, "rr_diffeo_node": 192, "rr_metric_desc": 56,
+    "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
     "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 16,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 72,
     "rr_options": 32,

@@ -9,6 +9,7 @@ ValidationError/ParseError naming the same key.  One superset key is accepted
     scene.lights: [{"position": [x,y,z], "intensity": I}]   point lights for
                    shadow geodesics; absent/empty = reference shading.
     scene.ambient: ambient term of the lit shading (default 0.2).
+    metric.map (any level) = {"kind": "bend", "curvature": k}   Barr bend about z.
     scene.primitives[i] = {"kind": "mesh", "vertices": [...], "triangles": [...]}
                    or {"kind": "mesh", "generator": {"kind": "torus", ...}}
                    triangle meshes (BVH-accelerated on the GPU).
@@ -80,6 +81,11 @@ class TwistMap:
 
 
 @dataclass
+class BendMap:                        # EXTENSION: Barr bend, angle = curvature * x
+    curvature: float = 0.1
+
+
+@dataclass
 class LocalBumpMap:                   # diffeo.hpp:80-86
     bump: GaussianParams
     direction: Vec3
@@ -90,7 +96,7 @@ class ComposeMap:                     # maps[0] is the outermost map (diffeo.hpp
     maps: list
 
 
-Diffeo = Union[IdentityMap, AffineMap, TwistMap, LocalBumpMap, ComposeMap]
+Diffeo = Union[IdentityMap, AffineMap, TwistMap, LocalBumpMap, ComposeMap, BendMap]
 
 
 @dataclass
@@ -363,8 +369,14 @@ def _parse_field(o, path) -> ScalarField:                        # :154-196
     _fail(path + ".kind", f"must be one of gaussian|polynomial|sum, got '{kind}'")
 
 
-def _parse_diffeo(o, path) -> Diffeo:                             # :198-244
+def _parse_diffeo(o, path, allow_ext: bool = True) -> Diffeo:     # :198-244
     kind = _get_string_or(o, path, "kind", "")
+    if kind == "bend" and allow_ext:                                # EXTENSION
+        _check_keys(o, path, {"kind", "curvature"})
+        b = BendMap(_get_double(o, path, "curvature"))
+        if not (b.curvature != 0.0 and math.isfinite(b.curvature)):
+            _fail(path + ".curvature", "must be nonzero")
+        return b
     if kind == "identity":
         _check_keys(o, path, {"kind"})
         return IdentityMap()
@@ -395,12 +407,12 @@ def _parse_diffeo(o, path) -> Diffeo:                             # :198-244
         maps = o.get("maps")
         if not isinstance(maps, list) or not maps:
             _fail(path + ".maps", "required non-empty array")
-        return ComposeMap([_parse_diffeo(m, f"{path}.maps[{i}]") for i, m in enumerate(maps)])
+        return ComposeMap([_parse_diffeo(m, f"{path}.maps[{i}]", allow_ext) for i, m in enumerate(maps)])
     _fail(path + ".kind",
           f"must be one of identity|affine|twist|local_bump|compose, got '{kind}'")
 
 
-def _parse_metric(o, path) -> Metric:                             # :246-265
+def _parse_metric(o, path, allow_ext: bool = True) -> Metric:     # :246-265
     kind = _get_string_or(o, path, "kind", "") if isinstance(o, dict) else ""
     if not isinstance(o, dict):
         _fail(path, "must be an object")
@@ -416,7 +428,7 @@ def _parse_metric(o, path) -> Metric:                             # :246-265
         _check_keys(o, path, {"kind", "map"})
         if "map" not in o:
             _fail(path + ".map", "required")
-        return DiffeoMetric(_parse_diffeo(o["map"], path + ".map"))
+        return DiffeoMetric(_parse_diffeo(o["map"], path + ".map", allow_ext))
     _fail(path + ".kind", f"must be one of euclidean|graph|diffeo, got '{kind}'")
 
 
@@ -607,7 +619,7 @@ def parse_config(text: str, allow_ext: bool = True) -> RunConfig:  # :437-456
     if "metric" not in root:
         _fail("config.metric", "required")
     cfg = RunConfig()
-    cfg.metric = _parse_metric(root["metric"], "metric")
+    cfg.metric = _parse_metric(root["metric"], "metric", allow_ext)
     cfg.scene = _parse_scene(root.get("scene"), "scene", allow_ext)
     cfg.camera = _parse_camera(root.get("camera"), "camera")
     cfg.integrator = _parse_integrator(root.get("integrator"), "integrator")
@@ -644,6 +656,8 @@ def _diffeo_json(d):
         return {"kind": "affine", "matrix": [list(r) for r in d.matrix], "offset": list(d.offset)}
     if isinstance(d, TwistMap):
         return {"kind": "twist"}
+    if isinstance(d, BendMap):
+        return {"kind": "bend", "curvature": d.curvature}
     if isinstance(d, LocalBumpMap):
         return {"kind": "local_bump", "amplitude": d.bump.amplitude, "center": list(d.bump.center),
                 "sigma": list(d.bump.sigma), "direction": list(d.direction)}
@@ -769,6 +783,9 @@ class MetricDesc:
             node.offset = abi.rr_vec3.of(d.offset)
         elif isinstance(d, TwistMap):
             node.kind = abi.RR_DIFFEO_TWIST
+        elif isinstance(d, BendMap):
+            node.kind = abi.RR_DIFFEO_BEND
+            node.curvature = float(d.curvature)
         elif isinstance(d, LocalBumpMap):
             node.kind = abi.RR_DIFFEO_LOCAL_BUMP
             node.bump = self._gauss(d.bump)

@@ -38,6 +38,7 @@ struct HostPoly {
 };
 struct HostStage {
     int kind;                      // rr::Stage
+    double k = 0.0;                // bend curvature
     double m[9], off[3];           // affine
     HostGauss g;                   // bump
     double dir[3];                 // bump
@@ -178,6 +179,12 @@ void flatten_diffeo(const rr_metric_desc* m, int node, int depth, Compiled& out)
         case RR_DIFFEO_TWIST:
             st.kind = rr::kStageTwist;
             break;
+        case RR_DIFFEO_BEND:
+            if (!(d.curvature != 0.0) || !std::isfinite(d.curvature))
+                throw CompileError{RR_ERR_CONFIG, "metric.map.curvature: must be nonzero"};
+            st.kind = rr::kStageBend;
+            st.k = d.curvature;
+            break;
         case RR_DIFFEO_LOCAL_BUMP: {
             const rr_gaussian& g = d.bump;
             if (!(g.sigma.x > 0.0 && g.sigma.y > 0.0 && g.sigma.z > 0.0))
@@ -260,6 +267,9 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
             for (int k = 0; k < 9; ++k) d.v[k] = (float)s.m[k];
             for (int k = 0; k < 3; ++k) d.v[9 + k] = (float)s.off[k];
             d.det = (float)det3(s.m);
+        } else if (s.kind == rr::kStageBend) {
+            d.v[0] = (float)s.k;
+            d.v[1] = (float)(1.0 / s.k);
         } else if (s.kind == rr::kStageBump) {
             for (int k = 0; k < 3; ++k) {
                 d.v[k] = (float)s.g.c[k];
@@ -441,6 +451,14 @@ int metric_tensor(const Compiled& c, const double p[3], double g[6], std::string
             if (s.kind == rr::kStageAffine) {
                 std::memcpy(Js, s.m, sizeof Js);
                 for (int i = 0; i < 3; ++i) img[i] = s.m[3 * i] * x[0] + s.m[3 * i + 1] * x[1] + s.m[3 * i + 2] * x[2] + s.off[i];
+            } else if (s.kind == rr::kStageBend) {
+                const double c = 1.0 / s.k, th = s.k * x[0], sn = std::sin(th), cs = std::cos(th);
+                const double yc = x[1] - c;
+                const double t[9] = {-s.k * cs * yc, -sn, 0, -s.k * sn * yc, cs, 0, 0, 0, 1};
+                std::memcpy(Js, t, sizeof Js);
+                img[0] = -sn * yc;
+                img[1] = cs * yc + c;
+                img[2] = x[2];
             } else if (s.kind == rr::kStageTwist) {
                 const double cs = std::cos(x[2]), sn = std::sin(x[2]);
                 const double t[9] = {cs, -sn, -(x[0] * sn) - x[1] * cs, sn, cs, x[0] * cs - x[1] * sn, 0, 0, 1};

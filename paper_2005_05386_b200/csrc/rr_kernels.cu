@@ -218,6 +218,31 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
             x0 = j12;                                         // x c - y s
             x1 = -j02;                                        // x s + y c
             det = cs * cs + sn * sn;
+        } else if (st.kind == kStageBend) {                   // EXTENSION (oracle/rro.c)
+            const float k = st.v[0], c = st.v[1];
+            float sn, cs;
+            __sincosf(k * x0, &sn, &cs);
+            const float yc = x1 - c;
+            const float j00 = -k * cs * yc, j10 = -k * sn * yc;   // j01 = -sn, j11 = cs
+            const float wxx = w0 * w0, wxy = 2.f * w0 * w1;
+            const float d0 = wxx * (k * k * sn * yc) - wxy * (k * cs);
+            const float d1 = -wxx * (k * k * cs * yc) - wxy * (k * sn);
+            const float a0 = d0 + j00 * q0 - sn * q1;
+            const float a1 = d1 + j10 * q0 + cs * q1;
+            q0 = a0; q1 = a1;
+            const float b0 = j00 * w0 - sn * w1;
+            const float b1 = j10 * w0 + cs * w1;
+            w0 = b0; w1 = b1;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const float r0 = j00 * J[cc] - sn * J[3 + cc];
+                const float r1 = j10 * J[cc] + cs * J[3 + cc];
+                J[cc] = r0;
+                J[3 + cc] = r1;
+            }
+            x0 = -sn * yc;
+            x1 = fmaf(cs, yc, c);
+            det = -k * yc;
         } else {                                              // diffeo.hpp:175-193
             const float* b = st.v;
             const float ux = (x0 - b[0]) * b[3], uy = (x1 - b[1]) * b[4], uz = (x2 - b[2]) * b[5];
@@ -911,6 +936,17 @@ __device__ void metric_at(const DevParams& P, F3 x, float g[6], bool& ok) {
                 Js[6] = 0.f; Js[7] = 0.f; Js[8] = 1.f;
                 n0 = x0 * cs - x1 * sn;
                 n1 = x0 * sn + x1 * cs;
+                n2 = x2;
+            } else if (st.kind == kStageBend) {
+                const float k = st.v[0], c = st.v[1];
+                float sn, cs;
+                __sincosf(k * x0, &sn, &cs);
+                const float yc = x1 - c;
+                Js[0] = -k * cs * yc; Js[1] = -sn; Js[2] = 0.f;
+                Js[3] = -k * sn * yc; Js[4] = cs; Js[5] = 0.f;
+                Js[6] = 0.f; Js[7] = 0.f; Js[8] = 1.f;
+                n0 = -sn * yc;
+                n1 = fmaf(cs, yc, c);
                 n2 = x2;
             } else {
                 const float* b = st.v;

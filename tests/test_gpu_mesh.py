@@ -65,3 +65,24 @@ def test_mesh_with_shadows(renderer, oracle_lib):
     cam = renderer.build_camera(cfg.camera)
     rgb, _ = renderer.render(cam, cfg.integrator, w, h)
     assert compare_rgb(rgb, ref_rgb, flags).ok
+
+
+@pytest.mark.parametrize("metric", [
+    {"kind": "diffeo", "map": {"kind": "bend", "curvature": 0.12}},
+    {"kind": "diffeo", "map": {"kind": "compose", "maps": [{"kind": "twist"},
+                                                           {"kind": "bend", "curvature": 0.08}]}},
+])
+def test_bend_deformation_parity(renderer, oracle_lib, metric):
+    """EXTENSION: Barr bend (north star "twist/bend deformation") vs the FP64 oracle."""
+    from oracle.parity import compare_outcomes, compare_rgb
+    cfg = mesh_cfg(40, 24, metric, h=0.02, max_steps=1000)
+    w, h = 96, 54
+    ref_rgb, ref_out, _, flags = oracle_lib.render(cfg, w, h, with_flags=True)
+    renderer.set_config(cfg)
+    cam = renderer.build_camera(cfg.camera)
+    rgb, _ = renderer.render(cam, cfg.integrator, w, h)
+    rays = oracle_lib.primary_rays(oracle_lib.camera(cfg), w, h)
+    out = renderer.march(cfg.integrator, rays)
+    rep = compare_outcomes(out, ref_out, flags)
+    rep = compare_rgb(rgb, ref_rgb, flags, rep)
+    assert rep.ok, rep.summary() + " " + "; ".join(rep.details)

@@ -47,3 +47,27 @@ def test_mesh_hit_points_on_triangles(oracle_lib):
     for p in hits["point"][:50]:
         dist = np.abs(((p - v[:, 0]) * n).sum(1))
         assert dist.min() < 1e-9
+
+
+def test_bend_pullback_geodesics_are_straight(oracle_lib):
+    """EXTENSION bend: Phi maps geodesics of g = J^T J to straight lines (the
+    reference's pull-back straightness property, verify.cpp:233-261)."""
+    cfg = parse_config(json.dumps({"metric": {"kind": "diffeo", "map": {"kind": "bend",
+                                                                        "curvature": 0.15}},
+                                   "integrator": {"scheme": "rk4"}}))
+    k = 0.15
+
+    def phi(p):
+        c = 1 / k
+        th = k * p[0]
+        return np.array([-np.sin(th) * (p[1] - c), np.cos(th) * (p[1] - c) + c, p[2]])
+    st = [0.5, 0.4, 0.6, 0.8, 0.3, 0.2]
+    pts = [phi(np.array(st[:3]))]
+    for _ in range(200):
+        st, val = oracle_lib.step(cfg, st, 0.01)
+        assert val > 1e-14
+        pts.append(phi(np.array(st[:3])))
+    P = np.array(pts)
+    d = (P[-1] - P[0]) / np.linalg.norm(P[-1] - P[0])
+    dev = np.linalg.norm((P - P[0]) - np.outer((P - P[0]) @ d, d), axis=1).max()
+    assert dev < 1e-10
