@@ -55,6 +55,8 @@ def parse_args():
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-shadows", action="store_true")
+    p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                   help="gloo: host-synchronised collectives (dry runs of the N>1 path on fewer GPUs)")
     p.add_argument("--no-extras", action="store_true",
                    help="skip the secondary BASELINE workloads (C1, C2, C4+mesh, C5 4K)")
     p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
@@ -202,9 +204,15 @@ def run_b200(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    gloo = args.dist_backend == "gloo"
+    cdev = "cpu" if gloo else "cuda"     # device of the collectives' tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w, h = cfg.output.width, cfg.output.height
     integ = cfg.integrator
     r = Renderer(local)
@@ -219,7 +227,29 @@ def run_b200(args, cfg):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
     frame = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+    exchange = None
     if world > 1:
+        # Fused render + exchange (default): rank 0 shares its frame through a
+        # CUDA-IPC handle; every rank's shade epilogue stores its tiles straight
+        # into it over NVLink/NVSwitch; one tiny NCCL all-reduce per frame is
+        # the completion barrier.  Fallback: tile buffers + one NCCL gather +
+        # detile on rank 0.
+        exchange = "p2p-epilogue"
+        target = frame
+        try:
+            from torch.multiprocessing.reductions import reduce_tensor
+            payload = [reduce_tensor(frame)] if rank == 0 else [None]
+            dist.broadcast_object_list(payload, src=0)
+            if rank != 0:
+                fn, fargs = payload[0]
+                target = fn(*fargs)
+            ok = torch.tensor([1], device=cdev)
+        except Exception:
+            ok = torch.tensor([0], device=cdev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 or gloo:
+            exchange = "p2p-epilogue" if int(ok.item()) else "nccl-gather"
+        done = torch.zeros(1, device=cdev)
         max_k = r.shard_tile_count(w, h, TILE, TILE, 0, world)
         tiles = torch.zeros(max_k * TILE * TILE * 3, dtype=torch.uint8, device="cuda")
         gathered = torch.empty((world, tiles.numel()), dtype=torch.uint8, device="cuda") if rank == 0 else None
@@ -227,9 +257,21 @@ def run_b200(args, cfg):
     def one_frame():
         if world == 1:
             r.render_device(cam, integ, w, h, frame, stream=sp)
+        elif exchange == "p2p-epilogue":
+            r.render_shard(cam, integ, w, h, TILE, TILE, rank, world, target, stream=sp)
+            if gloo:
+                torch.cuda.synchronize()
+            dist.all_reduce(done)     # completion barrier: rank 0's frame is whole after it
         else:
             r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp)
-            dist.gather(tiles, list(gathered.unbind(0)) if rank == 0 else None, dst=0)
+            if gloo:
+                torch.cuda.synchronize()
+                g_cpu = [torch.empty_like(tiles, device="cpu") for _ in range(world)] if rank == 0 else None
+                dist.gather(tiles.cpu(), g_cpu, dst=0)
+                if rank == 0:
+                    gathered.copy_(torch.stack(g_cpu))
+            else:
+                dist.gather(tiles, list(gathered.unbind(0)) if rank == 0 else None, dst=0)
             if rank == 0:
                 r.detile(gathered, w, h, TILE, TILE, world, frame, stream=sp)
 
@@ -255,7 +297,7 @@ def run_b200(args, cfg):
     times_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(times_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
@@ -265,8 +307,8 @@ def run_b200(args, cfg):
     else:
         st = r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp,
                             with_stats=True)
-        keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors"]
-        t = torch.tensor([st[k] for k in keys], dtype=torch.float64, device="cuda")
+        keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors", "lane_slots"]
+        t = torch.tensor([st[k] for k in keys], dtype=torch.float64, device=cdev)
         dist.all_reduce(t)
         st.update({k: int(v) for k, v in zip(keys, t.tolist())})
     steps_per_frame = st["total_steps"]
@@ -310,6 +352,8 @@ def run_b200(args, cfg):
                                   (statistics.mean(sms) * 1e-3),
                    "achieved_tflops": algorithmic_flops(sst, integ.scheme) /
                                       (statistics.mean(sms) * 1e-3) / 1e12,
+                   "simt_efficiency_shadow": (sst["integrated_steps"] - st["integrated_steps"]) /
+                                             max(1, sst["shadow_lane_slots"]),
                    "launches_per_frame": sst["kernel_launches"]}
         r.set_config(cfg)
 
@@ -384,6 +428,7 @@ def run_b200(args, cfg):
             "config": {"workload": WORKLOAD, "width": w, "height": h, "bumps": 16,
                        "scheme": integ.scheme, "h": integ.h, "max_steps": integ.max_steps,
                        "shadows": False, "tile": TILE if world > 1 else None,
+                       "exchange": exchange,
                        "l2": "flushed between frames (256 MB write, untimed)",
                        "parallelism": f"tiles{world}"},
             "fps": fps,
@@ -398,7 +443,8 @@ def run_b200(args, cfg):
             "e2e": e2e,
             "shadows": shadows,
             "workloads": extras,
-            "gpu_launches": args.steps * (1 if world == 1 else (2 if rank == 0 else 1)),
+            "gpu_launches": args.steps * (1 if world == 1 or exchange == "p2p-epilogue" else 2),
+            "simt_efficiency": {"primary": st["integrated_steps"] / max(1, st["lane_slots"])},
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

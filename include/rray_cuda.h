@@ -210,6 +210,8 @@ typedef struct rr_stats {
     int64_t bump_evals;               /* Gaussian-term evaluations executed (N_eff accounting) */
     int64_t shadow_steps;             /* steps spent on shadow geodesics (EXT) */
     int64_t kernel_launches;          /* launches issued by the call */
+    int64_t lane_slots;               /* primary: warp loop iterations x 32 (SIMT efficiency = integrated / slots) */
+    int64_t shadow_lane_slots;        /* same for the shadow pass (EXT) */
 } rr_stats;
 
 /* ---- tuning knobs (extension; defaults are parity-safe) ------------------- */
@@ -279,6 +281,16 @@ int rr_shard_tile_count(int width, int height, int tile_w, int tile_h, int shard
 int rr_render_tiles(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
                     int height, int tile_w, int tile_h, int shard, int n_shards,
                     uint8_t* d_tiles, rr_stats* stats, void* stream);
+
+/* Fused render + exchange: renders shard `shard`'s tiles (same tiling as
+ * rr_render_tiles) and writes each pixel straight to its place in a
+ * row-major RGB8 frame d_frame, which may live on ANOTHER GPU (a CUDA-IPC /
+ * peer mapping of rank 0's frame: the shade epilogue's stores travel over
+ * NVLink, no gather or detile pass).  Visibility to the frame's owner
+ * follows kernel completion plus a cross-rank synchronisation. */
+int rr_render_shard(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
+                    int height, int tile_w, int tile_h, int shard, int n_shards,
+                    uint8_t* d_frame, rr_stats* stats, void* stream);
 
 /* Reassembles a frame from the concatenation of every shard's tile buffer
  * (shard 0 first, each padded to the largest shard's tile count). */

@@ -582,6 +582,8 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->bump_evals = (int64_t)c->h_stats[3];
         st->rays = (int64_t)c->h_stats[4];
         st->shadow_steps = (int64_t)c->h_stats[5];
+        st->lane_slots = (int64_t)c->h_stats[6];
+        st->shadow_lane_slots = (int64_t)c->h_stats[7];
         st->kernel_launches = c->P->n_lights > 0 ? 2 : 1;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -974,6 +976,26 @@ int rr_render_tiles(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ,
     rr::DevLaunch L;
     if ((rc = setup_frame_launch(c, cam, width, height, tile_w, tile_h, shard, n_shards,
                                  rr::kModeTiles, d_tiles, L)))
+        return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    if ((rc = run_launch(c, L, s))) return rc;
+    if (stats) return collect_stats(c, s, stats, t0);
+    return RR_OK;
+}
+
+int rr_render_shard(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                    int height, int tile_w, int tile_h, int shard, int n_shards, uint8_t* d_frame,
+                    rr_stats* stats, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    const double t0 = now_s();
+    int rc = check_ready(c, integ, stream ? (cudaStream_t)stream : c->stream);
+    if (rc) return rc;
+    if (!d_frame) return set_err(c, RR_ERR_CONFIG, "frame: required");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    rr::DevLaunch L;
+    if ((rc = setup_frame_launch(c, cam, width, height, tile_w, tile_h, shard, n_shards,
+                                 rr::kModeFrame, d_frame, L)))
         return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
     if ((rc = run_launch(c, L, s))) return rc;

@@ -707,6 +707,7 @@ struct RayResult {
 struct LaneCounters {
     unsigned steps_integrated;
     unsigned bump_evals;
+    unsigned lane_slots;       // loop iterations executed by this lane (active or not)
 };
 
 enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2 };
@@ -734,6 +735,7 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
     float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
     for (;;) {
         if (!__any_sync(kFull, active)) break;
+        cnt.lane_slots += 1;
         uint32_t um = 0;
         int nj = 0;                           // >= 2: this lane jumps nj straight steps
         if constexpr (KIND == kEuclid) {
@@ -1065,7 +1067,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             }
         }
 
-        LaneCounters cnt{0u, 0u};
+        LaneCounters cnt{0u, 0u, 0u};
         unsigned ref_steps = 0, errs = 0, shadow_steps = 0;
         bool pad_writer = true;
         if constexpr (PASS == kPassShadow) {
@@ -1156,6 +1158,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
         const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
         const unsigned nr = __reduce_add_sync(kFull, (live && PASS != kPassShadow) ? 1u : 0u);
         const unsigned shs = __reduce_add_sync(kFull, shadow_steps);
+        const unsigned slots = __reduce_add_sync(kFull, cnt.lane_slots);
         if (lane == 0) {
             if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
             if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
@@ -1163,8 +1166,13 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
             if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
             if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
+            if (slots) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), (unsigned long long)slots);
         }
     }
+    // Sharded frame mode may write into another GPU's frame (peer/IPC mapping):
+    // make the stores visible system-wide before the kernel retires, ahead of
+    // the cross-rank synchronisation that hands the frame to its owner.
+    if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
 }
 
 

@@ -169,6 +169,17 @@ class Renderer:
                                              _addr(stream)))
         return st.as_dict() if st is not None else None
 
+    def render_shard(self, cam, integ: IntegratorConfig, width, height, tile_w, tile_h, shard,
+                     n_shards, d_frame, stream=None, with_stats: bool = False):
+        """This shard's tiles written straight into a (possibly peer-mapped) frame."""
+        st = abi.rr_stats() if with_stats else None
+        it = integ.to_abi()
+        self._check(self.lib.rr_render_shard(self.ctx, C.byref(cam), C.byref(it), width, height,
+                                             tile_w, tile_h, shard, n_shards, _addr(d_frame),
+                                             C.byref(st) if st is not None else None,
+                                             _addr(stream)))
+        return st.as_dict() if st is not None else None
+
     def detile(self, d_gathered, width, height, tile_w, tile_h, n_shards, d_rgb, stream=None):
         self._check(self.lib.rr_detile(self.ctx, _addr(d_gathered), width, height, tile_w, tile_h,
                                        n_shards, _addr(d_rgb), _addr(stream)))
@@ -217,6 +228,8 @@ class RenderStats:                    # render.hpp:24-33 (+ device extensions)
     bump_evals: int = 0
     shadow_steps: int = 0
     kernel_launches: int = 0
+    lane_slots: int = 0
+    shadow_lane_slots: int = 0
 
     def avg_steps_per_ray(self) -> float:
         return self.total_steps / self.rays if self.rays > 0 else 0.0

@@ -75,7 +75,10 @@ def _worker(rank, world, port, q):
 def test_tile_shard_gather_detile_roundtrip(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + world * 7 + os.getpid() % 1000
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
