@@ -58,7 +58,7 @@ def parse_args():
     p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                    help="gloo: host-synchronised collectives (dry runs of the N>1 path on fewer GPUs)")
     p.add_argument("--no-extras", action="store_true",
-                   help="skip the secondary BASELINE workloads (C1, C2, C4+mesh, C5 4K)")
+                   help="skip the secondary workloads (C1, C2, C4+mesh, C5 4K, C3 rk23)")
     p.add_argument("--cpu-row-step", type=int, default=0, help="reference row subsample (0=auto)")
     p.add_argument("--opt", action="append", default=[],
                    help="renderer option key=value (rr_options field), e.g. cull_grid=64")
@@ -362,7 +362,8 @@ def run_b200(args, cfg):
     if world == 1 and not args.no_extras:
         from paper_2005_05386_b200.config import load_config
         extras = {}
-        for name in ("c1_gauss1_512", "c2_flat_1080p", "c4_twist_mesh_1080p", "c5_bumps16_4k"):
+        for name in ("c1_gauss1_512", "c2_flat_1080p", "c4_twist_mesh_1080p", "c5_bumps16_4k",
+                     "c3_bumps16_rk23_1080p"):
             ecfg = load_config(os.path.join(ROOT, "configs", name + ".json"))
             ew, eh = ecfg.output.width, ecfg.output.height
             ebuf = torch.empty((eh, ew, 3), dtype=torch.uint8, device="cuda")

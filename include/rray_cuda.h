@@ -164,12 +164,14 @@ typedef struct rr_scene_desc {
 } rr_scene_desc;
 
 /* ---- integrator (integrate.hpp:30-36) ------------------------------------ */
-enum { RR_SCHEME_EULER = 0, RR_SCHEME_RK4 = 1 };
+enum { RR_SCHEME_EULER = 0, RR_SCHEME_RK4 = 1,
+       RR_SCHEME_RK23 = 2 /* EXTENSION: adaptive Bogacki-Shampine 3(2), see oracle/rro.c */ };
 
 typedef struct rr_integrator {
-    double h;
-    int32_t max_steps;
+    double h;                         /* step (RK23: initial step; steps stay in [h/64, 4h]) */
+    int32_t max_steps;                /* RK23: accepted steps */
     int32_t scheme;                   /* RR_SCHEME_* */
+    double tol;                       /* RK23 (EXTENSION): abs+rel error tolerance per step */
 } rr_integrator;
 
 /* ---- march records (kernel.hpp:26-45) ------------------------------------ */

@@ -202,7 +202,7 @@ void check(int rc, rr_ctx* ctx) {
 
 rr_integrator integ_of(const geodesics::IntegratorConfig& c) {
     return rr_integrator{c.h, c.max_steps,
-                         c.scheme == geodesics::Scheme::Euler ? RR_SCHEME_EULER : RR_SCHEME_RK4};
+                         c.scheme == geodesics::Scheme::Euler ? RR_SCHEME_EULER : RR_SCHEME_RK4, 0.0};
 }
 
 std::mutex g_scene_mu;

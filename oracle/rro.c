@@ -864,8 +864,15 @@ static int aabb_contains(const rr_aabb* bx, V3 p) {                          /* 
 }
 
 /* ---- march (include/rray/render/detail/kernel_impl.hpp:22-94) ------------ */
+static void march_one_rk23(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                           const rr_ray_start* ray, rr_pixel_outcome* res, V3* normal);
+
 static void march_one_n(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
                         const rr_ray_start* ray, rr_pixel_outcome* res, V3* normal) {
+    if (in->scheme == RR_SCHEME_RK23) {
+        march_one_rk23(m, sc, in, ray, res, normal);
+        return;
+    }
     memset(res, 0, sizeof *res);
     res->status = RR_MISS;
     res->prim = -1;
@@ -907,6 +914,123 @@ static void march_one_n(const rr_metric_desc* m, const rr_scene_desc* sc, const 
         res->status = RR_MISS;
         res->steps = in->max_steps;
     }
+}
+
+
+/* ---- EXTENSION: adaptive Bogacki-Shampine 3(2) (integrator.scheme "rk23") --
+ * No reference counterpart (SPEC.md:393 lists adaptive stepping as a
+ * non-goal); this FP64 routine is the definition the GPU is checked against.
+ * y = (x, v), f(y) = (v, a(x, v)); FSAL:
+ *   k2 = f(y + h/2 k1), k3 = f(y + 3h/4 k2), y' = y + h(2/9 k1 + 1/3 k2 + 4/9 k3),
+ *   k4 = f(y'),  err = h(-5/72 k1 + 1/12 k2 + 1/9 k3 - 1/8 k4),
+ *   e = max_i |err_i| / (tol (1 + max(|y_i|, |y'_i|))).
+ * A step is accepted when e <= 1 (or h is at its floor h0/64); its chord
+ * [x, x'] is then tested exactly like a fixed step, a hit at chord fraction
+ * s reporting t = t_step + s h.  Then h <- h min(5, max(0.2, 0.9 e^(-1/3))),
+ * clamped to [h0/64, 4 h0].  max_steps counts accepted steps; at most
+ * 16 max_steps attempts. */
+static void f_eval(const rr_metric_desc* m, V3 x, V3 v, V3* kx, V3* kv, double* validity) {
+    *kx = v;
+    *kv = flow_accel(m, x, v, validity);
+}
+
+/* Adaptive core.  Primary rays: light == NULL, fills res (+ normal).  Shadow
+ * rays (light = the shaded point q, dist = |light - q|): returns 1 lit /
+ * 0 blocked with the fixed-step shadow_march rules (blocked by a hit nearer
+ * than the light, lit on crossing the light sphere, leaving the bounds or
+ * running out of steps, 0 on a singular metric); *accepted counts accepted
+ * steps (the shadow_steps statistic, as the fixed-step shadow_march). */
+static int rk23_core(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                     V3 x, V3 v, const V3* light, double dist, rr_pixel_outcome* res, V3* normal,
+                     long long* accepted) {
+    const double h0 = in->h, hmin = h0 / 64.0, hmax = 4.0 * h0, tol = in->tol;
+    double h = h0, t = 0.0, validity = 1.0;
+    V3 k1x, k1v;
+    f_eval(m, x, v, &k1x, &k1v, &validity);
+    int steps = 0;
+    for (long attempt = 0; steps < in->max_steps && attempt < 16L * in->max_steps; ++attempt) {
+        V3 k2x, k2v, k3x, k3v, k4x, k4v;
+        f_eval(m, vadd(x, vscale(0.5 * h, k1x)), vadd(v, vscale(0.5 * h, k1v)), &k2x, &k2v, &validity);
+        f_eval(m, vadd(x, vscale(0.75 * h, k2x)), vadd(v, vscale(0.75 * h, k2v)), &k3x, &k3v, &validity);
+        const V3 xn = vadd(x, vscale(h, vadd(vadd(vscale(2.0 / 9.0, k1x), vscale(1.0 / 3.0, k2x)),
+                                             vscale(4.0 / 9.0, k3x))));
+        const V3 vn = vadd(v, vscale(h, vadd(vadd(vscale(2.0 / 9.0, k1v), vscale(1.0 / 3.0, k2v)),
+                                             vscale(4.0 / 9.0, k3v))));
+        f_eval(m, xn, vn, &k4x, &k4v, &validity);
+        if (!(validity > kSingularDetEps)) {
+            if (res) {
+                res->status = RR_FAILED;
+                res->steps = steps;
+            }
+            return 0;
+        }
+        const double ce[4] = {-5.0 / 72.0, 1.0 / 12.0, 1.0 / 9.0, -1.0 / 8.0};
+        const V3 ex = vscale(h, vadd(vadd(vscale(ce[0], k1x), vscale(ce[1], k2x)),
+                                     vadd(vscale(ce[2], k3x), vscale(ce[3], k4x))));
+        const V3 ev = vscale(h, vadd(vadd(vscale(ce[0], k1v), vscale(ce[1], k2v)),
+                                     vadd(vscale(ce[2], k3v), vscale(ce[3], k4v))));
+        const double errs[6] = {ex.x, ex.y, ex.z, ev.x, ev.y, ev.z};
+        const double y0[6] = {x.x, x.y, x.z, v.x, v.y, v.z};
+        const double y1[6] = {xn.x, xn.y, xn.z, vn.x, vn.y, vn.z};
+        double e = 0.0;
+        for (int i = 0; i < 6; ++i) {
+            const double sc_i = tol * (1.0 + fmax(fabs(y0[i]), fabs(y1[i])));
+            e = fmax(e, fabs(errs[i]) / sc_i);
+        }
+        const int accept = e <= 1.0 || h <= hmin;
+        if (accept) {
+            V3 point;
+            double hs;
+            int prim;
+            if (accepted) ++*accepted;
+            if (intersect_segment_n(sc, x, xn, &point, &hs, &prim, normal)) {
+                if (light) {
+                    const V3 r = vsub(point, *light);
+                    return sqrt(vdot(r, r)) < dist ? 0 : 1;
+                }
+                res->status = RR_HIT;
+                res->prim = prim;
+                res->point.x = point.x;
+                res->point.y = point.y;
+                res->point.z = point.z;
+                res->t = t + hs * h;
+                res->steps = steps + 1;
+                return 1;
+            }
+            ++steps;
+            if (light) {
+                const V3 rb = vsub(xn, *light);
+                if (sqrt(vdot(rb, rb)) >= dist) return 1;
+            }
+            if (!aabb_contains(&sc->bounds, xn)) {
+                if (res) {
+                    res->status = RR_MISS;
+                    res->steps = steps;
+                }
+                return 1;
+            }
+            t += h;
+            x = xn;
+            v = vn;
+            k1x = k4x;
+            k1v = k4v;
+        }
+        const double fac = e > 0.0 ? fmin(5.0, fmax(0.2, 0.9 * pow(e, -1.0 / 3.0))) : 5.0;
+        h = fmin(hmax, fmax(hmin, h * fac));
+    }
+    if (res) {
+        res->status = RR_MISS;
+        res->steps = steps;
+    }
+    return 1;
+}
+
+static void march_one_rk23(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
+                           const rr_ray_start* ray, rr_pixel_outcome* res, V3* normal) {
+    memset(res, 0, sizeof *res);
+    res->status = RR_MISS;
+    res->prim = -1;
+    rk23_core(m, sc, in, vfrom(ray->position), vfrom(ray->direction), NULL, 0.0, res, normal, NULL);
 }
 
 static void march_one(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_integrator* in,
@@ -1016,6 +1140,8 @@ static int shadow_march(const rr_metric_desc* m, const rr_scene_desc* sc, const 
     S3 g;
     if (metric_tensor_checked(m, x0, &g)) return 0;
     State s = {x0, vdiv(dir, sqrt(quad_form(g, dir, dir)))};
+    if (in->scheme == RR_SCHEME_RK23)   /* EXT: adaptive shadow rays, same rules */
+        return rk23_core(m, sc, in, s.position, s.velocity, &q, dist, NULL, NULL, steps);
     for (int step = 0; step < in->max_steps; ++step) {
         double validity;
         const State next = flow_step(m, s, in->h, in->scheme, &validity);

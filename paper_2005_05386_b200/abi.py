@@ -19,7 +19,7 @@ RR_FIELD_GAUSSIAN, RR_FIELD_POLYNOMIAL, RR_FIELD_SUM = 0, 1, 2
  RR_DIFFEO_COMPOSE, RR_DIFFEO_BEND) = 0, 1, 2, 3, 4, 5
 RR_METRIC_EUCLIDEAN, RR_METRIC_GRAPH, RR_METRIC_DIFFEO = 0, 1, 2
 RR_PRIM_GRID_PLANES, RR_PRIM_SPHERE, RR_PRIM_HALF_SPACE, RR_PRIM_MESH = 0, 1, 2, 3
-RR_SCHEME_EULER, RR_SCHEME_RK4 = 0, 1
+RR_SCHEME_EULER, RR_SCHEME_RK4, RR_SCHEME_RK23 = 0, 1, 2
 RR_MISS, RR_HIT, RR_FAILED = 0, 1, 2
 
 
@@ -86,7 +86,8 @@ class rr_scene_desc(C.Structure):
 
 
 class rr_integrator(C.Structure):
-    _fields_ = [("h", C.c_double), ("max_steps", C.c_int32), ("scheme", C.c_int32)]
+    _fields_ = [("h", C.c_double), ("max_steps", C.c_int32), ("scheme", C.c_int32),
+                ("tol", C.c_double)]
 
 
 class rr_ray_start(C.Structure):
@@ -133,7 +134,7 @@ OUTCOME_DTYPE = np.dtype({
 EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
     "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
-    "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 16,
+    "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 24,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 88,
     "rr_options": 32,
 }

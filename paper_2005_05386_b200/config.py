@@ -10,6 +10,7 @@ ValidationError/ParseError naming the same key.  One superset key is accepted
                    shadow geodesics; absent/empty = reference shading.
     scene.ambient: ambient term of the lit shading (default 0.2).
     metric.map (any level) = {"kind": "bend", "curvature": k}   Barr bend about z.
+    integrator.scheme = "rk23", integrator.tol   adaptive Bogacki-Shampine 3(2).
     scene.primitives[i] = {"kind": "mesh", "vertices": [...], "triangles": [...]}
                    or {"kind": "mesh", "generator": {"kind": "torus", ...}}
                    triangle meshes (BVH-accelerated on the GPU).
@@ -209,17 +210,20 @@ class CameraSpec:                     # config.hpp:18-25
 
 
 @dataclass
-class IntegratorConfig:               # integrate.hpp:30-36
+class IntegratorConfig:               # integrate.hpp:30-36 (+ rk23/tol EXTENSION)
     h: float = 1e-2
     max_steps: int = 2000
     scheme: str = "euler"
+    tol: float = 1e-6
 
     @property
     def scheme_id(self) -> int:
-        return abi.RR_SCHEME_EULER if self.scheme == "euler" else abi.RR_SCHEME_RK4
+        return {"euler": abi.RR_SCHEME_EULER, "rk4": abi.RR_SCHEME_RK4,
+                "rk23": abi.RR_SCHEME_RK23}[self.scheme]
 
     def to_abi(self) -> abi.rr_integrator:
-        return abi.rr_integrator(float(self.h), int(self.max_steps), self.scheme_id)
+        return abi.rr_integrator(float(self.h), int(self.max_steps), self.scheme_id,
+                                 float(self.tol))
 
 
 @dataclass
@@ -570,11 +574,11 @@ def _parse_camera(o, path) -> CameraSpec:                         # :340-352
     return c
 
 
-def _parse_integrator(o, path) -> IntegratorConfig:               # :354-370
+def _parse_integrator(o, path, allow_ext: bool = True) -> IntegratorConfig:  # :354-370
     c = IntegratorConfig()
     if o is None:
         return c
-    _check_keys(o, path, {"h", "max_steps", "scheme"})
+    _check_keys(o, path, {"h", "max_steps", "scheme"} | ({"tol"} if allow_ext else set()))
     c.h = _get_double_or(o, path, "h", c.h)
     if not (c.h > 0.0):
         _fail(path + ".h", "must be > 0")
@@ -582,9 +586,13 @@ def _parse_integrator(o, path) -> IntegratorConfig:               # :354-370
     if c.max_steps < 1:
         _fail(path + ".max_steps", "must be >= 1")
     scheme = _get_string_or(o, path, "scheme", "euler")
-    if scheme not in ("euler", "rk4"):
+    if scheme not in ("euler", "rk4") and not (allow_ext and scheme == "rk23"):
         _fail(path + ".scheme", f"must be euler|rk4, got '{scheme}'")
     c.scheme = scheme
+    if allow_ext:
+        c.tol = _get_double_or(o, path, "tol", 1e-6)
+        if not (c.tol > 0.0):
+            _fail(path + ".tol", "must be > 0")
     return c
 
 
@@ -622,7 +630,7 @@ def parse_config(text: str, allow_ext: bool = True) -> RunConfig:  # :437-456
     cfg.metric = _parse_metric(root["metric"], "metric", allow_ext)
     cfg.scene = _parse_scene(root.get("scene"), "scene", allow_ext)
     cfg.camera = _parse_camera(root.get("camera"), "camera")
-    cfg.integrator = _parse_integrator(root.get("integrator"), "integrator")
+    cfg.integrator = _parse_integrator(root.get("integrator"), "integrator", allow_ext)
     cfg.output = _parse_output(root.get("output"), "output")
     return cfg
 
@@ -702,8 +710,10 @@ def config_to_dict(cfg: RunConfig, include_ext: bool = True) -> dict:
         "scene": scene,
         "camera": {"position": list(cfg.camera.position), "look_dir": list(cfg.camera.look_dir),
                    "up_hint": list(cfg.camera.up_hint), "fov_deg": cfg.camera.fov_deg},
-        "integrator": {"h": cfg.integrator.h, "max_steps": cfg.integrator.max_steps,
-                       "scheme": cfg.integrator.scheme},
+        "integrator": dict({"h": cfg.integrator.h, "max_steps": cfg.integrator.max_steps,
+                            "scheme": cfg.integrator.scheme},
+                           **({"tol": cfg.integrator.tol}
+                              if include_ext and cfg.integrator.scheme == "rk23" else {})),
         "output": {"path": cfg.output.path, "width": cfg.output.width,
                    "height": cfg.output.height, "format": cfg.output.format},
     }

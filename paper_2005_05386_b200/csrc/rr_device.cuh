@@ -126,12 +126,14 @@ struct DevParams {
     int nb_slot;          // kBumps: bump slots of the kernel variant (4/8/16/32)
     float h, fog;
     float ambient;        // EXTENSION: lit shading ambient term
+    float tol;            // EXTENSION: rk23 error tolerance
     float lo[3], hi[3];   // scene bounds
     int cull;             // 1: cull_masks valid
     int grid;             // culling voxels per axis
     float grid_lo[3], grid_inv[3];
     uint32_t all_mask;    // bits of every live bump (slot bits for kBumps)
-    const uint32_t* cull_masks;   // grid^3 bump masks (device)
+    const uint32_t* cull_masks;   // grid^3 bump masks (device); rk23: 3 levels
+    unsigned cull_cells;          // grid^3 (level stride)
     const uint8_t* skip_k;        // grid^3 Chebyshev distance (cells) to the nearest non-empty cell
     int skip;                     // 1: empty-space skipping enabled
     float cell_min;               // smallest culling-cell edge (world units)

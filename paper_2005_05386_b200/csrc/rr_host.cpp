@@ -86,6 +86,7 @@ struct rr_ctx {
     uint16_t* d_cull_scratch = nullptr;      // 2 G^3 uint16 for the distance transform passes
     double* d_cull_gauss = nullptr;          // bump records for the device grid build
     double masks_dilation = -1.0;
+    int masks_levels = 0, masks_alloc_levels = 0;   // rk23: 3 dilation levels
     int masks_grid = 0;
     double masks_radius = 0.0;
     // scratch
@@ -344,7 +345,7 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
 // implies |y| <= 1 for graph metrics), plus the Chebyshev distance to the
 // nearest non-empty cell for empty-space skipping.  Rebuilt when the scene or
 // the options change, or h grows; stream-ordered before the march.
-int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
+int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
     DevParams& P = *c->P;
     P.skip = c->opt.o.skip ? 1 : 0;   // Euclid: straight jumps need no grid
     if (P.kind != rr::kBumps || !c->opt.o.cull) {
@@ -355,19 +356,21 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
     const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));
     const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 6.0;
     const double dil = 1.5 * h;
-    if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil) {
+    if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil &&
+        c->masks_levels == levels) {
         P.cull = 1;
         return RR_OK;
     }
     const size_t cells = (size_t)G * G * G;
-    if (c->masks_grid != G) {
+    if (c->masks_grid != G || c->masks_alloc_levels < levels) {
         if (c->d_masks) cudaFree(c->d_masks);
         if (c->d_skip) cudaFree(c->d_skip);
         if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
         c->d_masks = nullptr;
         c->d_skip = nullptr;
         c->d_cull_scratch = nullptr;
-        RR_CUDA(c, cudaMalloc(&c->d_masks, cells * sizeof(uint32_t)));
+        RR_CUDA(c, cudaMalloc(&c->d_masks, (size_t)levels * cells * sizeof(uint32_t)));
+        c->masks_alloc_levels = levels;
         RR_CUDA(c, cudaMalloc(&c->d_skip, cells));
         RR_CUDA(c, cudaMalloc(&c->d_cull_scratch, 2 * cells * sizeof(uint16_t)));
         c->masks_grid = G;
@@ -395,10 +398,16 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s) {
         lo[k] = P.lo[k];
         cell[k] = ((double)P.hi[k] - P.lo[k]) / G;
     }
-    RR_CUDA(c, rr::launch_cull_build(c->d_cull_gauss, n, G, lo, cell, R, dil, c->d_masks,
-                                     c->d_cull_scratch, c->d_skip, s));
+    // level l covers steps up to 2^l h (rk23); the skip distances come from the
+    // widest level, built last
+    for (int l = 0; l < levels; ++l)
+        RR_CUDA(c, rr::launch_cull_build(c->d_cull_gauss, n, G, lo, cell, R, dil * (1 << l),
+                                         c->d_masks + (size_t)l * cells, c->d_cull_scratch,
+                                         c->d_skip, s));
     c->masks_radius = R;
     c->masks_dilation = dil;
+    c->masks_levels = levels;
+    P.cull_cells = (unsigned)cells;
     P.cull = 1;
     P.grid = G;
     P.cull_masks = c->d_masks;
@@ -542,12 +551,17 @@ int check_ready(rr_ctx* c, const rr_integrator* integ, cudaStream_t s) {
     if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
     if (!integ || !(integ->h > 0.0)) return set_err(c, RR_ERR_CONFIG, "integrator.h: must be > 0");
     if (integ->max_steps < 1) return set_err(c, RR_ERR_CONFIG, "integrator.max_steps: must be >= 1");
-    if (integ->scheme != RR_SCHEME_EULER && integ->scheme != RR_SCHEME_RK4)
-        return set_err(c, RR_ERR_CONFIG, "integrator.scheme: must be euler|rk4");
+    if (integ->scheme != RR_SCHEME_EULER && integ->scheme != RR_SCHEME_RK4 &&
+        integ->scheme != RR_SCHEME_RK23)
+        return set_err(c, RR_ERR_CONFIG, "integrator.scheme: must be euler|rk4|rk23");
+    if (integ->scheme == RR_SCHEME_RK23 && !(integ->tol > 0.0))
+        return set_err(c, RR_ERR_CONFIG, "integrator.tol: must be > 0");
     c->P->h = (float)integ->h;
     c->P->max_steps = integ->max_steps;
     c->P->scheme = integ->scheme;
-    return ensure_masks(c, integ->h, s);
+    c->P->tol = (float)integ->tol;
+    // rk23 steps grow to 4 h: masks at dilations for h, 2h and 4h
+    return ensure_masks(c, integ->h, s, integ->scheme == RR_SCHEME_RK23 ? 3 : 1);
 }
 
 // Launch one march over `units` warp units; zeroes counters+stats first.

@@ -27,6 +27,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_GROUP_TESTS
 #define RR_GROUP_TESTS 1
 #endif
+#ifndef RR_MIN_BLOCKS_RK23
+#define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
+#endif
 #ifndef RR_MIN_BLOCKS
 #define RR_MIN_BLOCKS 7   // <= 72 registers: 7 CTAs = 28 warps per SM (measured best)
 #endif
@@ -720,8 +723,12 @@ enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2 };
 // shadow_march): lit (1) when it crosses the sphere |x - q| = sqrt(dist2),
 // leaves the bounds or runs out of steps; blocked (0) on a nearer hit or a
 // metric failure.
+template <int KIND, int NB, int PASS, bool MESH>
+__device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool live, F3 p, F3 v,
+                                                     LaneCounters& cnt, F3 q, float dist2);
+
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
+__device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, F3 p, F3 v,
                                                 LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
                                                 float dist2 = 0.f) {
     RayResult res{PASS == kPassShadow ? 1 : 0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
@@ -889,6 +896,207 @@ __device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F
     return res;
 }
 
+
+// ---------------------------------------------------------------------------
+// EXTENSION: adaptive Bogacki-Shampine 3(2) march (integrator.scheme "rk23";
+// FP64 definition: oracle/rro.c march_one_rk23).  Per-lane step size; FSAL
+// (k1 of the next step is k4 of the accepted one); the warp-uniform bump mask
+// is taken at the step start and covers every stage point because the
+// culling grid is dilated for h_max = 4 h0.  Rejected lanes keep their state.
+template <int KIND, int NB, int PASS, bool MESH>
+__device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool live, F3 p, F3 v,
+                                                     LaneCounters& cnt, F3 q, float dist2) {
+    RayResult res{PASS == kPassShadow ? 1 : 0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
+    bool active = live;
+    const float h0 = P.h, hmin = h0 / 64.f, hmax = 4.f * h0, tol = P.tol;
+    const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
+    float h = h0, t = 0.f;
+    int steps = 0, attempts = 0;
+    float mfree = 0.f;
+    bool have_k1 = false;
+    F3 k1v = f3(0.f, 0.f, 0.f);
+    for (;;) {
+        if (!__any_sync(kFull, active)) break;
+        cnt.lane_slots += 1;
+        uint32_t um = 0;
+        int nj = 0;                   // >= 2: this lane jumps nj straight steps of h_max
+        // Straight jumps: where the (culled) metric is flat the error estimate
+        // is ~0, so h sits at h_max and the geodesic is x + j h_max y; a lane
+        // at h_max collapses nj such steps into one chord (same rules as the
+        // fixed-step march: never past the bounds exit or the light's sphere,
+        // bump scenes only inside empty cells of the culling grid).
+        float L = -1.f;
+        if (P.skip && active && h >= hmax) {
+            if constexpr (KIND == kEuclid) L = 3.0e38f;
+            if constexpr (KIND == kBumps) {
+                if (P.cull) {
+                    const unsigned cell = cell_of(P, p);
+                    if (__ldg(P.cull_masks + 2u * P.cull_cells + cell) == 0u) {
+                        const int k = __ldg(P.skip_k + cell);
+                        if (k >= 2) L = (float)(k - 1) * P.cell_min;
+                    }
+                }
+            }
+        }
+        if (L > 0.f) {
+            const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
+            const float isp = rsqrtf(speed2);
+            float te = 3.0e38f;
+            if (v.x != 0.f) te = fminf(te, ((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x) / v.x);
+            if (v.y != 0.f) te = fminf(te, ((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y) / v.y);
+            if (v.z != 0.f) te = fminf(te, ((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z) / v.z);
+            L = fminf(L, te * speed2 * isp);
+            if (PASS == kPassShadow) {
+                const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
+                L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
+            }
+            const float n = floorf(L * isp / hmax) - 1.f;
+            nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - steps));
+            if (nj < 2) nj = 0;
+        }
+        if constexpr (KIND == kBumps) {
+            uint32_t lm = 0;
+            if (active && !nj) {   // the mask level whose dilation covers this lane's h
+                const unsigned lvl = h <= h0 ? 0u : (h <= 2.f * h0 ? 1u : 2u);
+                lm = P.cull ? __ldg(P.cull_masks + lvl * P.cull_cells + cell_of(P, p)) : P.all_mask;
+            }
+            um = __reduce_or_sync(kFull, lm);
+        }
+        float valid = 3.0e38f;
+        const bool need_k1 = !__all_sync(kFull, have_k1 || !active);
+        if (need_k1) {                         // first step (warp-uniform branch)
+            const F3 a = accel<KIND, NB>(P, um, p, v, valid);
+            if (!have_k1) k1v = a;
+            have_k1 = true;
+        }
+        const F3 k1x = v;
+        F3 k2x, k2v, k3x, k3v, k4x, k4v, xn, vn;
+        float e = 0.f;
+        if (__all_sync(kFull, nj != 0 || !active)) {   // whole warp jumps: no integration
+            k2x = k3x = k4x = v;
+            k2v = k3v = k4v = f3(0.f, 0.f, 0.f);
+            xn = p;
+            vn = v;
+        } else {
+            // stages k2, k3, k4 through one call site
+            F3 ps = f3(fmaf(0.5f * h, k1x.x, p.x), fmaf(0.5f * h, k1x.y, p.y), fmaf(0.5f * h, k1x.z, p.z));
+            F3 vs = f3(fmaf(0.5f * h, k1v.x, v.x), fmaf(0.5f * h, k1v.y, v.y), fmaf(0.5f * h, k1v.z, v.z));
+#pragma unroll 1
+            for (int st = 0; st < 3; ++st) {
+                const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
+                if (st == 0) {
+                    k2x = vs; k2v = a;
+                    ps = f3(fmaf(0.75f * h, k2x.x, p.x), fmaf(0.75f * h, k2x.y, p.y), fmaf(0.75f * h, k2x.z, p.z));
+                    vs = f3(fmaf(0.75f * h, k2v.x, v.x), fmaf(0.75f * h, k2v.y, v.y), fmaf(0.75f * h, k2v.z, v.z));
+                } else if (st == 1) {
+                    k3x = vs; k3v = a;
+                    const float c1 = 2.f / 9.f * h, c2 = 1.f / 3.f * h, c3 = 4.f / 9.f * h;
+                    xn = f3(fmaf(c1, k1x.x, fmaf(c2, k2x.x, fmaf(c3, k3x.x, p.x))),
+                            fmaf(c1, k1x.y, fmaf(c2, k2x.y, fmaf(c3, k3x.y, p.y))),
+                            fmaf(c1, k1x.z, fmaf(c2, k2x.z, fmaf(c3, k3x.z, p.z))));
+                    vn = f3(fmaf(c1, k1v.x, fmaf(c2, k2v.x, fmaf(c3, k3v.x, v.x))),
+                            fmaf(c1, k1v.y, fmaf(c2, k2v.y, fmaf(c3, k3v.y, v.y))),
+                            fmaf(c1, k1v.z, fmaf(c2, k2v.z, fmaf(c3, k3v.z, v.z))));
+                    ps = xn;
+                    vs = vn;
+                } else {
+                    k4x = vs; k4v = a;
+                }
+            }
+            if constexpr (KIND == kBumps) {
+                if (active && !nj) cnt.bump_evals += 3u * __popc(um);
+            }
+            // embedded error, mixed abs/rel scale
+            const float e1 = -5.f / 72.f * h, e2 = 1.f / 12.f * h, e3 = 1.f / 9.f * h, e4 = -1.f / 8.f * h;
+            const float y0[6] = {p.x, p.y, p.z, v.x, v.y, v.z};
+            const float y1[6] = {xn.x, xn.y, xn.z, vn.x, vn.y, vn.z};
+            const float ka[6] = {k1x.x, k1x.y, k1x.z, k1v.x, k1v.y, k1v.z};
+            const float kb[6] = {k2x.x, k2x.y, k2x.z, k2v.x, k2v.y, k2v.z};
+            const float kc[6] = {k3x.x, k3x.y, k3x.z, k3v.x, k3v.y, k3v.z};
+            const float kd[6] = {k4x.x, k4x.y, k4x.z, k4v.x, k4v.y, k4v.z};
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const float err = fmaf(e1, ka[i], fmaf(e2, kb[i], fmaf(e3, kc[i], e4 * kd[i])));
+                const float sc = tol * (1.f + fmaxf(fabsf(y0[i]), fabsf(y1[i])));
+                e = fmaxf(e, __fdividef(fabsf(err), sc));
+            }
+        }
+        if (nj) {                                            // straight jump of nj h_max steps
+            const float hn = hmax * (float)nj;
+            xn = f3(fmaf(hn, v.x, p.x), fmaf(hn, v.y, p.y), fmaf(hn, v.z, p.z));
+            vn = v;
+            k4v = f3(0.f, 0.f, 0.f);                         // flat (culled) metric at xn
+            e = 0.f;
+            valid = 3.0e38f;
+        }
+        const bool accept = e <= 1.f || h <= hmin;
+        if (active) {
+            const int nsub = nj ? nj : 1;
+            const float hstep = nj ? hmax * (float)nj : h;
+            cnt.steps_integrated += 1;
+            attempts += nsub;
+            float s = 0.f;
+            int prim = -1, hid = 0, mrec = 0;
+            if (KIND == kDiffeo && !(valid > 1e-14f)) {
+                res.status = PASS == kPassShadow ? 0 : 2;
+                res.steps = steps;
+                active = false;
+            } else if (accept) {
+                if (intersect<MESH>(P, p, xn, s, prim, hid, mfree, mrec)) {
+                    const F3 pt = f3(fmaf(s, xn.x - p.x, p.x), fmaf(s, xn.y - p.y, p.y),
+                                     fmaf(s, xn.z - p.z, p.z));
+                    const int sub = min((int)(s * (float)nsub), nsub - 1);
+                    if constexpr (PASS == kPassShadow) {
+                        const F3 r = f3(pt.x - q.x, pt.y - q.y, pt.z - q.z);
+                        res.status = (r.x * r.x + r.y * r.y + r.z * r.z) < dist2 ? 0 : 1;
+                    } else {
+                        res.status = 1;
+                        res.prim = prim;
+                        res.point = pt;
+                        res.t = fmaf(s, hstep, t);
+                        if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, xn, pt, mrec);
+                    }
+                    res.steps = steps + sub + 1;
+                    active = false;
+                } else {
+                    steps += nsub;
+                    const bool crossed = PASS == kPassShadow &&
+                        (xn.x - q.x) * (xn.x - q.x) + (xn.y - q.y) * (xn.y - q.y) +
+                            (xn.z - q.z) * (xn.z - q.z) >= dist2;
+                    if (crossed || !inside_bounds(P, xn)) {
+                        res.status = PASS == kPassShadow ? 1 : 0;
+                        res.steps = steps;
+                        active = false;
+                    } else {
+                        t += hstep;
+                        p = xn;
+                        v = vn;
+                        k1v = k4v;
+                    }
+                }
+            }
+            if (active) {
+                const float fac = e > 0.f ? fminf(5.f, fmaxf(0.2f, 0.9f * ex2(-__log2f(e) / 3.f))) : 5.f;
+                h = fminf(hmax, fmaxf(hmin, h * fac));
+                if (steps >= P.max_steps || attempts >= 16 * P.max_steps) {
+                    res.status = PASS == kPassShadow ? 1 : 0;
+                    res.steps = steps;
+                    active = false;
+                }
+            }
+        }
+    }
+    return res;
+}
+
+template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
+__device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
+                                                LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
+                                                float dist2 = 0.f) {
+    if constexpr (SCHEME == 2) return march_unit_rk23<KIND, NB, PASS, MESH>(P, live, p, v, cnt, q, dist2);
+    else return march_fixed<KIND, NB, SCHEME, PASS, MESH>(P, live, p, v, cnt, q, dist2);
+}
+
 // g at x (metric.cpp:12-15 / :40-42), for the shadow ray's unit g-speed.
 __device__ void metric_at(const DevParams& P, F3 x, float g[6], bool& ok) {
     float gx = 0.f, gy = 0.f, gz = 0.f;   // grad f (graph) ; J (diffeo) below
@@ -1019,7 +1227,7 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
 }
 
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__global__ void __launch_bounds__(kThreads, RR_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23 : RR_MIN_BLOCKS)
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -1312,7 +1520,7 @@ cudaError_t dispatch_kind(const DevParams& P, const DevLaunch& L, cudaStream_t s
             *name = MESH ? "march_kernel<euclid,mesh>" : "march_kernel<euclid>";
             return launch_variant<kEuclid, 0, SCHEME, MESH>(P, L, s, sms);
         case kBumps:
-            if constexpr (!MESH) {   // mesh scenes use the 16/32-slot variants only
+            if constexpr (!MESH && SCHEME != 2) {   // mesh / rk23 scenes use 16/32 slots only
                 if (P.nb_slot <= 4) {
                     *name = "march_kernel<bumps4>";
                     return launch_variant<kBumps, 4, SCHEME, MESH>(P, L, s, sms);
@@ -1351,6 +1559,7 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
     const char* dummy;
     if (!kernel_name) kernel_name = &dummy;
     if (L.n_units == 0) return cudaSuccess;
+    if (P.scheme == 2) return dispatch_scheme<2>(P, L, stream, num_sms, kernel_name);
     return P.scheme == 0 ? dispatch_scheme<0>(P, L, stream, num_sms, kernel_name)
                          : dispatch_scheme<1>(P, L, stream, num_sms, kernel_name);
 }

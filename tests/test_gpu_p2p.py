@@ -75,11 +75,17 @@ def test_shards_write_into_shared_frame():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
+    import queue
     msgs = []
+    try:   # read before join (a queue polled after join can look empty)
+        while not any(m[0] == "result" for m in msgs):
+            msgs.append(q.get(timeout=300))
+            if msgs[-1][0] == "error":
+                break
+    except queue.Empty:
+        pass
     for p in procs:
         p.join(300)
-    while not q.empty():
-        msgs.append(q.get())
     errors = [m for m in msgs if m[0] == "error"]
     assert not errors, errors
     assert all(p.exitcode == 0 for p in procs), ([p.exitcode for p in procs], msgs)

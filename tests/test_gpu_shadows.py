@@ -80,3 +80,21 @@ def test_shadows_change_the_image_and_stay_deterministic(renderer):
     plain, st = renderer.render(cam, flat.integrator, w, h)
     assert st["kernel_launches"] == 1 and st["shadow_steps"] == 0
     assert (lit.astype(int) - plain.astype(int)).any()
+
+
+def test_larger_frame_parity_with_shadows(renderer, oracle_lib):
+    """C3 with both lights at 384x216 (83k primary rays + shadow geodesics)."""
+    from oracle.parity import compare_outcomes, compare_rgb
+    cfg = _cfg("c3_bumps16_shadows_1080p")
+    w, h = 384, 216
+    ref_rgb, ref_out, ref_st, flags = oracle_lib.render(cfg, w, h, with_flags=True)
+    renderer.set_config(cfg)
+    cam = renderer.build_camera(cfg.camera)
+    rgb, st = renderer.render(cam, cfg.integrator, w, h)
+    rays = oracle_lib.primary_rays(oracle_lib.camera(cfg), w, h)
+    out = renderer.march(cfg.integrator, rays)
+    rep = compare_outcomes(out, ref_out, flags)
+    rep = compare_rgb(rgb, ref_rgb, flags, rep)
+    assert rep.ok, rep.summary()
+    assert rep.exempt < 0.01 * w * h and rep.endpoint_max_rel < 1e-4
+    print("C3 384x216 parity:", rep.summary())
