@@ -299,6 +299,39 @@ int rr_render_shard(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* inte
 int rr_detile(rr_ctx* ctx, const uint8_t* d_gathered, int width, int height, int tile_w,
               int tile_h, int n_shards, uint8_t* d_rgb, void* stream);
 
+/* ---- Off the render path: geodesic export and device verify ------------
+ * (`python -m paper_2005_05386_b200 geodesic|verify`). */
+
+/* trace_geodesic (src/geodesics/integrate.cpp:40-54) on the device, one
+ * geodesic per start, scheme euler|rk4 with step integ->h for up to
+ * integ->max_steps steps.  states: n x (max_steps+1) x 6 doubles
+ * {x, y, z, vx, vy, vz} (state i at t = i h; states[0] = the start);
+ * counts[r] = states written (the exiting state is kept when use_bounds and
+ * the scene bounds are left, integrate.cpp:51); fail_step[r] = the step whose
+ * metric evaluation failed (|det J| <= 1e-14, integrate.cpp:48: the
+ * reference throws NumericError naming it) or -1. */
+int rr_trace(rr_ctx* ctx, const rr_integrator* integ, const rr_ray_start* starts, size_t n,
+             int use_bounds, double* states, int32_t* counts, int32_t* fail_step);
+
+/* flow_accel (include/rray/geodesics/integrate.hpp:46-53) evaluated by the
+ * device metric program at n points: acc = -Gamma(vel, vel) (n x 3) and the
+ * validity (min |det J|; 1 for graph / Euclidean metrics). */
+int rr_accel(rr_ctx* ctx, const double* pos, const double* vel, size_t n, double* acc,
+             double* validity);
+
+/* FP64 host metric tensor g(p) as {xx, xy, xz, yy, yz, zz}
+ * (src/metrics/metric.cpp:12-15, :40-42); status 2 when singular. */
+int rr_metric_tensor(rr_ctx* ctx, const double* p, double* g);
+
+/* FP64 finite-difference Christoffel oracle (src/metrics/metric.cpp:88-133,
+ * step h_fd, reference default 1e-4): gamma[6 m + q] = Gamma^m in the
+ * SymMat3 order {xx, xy, xz, yy, yz, zz}. */
+int rr_christoffel_fd(rr_ctx* ctx, const double* p, double h_fd, double* gamma);
+
+/* FP64 image Phi(p) of the diffeo chain (eval_diffeo_raw, diffeo.hpp:214-225;
+ * p itself for graph / Euclidean metrics). */
+int rr_diffeo_image(rr_ctx* ctx, const double* p, double* image);
+
 /* Microbenchmark of the FP32 FMA pipe (roofline denominator): returns the
  * measured dense FFMA throughput of this device in TFLOP/s. */
 int rr_measure_fp32_peak(rr_ctx* ctx, double* tflops);

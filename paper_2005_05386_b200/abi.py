@@ -179,6 +179,11 @@ SIGNATURES = {
                                   C.POINTER(rr_stats), _P]),
     "rr_detile": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     "rr_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "rr_trace": (C.c_int, [_P, C.POINTER(rr_integrator), _P, C.c_size_t, C.c_int, _P, _P, _P]),
+    "rr_accel": (C.c_int, [_P, _P, _P, C.c_size_t, _P, _P]),
+    "rr_metric_tensor": (C.c_int, [_P, _P, _P]),
+    "rr_christoffel_fd": (C.c_int, [_P, _P, C.c_double, _P]),
+    "rr_diffeo_image": (C.c_int, [_P, _P, _P]),
 }
 
 

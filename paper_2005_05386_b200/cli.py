@@ -11,8 +11,12 @@ plus the B200 extension
          c_j(t) = c_j + A (sin(w t + phi_j), cos(w t + phi_j), 0),
          phi_j = 2 pi j / N_bumps, t = frame / fps; every frame is a static
          reference-schema scene (uploaded per frame), rendered on the GPU.
-`geodesic` (polyline CSV export) and `verify` (property suites) are off the
-render hot path and not part of this build: exit code 1.
+and, off the render hot path, on the same device code
+  geodesic CONFIG --start x,y,z --dir x,y,z [-o CSV] [--h H]
+      -> trace_geodesic polyline as CSV (rray_main.cpp:86-116) from rr_trace
+  verify [--seed N]
+      -> the property suites restated on the device arithmetic
+         (verify.py; rray_main.cpp:118-131), exit 0 iff all pass, else 2.
 """
 from __future__ import annotations
 
@@ -88,6 +92,52 @@ def cmd_render(cfg: cfgmod.RunConfig, device: int = 0) -> int:
     return 0
 
 
+def _vec3(s: str, flag: str):
+    """rray_main.cpp:38-45."""
+    parts = s.split(",")
+    try:
+        if len(parts) != 3:
+            raise ValueError
+        return [float(x) for x in parts]
+    except ValueError:
+        raise ValidationError(f"{flag} expects x,y,z, got '{s}'") from None
+
+
+def cmd_geodesic(cfg: cfgmod.RunConfig, start, direction, out_path: str, device: int = 0) -> int:
+    """rray_main.cpp:86-116: one geodesic polyline as CSV, traced on the device."""
+    import numpy as np
+    from .render import Renderer
+    try:
+        f = open(out_path, "w")
+    except OSError:
+        raise IoError(f"cannot open '{out_path}' for writing") from None
+    with f:
+        f.write("t,x,y,z,vx,vy,vz\n")
+        row = lambda t, st: f.write(",".join(f"{v:.17g}" for v in (t, *st)) + "\n")
+        r = Renderer(device)
+        try:
+            r.set_config(cfg)
+            g = r.metric_tensor(np.array(start, np.float64))
+            d = np.array(direction, np.float64)
+            ln = float(np.sqrt(d @ g @ d))
+            if ln == 0.0:
+                row(0.0, [*start, *direction])
+                print("warning: zero direction, wrote the start state only", file=sys.stderr)
+                return 0
+            s0 = np.concatenate([np.array(start, np.float64), d / ln])
+            states, counts, fail = r.trace(cfg.integrator, s0[None, :], use_bounds=True)
+        finally:
+            r.close()
+        if fail[0] >= 0:
+            raise NumericError("trace_geodesic: metric evaluation failed (|det J| <= 1e-14) "
+                               f"at step {int(fail[0])}")
+        h = cfg.integrator.h
+        for i in range(int(counts[0])):
+            row(i * h, states[0, i])
+    print(f"{out_path}: {int(counts[0])} states, h = {h:g}")
+    return 0
+
+
 def animated_config(cfg: cfgmod.RunConfig, frame: int, fps: float, omega: float,
                     amp: float) -> cfgmod.RunConfig:
     """Frame `frame` of the BASELINE configs[4] bump animation (static scene)."""
@@ -158,12 +208,31 @@ def main(argv=None) -> int:
     pa.add_argument("--size")
     pa.add_argument("--h", type=float, default=0.0)
     pa.add_argument("--device", type=int, default=0)
-    for name in ("geodesic", "verify"):
-        sub.add_parser(name, help="not part of this build (off the render hot path)")
+    pg = sub.add_parser("geodesic", help="export one geodesic polyline as CSV")
+    pg.add_argument("config")
+    pg.add_argument("--start", required=True)
+    pg.add_argument("--dir", required=True)
+    pg.add_argument("-o", "--output", default="geodesic.csv")
+    pg.add_argument("--h", type=float, default=0.0)
+    pg.add_argument("--print-config", action="store_true")
+    pg.add_argument("--device", type=int, default=0)
+    pv = sub.add_parser("verify", help="run the numerical property suites (on the device)")
+    pv.add_argument("--seed", type=int, default=42)
+    pv.add_argument("--device", type=int, default=0)
     args = p.parse_args(argv)
     try:
-        if args.cmd in ("geodesic", "verify"):
-            raise ValidationError(f"'{args.cmd}' is not part of the B200 render-path build")
+        if args.cmd == "verify":
+            from .verify import cmd_verify
+            return cmd_verify(args.seed, args.device)
+        if args.cmd == "geodesic":
+            out_path = args.output
+            args.output = None                    # -o is the CSV, not output.path
+            cfg = _load(args)
+            if args.print_config:
+                sys.stdout.write(cfgmod.serialize_config(cfg))
+                return 0
+            return cmd_geodesic(cfg, _vec3(args.start, "--start"), _vec3(args.dir, "--dir"),
+                                out_path, args.device)
         if args.cmd == "render":
             cfg = _load(args)
             if args.print_config:

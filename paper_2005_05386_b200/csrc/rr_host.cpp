@@ -420,9 +420,12 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
     return RR_OK;
 }
 
-// ---- FP64 metric tensor at a point (camera only) -------------------------------
-// g = I + grad f grad f^T (metric.cpp:12-15) or J^T J (metric.cpp:40-42).
-int metric_tensor(const Compiled& c, const double p[3], double g[6], std::string& err) {
+// ---- FP64 metric tensor at a point (camera, geodesic export, verify) ------------
+// g = I + grad f grad f^T (metric.cpp:12-15) or J^T J (metric.cpp:40-42);
+// `image` (optional) receives the diffeo chain's image Phi(p).
+int metric_tensor(const Compiled& c, const double p[3], double g[6], std::string& err,
+                  double* image = nullptr, const char* where = "at the camera") {
+    if (image) std::memcpy(image, p, 3 * sizeof(double));
     double J[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
     if (c.metric_kind == RR_METRIC_GRAPH) {
         double f[3] = {0, 0, 0};
@@ -499,8 +502,9 @@ int metric_tensor(const Compiled& c, const double p[3], double g[6], std::string
             dprod *= ds;
             vmin = std::min(vmin, std::fabs(dprod));
         }
+        if (image) std::memcpy(image, x, sizeof x);
         if (!c.stages.empty() && !(std::min(vmin, std::fabs(det3(J))) > 1e-14)) {
-            err = "diffeo_metric: |det J| <= 1e-14 at the camera";
+            err = std::string("diffeo_metric: |det J| <= 1e-14 ") + where;
             return RR_ERR_NUMERIC;
         }
     }
@@ -1042,3 +1046,143 @@ int rr_measure_fp32_peak(rr_ctx* c, double* tflops) {
 const char* rr_last_kernel(const rr_ctx* c) { return c ? c->last_kernel : ""; }
 
 } // extern "C"
+
+// ---- off the render path: geodesic export + device verify ---------------------
+
+namespace {
+
+// sym_inverse (linalg.hpp:223-236): adjugate / det of a symmetric 3x3.
+void sym_inverse6(const double g[6], double inv[6]) {
+    const double a = g[0], b = g[1], c = g[2], d = g[3], e = g[4], f = g[5];
+    const double A = d * f - e * e, B = c * e - b * f, C = b * e - c * d;
+    const double det = a * A + b * B + c * C;
+    inv[0] = A / det;
+    inv[1] = B / det;
+    inv[2] = C / det;
+    inv[3] = (a * f - c * c) / det;
+    inv[4] = (b * c - a * e) / det;
+    inv[5] = (a * d - b * b) / det;
+}
+
+double sym_at(const double s[6], int i, int j) {
+    static const int idx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    return s[idx[i][j]];
+}
+
+} // namespace
+
+int rr_metric_tensor(rr_ctx* c, const double* p, double* g) {
+    if (!c || !p || !g) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    std::string err;
+    const int rc = metric_tensor(c->prog, p, g, err, nullptr, "at the sample point");
+    return rc ? set_err(c, rc, err) : RR_OK;
+}
+
+int rr_diffeo_image(rr_ctx* c, const double* p, double* image) {
+    if (!c || !p || !image) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    double g[6];
+    std::string err;
+    metric_tensor(c->prog, p, g, err, image, "at the sample point");   // image even if singular
+    return RR_OK;
+}
+
+int rr_christoffel_fd(rr_ctx* c, const double* p, double h_fd, double* gamma) {
+    if (!c || !p || !gamma || !(h_fd > 0.0)) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    // metric.cpp:88-133: central differences over a 6-point stencil, then
+    // Gamma^m_ij = 1/2 g^{mk} (d_i g_jk + d_j g_ik - d_k g_ij), symmetrised.
+    std::string err;
+    double dg[3][6], g[6], ginv[6];
+    for (int k = 0; k < 3; ++k) {
+        double pp[3] = {p[0], p[1], p[2]}, pm[3] = {p[0], p[1], p[2]}, gp[6], gm[6];
+        pp[k] += h_fd;
+        pm[k] -= h_fd;
+        if (metric_tensor(c->prog, pp, gp, err, nullptr, "at a stencil point") ||
+            metric_tensor(c->prog, pm, gm, err, nullptr, "at a stencil point"))
+            return set_err(c, RR_ERR_NUMERIC, "christoffel_fd: " + err);
+        for (int q = 0; q < 6; ++q) dg[k][q] = (1.0 / (2.0 * h_fd)) * (gp[q] - gm[q]);
+    }
+    if (metric_tensor(c->prog, p, g, err, nullptr, "at the sample point"))
+        return set_err(c, RR_ERR_NUMERIC, "christoffel_fd: " + err);
+    sym_inverse6(g, ginv);
+    double raw[3][3][3];
+    for (int m = 0; m < 3; ++m)
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < 3; ++k)
+                    acc += (sym_at(dg[i], j, k) + sym_at(dg[j], i, k) - sym_at(dg[k], i, j)) *
+                           sym_at(ginv, k, m);
+                raw[m][i][j] = 0.5 * acc;
+            }
+    static const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int m = 0; m < 3; ++m)
+        for (int q = 0; q < 6; ++q) {
+            const int i = ij[q][0], j = ij[q][1];
+            gamma[6 * m + q] = 0.5 * (raw[m][i][j] + raw[m][j][i]);
+        }
+    return RR_OK;
+}
+
+int rr_accel(rr_ctx* c, const double* pos, const double* vel, size_t n, double* acc,
+             double* validity) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    if (n == 0) return RR_OK;
+    if (!pos || !vel || !acc || !validity) return set_err(c, RR_ERR_CONFIG, "pos/vel/acc/validity: required");
+    if (n > (size_t)1 << 28) return set_err(c, RR_ERR_CONFIG, "n: too large");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    double* d = nullptr;
+    const size_t b3 = 3 * n * sizeof(double);
+    RR_CUDA(c, cudaMalloc(&d, 3 * b3 + n * sizeof(double)));
+    cudaError_t e = cudaMemcpyAsync(d, pos, b3, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + 3 * n, vel, b3, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+        e = rr::launch_accel_points(*c->P, d, d + 3 * n, (int)n, d + 6 * n, d + 9 * n, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(acc, d + 6 * n, b3, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(validity, d + 9 * n, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    return e == cudaSuccess ? RR_OK : cuda_err(c, e, "rr_accel");
+}
+
+int rr_trace(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* starts, size_t n,
+             int use_bounds, double* states, int32_t* counts, int32_t* fail_step) {
+    if (!c || !integ) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    if (!(integ->h > 0.0)) return set_err(c, RR_ERR_CONFIG, "integrator.h: must be > 0");
+    if (integ->max_steps < 1) return set_err(c, RR_ERR_CONFIG, "integrator.max_steps: must be >= 1");
+    if (integ->scheme != RR_SCHEME_EULER && integ->scheme != RR_SCHEME_RK4)
+        return set_err(c, RR_ERR_CONFIG, "rr_trace: integrator.scheme must be euler|rk4 (polylines are uniform in t)");
+    if (n == 0) return RR_OK;
+    if (!starts || !states || !counts || !fail_step)
+        return set_err(c, RR_ERR_CONFIG, "starts/states/counts/fail_step: required");
+    const size_t per = (size_t)(integ->max_steps + 1) * 6;
+    if (n > ((size_t)1 << 34) / (per * sizeof(double)))
+        return set_err(c, RR_ERR_CONFIG, "rr_trace: n x (max_steps+1) states exceed 16 GB");
+    RR_CUDA(c, cudaSetDevice(c->device));
+    double* d = nullptr;
+    const size_t b_in = n * sizeof(rr_ray_start), b_out = n * per * sizeof(double);
+    RR_CUDA(c, cudaMalloc(&d, b_in + b_out + 2 * n * sizeof(int)));
+    double* d_states = d + 6 * n;
+    int* d_counts = reinterpret_cast<int*>(d_states + n * per);
+    cudaError_t e = cudaMemcpyAsync(d, starts, b_in, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+        e = rr::launch_trace(*c->P, d, (int)n, (float)integ->h, integ->max_steps, integ->scheme,
+                             use_bounds, d_states, d_counts, d_counts + n, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(states, d_states, b_out, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(counts, d_counts, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(fail_step, d_counts + n, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    return e == cudaSuccess ? RR_OK : cuda_err(c, e, "rr_trace");
+}

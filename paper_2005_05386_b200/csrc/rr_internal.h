@@ -28,6 +28,15 @@ cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int ti
                           int tile_h, int n_shards, int max_tiles_per_shard, uint8_t* rgb,
                           cudaStream_t stream);
 
+// Off the render path: trace_geodesic polylines (scheme 0 Euler / 1 RK4;
+// states n x (max_steps+1) x 6 doubles) and flow_accel at n points, all
+// device buffers, on `s`.
+cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float h, int max_steps,
+                         int scheme, int use_bounds, double* states, int* counts, int* fail,
+                         cudaStream_t s);
+cudaError_t launch_accel_points(const DevParams& P, const double* pos, const double* vel, int n,
+                                double* acc, double* validity, cudaStream_t s);
+
 // Dense FFMA microbenchmark; returns TFLOP/s (2 flop per FFMA).
 cudaError_t measure_fp32_peak(int num_sms, double* tflops);
 

@@ -1470,6 +1470,97 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
     if (s == 12345.678f) out[0] = s;   // keep the chains alive
 }
 
+
+// ---------------------------------------------------------------------------
+// Off the render path (geodesic export + device verify): one thread per
+// geodesic.  trace_geodesic (integrate.cpp:40-54): states[0] = start, one
+// state per step, stop after the state that left the bounds (when asked) or
+// at the first step whose metric evaluation failed (fail = step index).
+// Positions carry the same compensated sum as the march.
+template <int KIND, int NB, int SCHEME>
+__global__ void __launch_bounds__(128) trace_kernel(const __grid_constant__ DevParams P,
+                                                    const double* __restrict__ starts, int n,
+                                                    float h, int max_steps, int use_bounds,
+                                                    double* __restrict__ states,
+                                                    int* __restrict__ counts, int* __restrict__ fail) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const double* s0 = starts + 6 * (size_t)r;
+    double* out = states + (size_t)r * (size_t)(max_steps + 1) * 6;
+    for (int k = 0; k < 6; ++k) out[k] = s0[k];
+    F3 p = f3((float)s0[0], (float)s0[1], (float)s0[2]);
+    F3 v = f3((float)s0[3], (float)s0[4], (float)s0[5]);
+    float cx = (float)(s0[0] - (double)p.x), cy = (float)(s0[1] - (double)p.y),
+          cz = (float)(s0[2] - (double)p.z);   // carried low part (added back)
+    cx = -cx; cy = -cy; cz = -cz;               // Kahan convention: true = p - c
+    const uint32_t um = P.all_mask;
+    int cnt = 1, fs = -1;
+    for (int i = 0; i < max_steps; ++i) {
+        float valid = 3.0e38f;
+        F3 dp, vn;
+        if constexpr (SCHEME == 0) {                                 // integrate.hpp:55-61
+            const F3 a = accel<KIND, NB>(P, um, p, v, valid);
+            dp = f3(h * v.x, h * v.y, h * v.z);
+            vn = f3(fmaf(h, a.x, v.x), fmaf(h, a.y, v.y), fmaf(h, a.z, v.z));
+        } else {                                                     // integrate.hpp:63-93
+            const float half = 0.5f * h, sixth = h / 6.f;
+            F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f), ps = p, vs = v;
+            for (int st = 0; st < 4; ++st) {
+                const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
+                const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
+                sx = f3(fmaf(wgt, vs.x, sx.x), fmaf(wgt, vs.y, sx.y), fmaf(wgt, vs.z, sx.z));
+                sv = f3(fmaf(wgt, a.x, sv.x), fmaf(wgt, a.y, sv.y), fmaf(wgt, a.z, sv.z));
+                const float c = st < 2 ? half : h;
+                ps = f3(fmaf(c, vs.x, p.x), fmaf(c, vs.y, p.y), fmaf(c, vs.z, p.z));
+                vs = f3(fmaf(c, a.x, v.x), fmaf(c, a.y, v.y), fmaf(c, a.z, v.z));
+            }
+            dp = f3(sixth * sx.x, sixth * sx.y, sixth * sx.z);
+            vn = f3(fmaf(sixth, sv.x, v.x), fmaf(sixth, sv.y, v.y), fmaf(sixth, sv.z, v.z));
+        }
+        if (KIND == kDiffeo && !(valid > 1e-14f)) {                  // integrate.cpp:48
+            fs = i;
+            break;
+        }
+        const float yx = dp.x - cx, yy = dp.y - cy, yz = dp.z - cz;
+        const F3 pn = f3(p.x + yx, p.y + yy, p.z + yz);
+        cx = (pn.x - p.x) - yx;
+        cy = (pn.y - p.y) - yy;
+        cz = (pn.z - p.z) - yz;
+        p = pn;
+        v = vn;
+        double* o = out + 6 * (size_t)cnt++;
+        o[0] = (double)p.x - (double)cx;
+        o[1] = (double)p.y - (double)cy;
+        o[2] = (double)p.z - (double)cz;
+        o[3] = v.x;
+        o[4] = v.y;
+        o[5] = v.z;
+        if (use_bounds && !inside_bounds(P, p)) break;               // integrate.cpp:51
+    }
+    counts[r] = cnt;
+    fail[r] = fs;
+}
+
+// flow_accel (integrate.hpp:46-53) at n points: acc = -Gamma(y, y), validity
+// = min |det J| over the diffeo stages (1 for graph / Euclidean metrics).
+template <int KIND, int NB>
+__global__ void __launch_bounds__(128) accel_points_kernel(const __grid_constant__ DevParams P,
+                                                           const double* __restrict__ pos,
+                                                           const double* __restrict__ vel, int n,
+                                                           double* __restrict__ acc,
+                                                           double* __restrict__ validity) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const F3 p = f3((float)pos[3 * r], (float)pos[3 * r + 1], (float)pos[3 * r + 2]);
+    const F3 v = f3((float)vel[3 * r], (float)vel[3 * r + 1], (float)vel[3 * r + 2]);
+    float valid = 3.0e38f;
+    const F3 a = accel<KIND, NB>(P, P.all_mask, p, v, valid);
+    acc[3 * r] = a.x;
+    acc[3 * r + 1] = a.y;
+    acc[3 * r + 2] = a.z;
+    validity[r] = KIND == kDiffeo ? (double)valid : 1.0;
+}
+
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 int occupancy_of() {
     static int occ = [] {
@@ -1552,7 +1643,58 @@ cudaError_t dispatch_scheme(const DevParams& P, const DevLaunch& L, cudaStream_t
                           : dispatch_kind<SCHEME, false>(P, L, s, sms, name);
 }
 
+
+template <int KIND, int NB>
+cudaError_t trace_kind(const DevParams& P, const double* starts, int n, float h, int max_steps,
+                       int scheme, int use_bounds, double* states, int* counts, int* fail,
+                       cudaStream_t s) {
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    if (scheme == 0)
+        trace_kernel<KIND, NB, 0><<<blocks, 128, 0, s>>>(P, starts, n, h, max_steps, use_bounds,
+                                                          states, counts, fail);
+    else
+        trace_kernel<KIND, NB, 1><<<blocks, 128, 0, s>>>(P, starts, n, h, max_steps, use_bounds,
+                                                          states, counts, fail);
+    return cudaGetLastError();
+}
+
 } // namespace
+
+cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float h, int max_steps,
+                         int scheme, int use_bounds, double* states, int* counts, int* fail,
+                         cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    switch (P.kind) {
+        case kEuclid:
+            return trace_kind<kEuclid, 0>(P, starts, n, h, max_steps, scheme, use_bounds, states, counts, fail, s);
+        case kBumps:
+            return trace_kind<kBumps, 32>(P, starts, n, h, max_steps, scheme, use_bounds, states, counts, fail, s);
+        case kGraphGeneral:
+            return trace_kind<kGraphGeneral, 0>(P, starts, n, h, max_steps, scheme, use_bounds, states, counts, fail, s);
+        default:
+            return trace_kind<kDiffeo, 0>(P, starts, n, h, max_steps, scheme, use_bounds, states, counts, fail, s);
+    }
+}
+
+cudaError_t launch_accel_points(const DevParams& P, const double* pos, const double* vel, int n,
+                                double* acc, double* validity, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    switch (P.kind) {
+        case kEuclid:
+            accel_points_kernel<kEuclid, 0><<<blocks, 128, 0, s>>>(P, pos, vel, n, acc, validity);
+            break;
+        case kBumps:
+            accel_points_kernel<kBumps, 32><<<blocks, 128, 0, s>>>(P, pos, vel, n, acc, validity);
+            break;
+        case kGraphGeneral:
+            accel_points_kernel<kGraphGeneral, 0><<<blocks, 128, 0, s>>>(P, pos, vel, n, acc, validity);
+            break;
+        default:
+            accel_points_kernel<kDiffeo, 0><<<blocks, 128, 0, s>>>(P, pos, vel, n, acc, validity);
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream, int num_sms,
                          const char** kernel_name) {

@@ -48,6 +48,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         return _lib
 
 
+def _sym(s) -> np.ndarray:
+    """{xx, xy, xz, yy, yz, zz} -> symmetric 3x3."""
+    return np.array([[s[0], s[1], s[2]], [s[1], s[3], s[4]], [s[2], s[4], s[5]]], np.float64)
+
+
 def _addr(a) -> C.c_void_p:
     """Device/host address of a numpy array, torch tensor or int."""
     if a is None:
@@ -183,6 +188,51 @@ class Renderer:
     def detile(self, d_gathered, width, height, tile_w, tile_h, n_shards, d_rgb, stream=None):
         self._check(self.lib.rr_detile(self.ctx, _addr(d_gathered), width, height, tile_w, tile_h,
                                        n_shards, _addr(d_rgb), _addr(stream)))
+
+    # -- off the render path: geodesic export + device verify --------------
+    def trace(self, integ: IntegratorConfig, starts: np.ndarray, use_bounds: bool = True):
+        """trace_geodesic (integrate.cpp:40-54) on the device for each start
+        (n x 6 doubles {x, y, z, vx, vy, vz}) -> (states n x (max_steps+1) x 6,
+        counts n, fail_step n)."""
+        starts = np.ascontiguousarray(np.asarray(starts, np.float64).reshape(-1, 6))
+        n = len(starts)
+        states = np.zeros((n, integ.max_steps + 1, 6), np.float64)
+        counts = np.zeros(n, np.int32)
+        fail = np.zeros(n, np.int32)
+        it = integ.to_abi()
+        self._check(self.lib.rr_trace(self.ctx, C.byref(it), _addr(starts), n, int(use_bounds),
+                                      _addr(states), _addr(counts), _addr(fail)))
+        return states, counts, fail
+
+    def accel(self, pos: np.ndarray, vel: np.ndarray):
+        """Device flow_accel (integrate.hpp:46-53): (-Gamma(vel, vel), validity)."""
+        pos = np.ascontiguousarray(np.asarray(pos, np.float64).reshape(-1, 3))
+        vel = np.ascontiguousarray(np.asarray(vel, np.float64).reshape(-1, 3))
+        acc = np.zeros_like(pos)
+        val = np.zeros(len(pos), np.float64)
+        self._check(self.lib.rr_accel(self.ctx, _addr(pos), _addr(vel), len(pos), _addr(acc),
+                                      _addr(val)))
+        return acc, val
+
+    def metric_tensor(self, p) -> np.ndarray:
+        """FP64 g(p) as a 3x3 matrix (metric.cpp:12-15, :40-42)."""
+        p = np.ascontiguousarray(p, np.float64)
+        g = np.zeros(6, np.float64)
+        self._check(self.lib.rr_metric_tensor(self.ctx, _addr(p), _addr(g)))
+        return _sym(g)
+
+    def christoffel_fd(self, p, h_fd: float = 1e-4) -> np.ndarray:
+        """FP64 finite-difference Gamma[m, i, j] (metric.cpp:88-133)."""
+        p = np.ascontiguousarray(p, np.float64)
+        gam = np.zeros(18, np.float64)
+        self._check(self.lib.rr_christoffel_fd(self.ctx, _addr(p), h_fd, _addr(gam)))
+        return np.stack([_sym(gam[6 * m:6 * m + 6]) for m in range(3)])
+
+    def diffeo_image(self, p) -> np.ndarray:
+        p = np.ascontiguousarray(p, np.float64)
+        out = np.zeros(3, np.float64)
+        self._check(self.lib.rr_diffeo_image(self.ctx, _addr(p), _addr(out)))
+        return out
 
     def fp32_peak_tflops(self) -> float:
         v = C.c_double()

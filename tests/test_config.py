@@ -139,7 +139,9 @@ def test_cli_print_config_and_exit_codes(tmp_path):
     bad = tmp_path / "bad.json"
     bad.write_text('{"metric": {"kind": "x"}}')
     assert _cli("render", str(bad)).returncode == 1
-    assert _cli("verify").returncode == 1
+    # geodesic: argument errors are config errors (rray_main.cpp:38-45) before any device work
+    assert _cli("geodesic", cfgp, "--start", "1,2", "--dir", "1,0,0").returncode == 1
+    assert _cli("geodesic", cfgp, "--start", "0,0,0", "--dir", "1,0,0", "--print-config").returncode == 0
 
 
 def test_animation_moves_bump_centres():
