@@ -451,6 +451,9 @@ def run_b200(args, cfg):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if rank != 0:
+            target = None             # drop the IPC mapping before rank 0 frees its frame
+            torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
     r.close()

@@ -289,7 +289,10 @@ int rr_render_tiles(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* inte
  * row-major RGB8 frame d_frame, which may live on ANOTHER GPU (a CUDA-IPC /
  * peer mapping of rank 0's frame: the shade epilogue's stores travel over
  * NVLink, no gather or detile pass).  Visibility to the frame's owner
- * follows kernel completion plus a cross-rank synchronisation. */
+ * follows kernel completion plus a cross-rank synchronisation.  As for every
+ * `stream` argument, NULL selects the context's own NON-BLOCKING stream,
+ * which is not ordered after work on the legacy default stream: initialise
+ * d_frame (if at all) and synchronise before the call. */
 int rr_render_shard(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
                     int height, int tile_w, int tile_h, int shard, int n_shards,
                     uint8_t* d_frame, rr_stats* stats, void* stream);

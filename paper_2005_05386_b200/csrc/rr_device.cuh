@@ -59,6 +59,16 @@ struct DevBump {          // one Gaussian term in factored form
     float sgn;            // sign(amplitude)
 };
 
+// Two bump slots (2k, 2k+1) interleaved for the packed-FP32 (FFMA2) path:
+// each field is a {slot 2k, slot 2k+1} float2, read as one 64-bit uniform
+// operand.  Empty slots: la = -inf, K = 0, sgn = 0.
+struct alignas(8) DevBump2 {
+    float2 ncx, ncy, ncz;  // -centre
+    float2 kx, ky, kz;     // K
+    float2 la;             // log2 |amplitude|
+    float2 sgn;            // sign(amplitude)
+};
+
 struct DevPoly {          // coef * x^a y^b z^c
     float coef;
     int a, b, c;
@@ -138,6 +148,7 @@ struct DevParams {
     int skip;                     // 1: empty-space skipping enabled
     float cell_min;               // smallest culling-cell edge (world units)
     DevBump bumps[kMaxBumps];
+    DevBump2 bumps2[kMaxBumps / 2];   // the same slots, paired (packed FP32 path)
     DevPoly poly[kMaxPoly];
     DevStage stages[kMaxStages];
     DevSphere spheres[kMaxPrims];

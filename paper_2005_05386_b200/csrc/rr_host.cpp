@@ -256,6 +256,19 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
         if (slot < 32) P.all_mask |= 1u << slot;
         slots_out[j] = slot;
     }
+    for (int k = 0; k < rr::kMaxBumps / 2; ++k) {          // paired copy for FFMA2
+        const rr::DevBump& a = P.bumps[2 * k];
+        const rr::DevBump& b = P.bumps[2 * k + 1];
+        rr::DevBump2& d = P.bumps2[k];
+        d.ncx = make_float2(-a.cx, -b.cx);
+        d.ncy = make_float2(-a.cy, -b.cy);
+        d.ncz = make_float2(-a.cz, -b.cz);
+        d.kx = make_float2(a.kx, b.kx);
+        d.ky = make_float2(a.ky, b.ky);
+        d.kz = make_float2(a.kz, b.kz);
+        d.la = make_float2(a.la, b.la);
+        d.sgn = make_float2(a.sgn, b.sgn);
+    }
     P.n_poly = (int)c.poly.size();
     for (size_t i = 0; i < c.poly.size(); ++i)
         P.poly[i] = {(float)c.poly[i].coef, c.poly[i].p[0], c.poly[i].p[1], c.poly[i].p[2]};

@@ -27,6 +27,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_GROUP_TESTS
 #define RR_GROUP_TESTS 1
 #endif
+#ifndef RR_PAIRED_BUMPS
+// 1: two bump slots per packed FP32 instruction (FFMA2/FADD2/FMUL2).  Measured
+// slower on B200 (C3 14.16 vs 13.76 ms, C1 3.18 vs 2.84 ms, profiles/r1e_ffma2.md):
+// the unculled partner slot's work outweighs the issue-slot saving.
+#define RR_PAIRED_BUMPS 0
+#endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
 #endif
@@ -99,6 +105,81 @@ __device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p,
     const float w = fmaf(kBeta * kBeta, fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)), 1.f);
     const float r = Q * rcp_approx(w) * kBeta;
     return f3(r * Gx, r * Gy, r * Gz);
+}
+
+// Packed FP32 (sm_100 FFMA2 / FADD2 / FMUL2): two bump slots per
+// instruction.  Issue slots, not FMA-pipe cycles, bound the march, and a
+// packed instruction does two slots' arithmetic in one issue.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ u64 ld2(const float2& f) { return *reinterpret_cast<const u64*>(&f); }
+__device__ __forceinline__ float hsum2(u64 v) {
+    float a, b;
+    upk2(v, a, b);
+    return a + b;
+}
+
+// accel_bumps with slot pairs: a pair is evaluated when either slot is in
+// `um` (an unculled partner adds its exact, negligible term).
+template <int NB>
+__device__ __forceinline__ F3 accel_bumps2(const DevParams& P, uint32_t um, F3 p, F3 y) {
+    const u64 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pz = pk2(p.z, p.z);
+    const u64 yx = pk2(y.x, y.x), yy = pk2(y.y, y.y), yz = pk2(y.z, y.z);
+    u64 Gx = 0ull, Gy = 0ull, Gz = 0ull, Q1 = 0ull, Sx = 0ull, Sy = 0ull, Sz = 0ull;
+#pragma unroll
+    for (int g = 0; g < NB; g += 4) {
+#if RR_GROUP_TESTS
+        if (!((um >> g) & 0xFu)) continue;
+#endif
+#pragma unroll
+        for (int j = g; j < g + 4; j += 2) {
+            if ((um >> j) & 3u) {
+                const DevBump2& b = P.bumps2[j >> 1];
+                const u64 dx = add2(px, ld2(b.ncx)), dy = add2(py, ld2(b.ncy)), dz = add2(pz, ld2(b.ncz));
+                const u64 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
+                const u64 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
+                float q0, q1;
+                upk2(q, q0, q1);
+                const u64 v = mul2(pk2(ex2(q0), ex2(q1)), ld2(b.sgn));
+                Gx = fma2(v, gx, Gx);
+                Gy = fma2(v, gy, Gy);
+                Gz = fma2(v, gz, Gz);
+                const u64 t = fma2(yx, gx, fma2(yy, gy, mul2(yz, gz)));
+                Q1 = fma2(mul2(v, t), t, Q1);
+                Sx = fma2(v, ld2(b.kx), Sx);
+                Sy = fma2(v, ld2(b.ky), Sy);
+                Sz = fma2(v, ld2(b.kz), Sz);
+            }
+        }
+    }
+    const float gX = hsum2(Gx), gY = hsum2(Gy), gZ = hsum2(Gz);
+    const float ys = fmaf(y.x * y.x, hsum2(Sx), fmaf(y.y * y.y, hsum2(Sy), y.z * y.z * hsum2(Sz)));
+    const float Q = fmaf(kBeta * kBeta, hsum2(Q1), -kBeta * ys);
+    const float w = fmaf(kBeta * kBeta, fmaf(gX, gX, fmaf(gY, gY, gZ * gZ)), 1.f);
+    const float r = Q * rcp_approx(w) * kBeta;
+    return f3(r * gX, r * gY, r * gZ);
 }
 
 // ---------------------------------------------------------------------------
@@ -300,7 +381,11 @@ __device__ __forceinline__ F3 accel(const DevParams& P, uint32_t um, F3 p, F3 y,
     if constexpr (KIND == kEuclid) {
         return f3(0.f, 0.f, 0.f);
     } else if constexpr (KIND == kBumps) {
+#if RR_PAIRED_BUMPS
+        return accel_bumps2<NB>(P, um, p, y);
+#else
         return accel_bumps<NB>(P, um, p, y);
+#endif
     } else if constexpr (KIND == kGraphGeneral) {
         return accel_graph_general(P, p, y);
     } else {
