@@ -263,7 +263,10 @@ int rr_march_device(rr_ctx* ctx, const rr_integrator* integ, const rr_ray_start*
                     rr_pixel_outcome* d_out, size_t n, void* stream);
 
 /* Whole-frame render (render::render, render.cpp:43-111): device raygen +
- * march + shade, RGB8 row-major into a HOST buffer of 3*w*h bytes. */
+ * march + shade, RGB8 row-major into a HOST buffer of 3*w*h bytes.  When the
+ * buffer is page-locked (cudaHostAlloc / cudaHostRegister / torch
+ * pin_memory) the kernel writes the pixels straight into it through its UVA
+ * mapping; pageable buffers get a device->host copy after the kernel. */
 int rr_render(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
               int height, uint8_t* rgb_out, rr_stats* stats);
 

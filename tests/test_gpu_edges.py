@@ -93,3 +93,29 @@ def test_large_frame_accounting(renderer):
     b, _ = renderer.render(cam, cfg.integrator, 3840, 2160)
     assert st["rays"] == 3840 * 2160 and np.array_equal(a, b)
     assert 150 < st["total_steps"] / st["rays"] < 200     # ~170 reference steps/ray
+
+
+def test_pinned_host_output_is_written_by_the_kernel():
+    """rr_render stores straight into page-locked caller memory (UVA) and
+    gives the same bytes as the pageable (device buffer + copy) route."""
+    import torch
+    from paper_2005_05386_b200.config import load_config
+    from paper_2005_05386_b200.render import Renderer
+    cfg = load_config(os.path.join(ROOT, "configs", "c3_bumps16_1080p.json"))
+    cfg.scene.lights = []
+    r = Renderer(0)
+    r.set_config(cfg)
+    cam = r.build_camera(cfg.camera)
+    w, h = 321, 179
+    pageable, st0 = r.render(cam, cfg.integrator, w, h)
+    pinned = torch.full((h, w, 3), 7, dtype=torch.uint8).pin_memory()
+    _, st1 = r.render(cam, cfg.integrator, w, h, out=pinned)
+    assert np.array_equal(pinned.numpy(), pageable)
+    assert st0["total_steps"] == st1["total_steps"]
+    from paper_2005_05386_b200.config import Light
+    cfg.scene.lights = [Light([2.0, 3.0, 4.0], 0.6)]
+    r.set_config(cfg)
+    lit, _ = r.render(cam, cfg.integrator, w, h)
+    _, _ = r.render(cam, cfg.integrator, w, h, out=pinned)
+    assert np.array_equal(pinned.numpy(), lit)
+    r.close()
