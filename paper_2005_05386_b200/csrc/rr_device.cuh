@@ -59,14 +59,16 @@ struct DevBump {          // one Gaussian term in factored form
     float sgn;            // sign(amplitude)
 };
 
-// Two bump slots (2k, 2k+1) interleaved for the packed-FP32 (FFMA2) path:
-// each field is a {slot 2k, slot 2k+1} float2, read as one 64-bit uniform
-// operand.  Empty slots: la = -inf, K = 0, sgn = 0.
-struct alignas(8) DevBump2 {
+// One bump slot as broadcast pairs {c, c} for the ray-pair (packed FP32,
+// FFMA2) march: each field is read as one 64-bit uniform operand and applies
+// to both rays of a thread.  Empty slots: la = -inf, K = 0, sgn = 0.
+struct alignas(8) DevBumpB {
     float2 ncx, ncy, ncz;  // -centre
     float2 kx, ky, kz;     // K
     float2 la;             // log2 |amplitude|
     float2 sgn;            // sign(amplitude)
+    uint2 sgnbit;          // sign-bit mask of the amplitude (0 or 0x80000000)
+    float2 kcx, kcy, kcz;  // K * centre
 };
 
 struct DevPoly {          // coef * x^a y^b z^c
@@ -135,6 +137,7 @@ struct DevParams {
     int n_spheres, n_halves, n_grids, n_meshes;
     int nb_slot;          // kBumps: bump slots of the kernel variant (4/8/16/32)
     float h, fog;
+    float inv_h;          // 1 / h
     float ambient;        // EXTENSION: lit shading ambient term
     float tol;            // EXTENSION: rk23 error tolerance
     float lo[3], hi[3];   // scene bounds
@@ -148,7 +151,7 @@ struct DevParams {
     int skip;                     // 1: empty-space skipping enabled
     float cell_min;               // smallest culling-cell edge (world units)
     DevBump bumps[kMaxBumps];
-    DevBump2 bumps2[kMaxBumps / 2];   // the same slots, paired (packed FP32 path)
+    DevBumpB bumpsb[32];              // slots 0..31 as broadcast pairs (ray-pair march)
     DevPoly poly[kMaxPoly];
     DevStage stages[kMaxStages];
     DevSphere spheres[kMaxPrims];

@@ -256,18 +256,22 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
         if (slot < 32) P.all_mask |= 1u << slot;
         slots_out[j] = slot;
     }
-    for (int k = 0; k < rr::kMaxBumps / 2; ++k) {          // paired copy for FFMA2
-        const rr::DevBump& a = P.bumps[2 * k];
-        const rr::DevBump& b = P.bumps[2 * k + 1];
-        rr::DevBump2& d = P.bumps2[k];
-        d.ncx = make_float2(-a.cx, -b.cx);
-        d.ncy = make_float2(-a.cy, -b.cy);
-        d.ncz = make_float2(-a.cz, -b.cz);
-        d.kx = make_float2(a.kx, b.kx);
-        d.ky = make_float2(a.ky, b.ky);
-        d.kz = make_float2(a.kz, b.kz);
-        d.la = make_float2(a.la, b.la);
-        d.sgn = make_float2(a.sgn, b.sgn);
+    for (int k = 0; k < 32; ++k) {                          // broadcast pairs (ray-pair march)
+        const rr::DevBump& a = P.bumps[k];
+        rr::DevBumpB& d = P.bumpsb[k];
+        d.ncx = make_float2(-a.cx, -a.cx);
+        d.ncy = make_float2(-a.cy, -a.cy);
+        d.ncz = make_float2(-a.cz, -a.cz);
+        d.kx = make_float2(a.kx, a.kx);
+        d.ky = make_float2(a.ky, a.ky);
+        d.kz = make_float2(a.kz, a.kz);
+        d.la = make_float2(a.la, a.la);
+        d.sgn = make_float2(a.sgn, a.sgn);
+        const uint32_t m = a.sgn < 0.f ? 0x80000000u : 0u;
+        d.sgnbit = make_uint2(m, m);
+        d.kcx = make_float2(a.kx * a.cx, a.kx * a.cx);
+        d.kcy = make_float2(a.ky * a.cy, a.ky * a.cy);
+        d.kcz = make_float2(a.kz * a.cz, a.kz * a.cz);
     }
     P.n_poly = (int)c.poly.size();
     for (size_t i = 0; i < c.poly.size(); ++i)
@@ -574,6 +578,7 @@ int check_ready(rr_ctx* c, const rr_integrator* integ, cudaStream_t s) {
     if (integ->scheme == RR_SCHEME_RK23 && !(integ->tol > 0.0))
         return set_err(c, RR_ERR_CONFIG, "integrator.tol: must be > 0");
     c->P->h = (float)integ->h;
+    c->P->inv_h = (float)(1.0 / integ->h);
     c->P->max_steps = integ->max_steps;
     c->P->scheme = integ->scheme;
     c->P->tol = (float)integ->tol;

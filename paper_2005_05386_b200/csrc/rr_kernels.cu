@@ -27,11 +27,31 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_GROUP_TESTS
 #define RR_GROUP_TESTS 1
 #endif
-#ifndef RR_PAIRED_BUMPS
-// 1: two bump slots per packed FP32 instruction (FFMA2/FADD2/FMUL2).  Measured
-// slower on B200 (C3 14.16 vs 13.76 ms, C1 3.18 vs 2.84 ms, profiles/r1e_ffma2.md):
-// the unculled partner slot's work outweighs the issue-slot saving.
-#define RR_PAIRED_BUMPS 0
+#ifndef RR_RAY_PAIRS
+// 1: Gaussian-bump frames march two rays per thread with packed FP32
+// (march2_kernel); 0: one ray per thread (march_kernel) for every scene.
+#define RR_RAY_PAIRS 1
+#endif
+#ifndef RR_X2_SLOTS
+#define RR_X2_SLOTS 1      // slots evaluated per test in the ray-pair bump block: 1, 2 or 4
+#endif
+#ifndef RR_X2_SIGNXOR
+#define RR_X2_SIGNXOR 0
+#endif
+#ifndef RR_X2_TTRICK
+#define RR_X2_TTRICK 0
+#endif
+#ifndef RR_X2_GROUP_LOOP
+#define RR_X2_GROUP_LOOP 0
+#endif
+#ifndef RR_MIN_BLOCKS_X2
+// ray-pair kernel occupancy (CUDA-event A/B, profiles/r1g_raypair.md): 7 CTAs
+// (<= 72 registers, ~200 B of spills) beat 5 and 6 on C3; the 4-slot
+// variant (C1) prefers 6.
+#define RR_MIN_BLOCKS_X2 7
+#endif
+#ifndef RR_MIN_BLOCKS_X2_SMALL
+#define RR_MIN_BLOCKS_X2_SMALL 6
 #endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
@@ -107,79 +127,151 @@ __device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p,
     return f3(r * Gx, r * Gy, r * Gz);
 }
 
-// Packed FP32 (sm_100 FFMA2 / FADD2 / FMUL2): two bump slots per
-// instruction.  Issue slots, not FMA-pipe cycles, bound the march, and a
-// packed instruction does two slots' arithmetic in one issue.
+// ---------------------------------------------------------------------------
+// Ray pairs (packed FP32: FADD2 / FMUL2 / FFMA2).  The march is bound by
+// issue slots; a thread that carries TWO rays evaluates every per-ray
+// operation of both with one packed instruction, with the per-bump constants
+// as broadcast 64-bit uniform operands (DevBumpB).  Measured on the bump body
+// alone (tools/microbench/bump_body.cu, profiles/r1g_raypair.md): 0.88 vs
+// 1.10-1.15 ps per ray-bump at 8 active bumps.  (Pairing two bump SLOTS of one
+// ray instead was measured slower: profiles/r1e_ffma2.md.)
 typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk2(float a, float b) {
-    u64 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+struct F2 {           // (ray 0, ray 1)
+    u64 v;
+};
+__device__ __forceinline__ F2 mk2(float a, float b) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
     return r;
 }
-__device__ __forceinline__ void upk2(u64 v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-    u64 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-    u64 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-    u64 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ u64 ld2(const float2& f) { return *reinterpret_cast<const u64*>(&f); }
-__device__ __forceinline__ float hsum2(u64 v) {
+__device__ __forceinline__ F2 bc2(float a) { return mk2(a, a); }
+__device__ __forceinline__ float lo2(F2 x) {
     float a, b;
-    upk2(v, a, b);
-    return a + b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+    return a;
+}
+__device__ __forceinline__ float hi2(F2 x) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+    return b;
+}
+__device__ __forceinline__ float get2(F2 x, int r) { return r ? hi2(x) : lo2(x); }
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+    F2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+    F2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+    F2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+__device__ __forceinline__ F2 ld2(const float2& f) { return F2{*reinterpret_cast<const u64*>(&f)}; }
+// select per ray: r0 ? a.lo : b.lo, r1 ? a.hi : b.hi
+__device__ __forceinline__ F2 sel2(bool r0, bool r1, F2 a, F2 b) {
+    return mk2(r0 ? lo2(a) : lo2(b), r1 ? hi2(a) : hi2(b));
 }
 
-// accel_bumps with slot pairs: a pair is evaluated when either slot is in
-// `um` (an unculled partner adds its exact, negligible term).
+struct P3 {           // a 3-vector for a ray pair
+    F2 x, y, z;
+};
+__device__ __forceinline__ F3 ray_of(const P3& v, int r) { return f3(get2(v.x, r), get2(v.y, r), get2(v.z, r)); }
+__device__ __forceinline__ P3 pair_of(F3 a, F3 b) { return P3{mk2(a.x, b.x), mk2(a.y, b.y), mk2(a.z, b.z)}; }
+
+// accel_bumps for a ray pair (same factored form, same slot tests on the
+// warp-uniform mask of the 64 rays).
 template <int NB>
-__device__ __forceinline__ F3 accel_bumps2(const DevParams& P, uint32_t um, F3 p, F3 y) {
-    const u64 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pz = pk2(p.z, p.z);
-    const u64 yx = pk2(y.x, y.x), yy = pk2(y.y, y.y), yz = pk2(y.z, y.z);
-    u64 Gx = 0ull, Gy = 0ull, Gz = 0ull, Q1 = 0ull, Sx = 0ull, Sy = 0ull, Sz = 0ull;
+__device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, const P3& p, const P3& y) {
+    F2 Gx = bc2(0.f), Gy = bc2(0.f), Gz = bc2(0.f), Q1 = bc2(0.f);
+    F2 Sx = bc2(0.f), Sy = bc2(0.f), Sz = bc2(0.f);
+#if RR_X2_TTRICK
+    // G = sum_j v_j K_j (p - c_j) = p (.) S - T with T = sum_j v_j (K_j c_j):
+    // the G update reads one register pair instead of three
+    F2 Tx = bc2(0.f), Ty = bc2(0.f), Tz = bc2(0.f);
+#endif
+    auto body = [&](const DevBumpB& b) {
+        const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
+        const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
+        const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
+#if RR_X2_SIGNXOR
+        F2 v = mk2(ex2(lo2(q)), ex2(hi2(q)));            // sign applied as a bit flip (ALU pipe)
+        asm("xor.b64 %0, %0, %1;" : "+l"(v.v) : "l"(*reinterpret_cast<const u64*>(&b.sgnbit)));
+#else
+        const F2 v = mul2(mk2(ex2(lo2(q)), ex2(hi2(q))), ld2(b.sgn));
+#endif
+#if RR_X2_TTRICK
+        Tx = fma2(v, ld2(b.kcx), Tx);
+        Ty = fma2(v, ld2(b.kcy), Ty);
+        Tz = fma2(v, ld2(b.kcz), Tz);
+#else
+        Gx = fma2(v, gx, Gx);
+        Gy = fma2(v, gy, Gy);
+        Gz = fma2(v, gz, Gz);
+#endif
+        const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
+        Q1 = fma2(mul2(v, t), t, Q1);
+        Sx = fma2(v, ld2(b.kx), Sx);
+        Sy = fma2(v, ld2(b.ky), Sy);
+        Sz = fma2(v, ld2(b.kz), Sz);
+    };
+#if RR_X2_GROUP_LOOP
+    // groups of 4 slots in a rolled loop (uniform-indexed constant loads):
+    // a quarter of the code footprint of the unrolled block
+#pragma unroll 1
+    for (int g = 0; g < NB; g += 4) {
+        const uint32_t gm = (um >> g) & 0xFu;
+        if (!gm) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (gm & (1u << j)) body(P.bumpsb[g + j]);
+    }
+#else
 #pragma unroll
     for (int g = 0; g < NB; g += 4) {
 #if RR_GROUP_TESTS
         if (!((um >> g) & 0xFu)) continue;
 #endif
+#if RR_X2_SLOTS == 2
+        // slot pairs: both slots of a pair with a bit in um (independent
+        // bodies in one block, so their dependency chains interleave)
 #pragma unroll
-        for (int j = g; j < g + 4; j += 2) {
+        for (int j = g; j < g + 4; j += 2)
             if ((um >> j) & 3u) {
-                const DevBump2& b = P.bumps2[j >> 1];
-                const u64 dx = add2(px, ld2(b.ncx)), dy = add2(py, ld2(b.ncy)), dz = add2(pz, ld2(b.ncz));
-                const u64 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
-                const u64 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
-                float q0, q1;
-                upk2(q, q0, q1);
-                const u64 v = mul2(pk2(ex2(q0), ex2(q1)), ld2(b.sgn));
-                Gx = fma2(v, gx, Gx);
-                Gy = fma2(v, gy, Gy);
-                Gz = fma2(v, gz, Gz);
-                const u64 t = fma2(yx, gx, fma2(yy, gy, mul2(yz, gz)));
-                Q1 = fma2(mul2(v, t), t, Q1);
-                Sx = fma2(v, ld2(b.kx), Sx);
-                Sy = fma2(v, ld2(b.ky), Sy);
-                Sz = fma2(v, ld2(b.kz), Sz);
+                body(P.bumpsb[j]);
+                body(P.bumpsb[j + 1]);
             }
-        }
+#elif RR_X2_SLOTS == 4
+        body(P.bumpsb[g]);                     // whole group of 4
+        body(P.bumpsb[g + 1]);
+        body(P.bumpsb[g + 2]);
+        body(P.bumpsb[g + 3]);
+#else
+#pragma unroll
+        for (int j = g; j < g + 4; ++j)
+            if (um & (1u << j)) body(P.bumpsb[j]);
+#endif
     }
-    const float gX = hsum2(Gx), gY = hsum2(Gy), gZ = hsum2(Gz);
-    const float ys = fmaf(y.x * y.x, hsum2(Sx), fmaf(y.y * y.y, hsum2(Sy), y.z * y.z * hsum2(Sz)));
-    const float Q = fmaf(kBeta * kBeta, hsum2(Q1), -kBeta * ys);
-    const float w = fmaf(kBeta * kBeta, fmaf(gX, gX, fmaf(gY, gY, gZ * gZ)), 1.f);
-    const float r = Q * rcp_approx(w) * kBeta;
-    return f3(r * gX, r * gY, r * gZ);
+#endif
+#if RR_X2_TTRICK
+    Gx = fma2(p.x, Sx, mul2(bc2(-1.f), Tx));
+    Gy = fma2(p.y, Sy, mul2(bc2(-1.f), Ty));
+    Gz = fma2(p.z, Sz, mul2(bc2(-1.f), Tz));
+#endif
+    const F2 ys = fma2(mul2(y.x, y.x), Sx, fma2(mul2(y.y, y.y), Sy, mul2(mul2(y.z, y.z), Sz)));
+    const F2 Q = fma2(bc2(kBeta * kBeta), Q1, mul2(bc2(-kBeta), ys));
+    const F2 w = fma2(bc2(kBeta * kBeta), fma2(Gx, Gx, fma2(Gy, Gy, mul2(Gz, Gz))), bc2(1.f));
+    const F2 r = mul2(mul2(Q, mk2(rcp_approx(lo2(w)), rcp_approx(hi2(w)))), bc2(kBeta));
+    return P3{mul2(r, Gx), mul2(r, Gy), mul2(r, Gz)};
 }
 
 // ---------------------------------------------------------------------------
@@ -381,11 +473,7 @@ __device__ __forceinline__ F3 accel(const DevParams& P, uint32_t um, F3 p, F3 y,
     if constexpr (KIND == kEuclid) {
         return f3(0.f, 0.f, 0.f);
     } else if constexpr (KIND == kBumps) {
-#if RR_PAIRED_BUMPS
-        return accel_bumps2<NB>(P, um, p, y);
-#else
         return accel_bumps<NB>(P, um, p, y);
-#endif
     } else if constexpr (KIND == kGraphGeneral) {
         return accel_graph_general(P, p, y);
     } else {
@@ -1290,7 +1378,11 @@ __device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, ui
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const float frac = pv[k] - floorf(pv[k]);
-        long v = lroundf(255.f * (frac * atten * light));
+        // lround (half away from zero) for the non-negative argument, without
+        // the 64-bit conversion code of lroundf: trunc + exact fraction test
+        const float x = 255.f * (frac * atten * light);
+        const float tr = truncf(x);
+        int v = (int)tr + ((x - tr) >= 0.5f ? 1 : 0);
         v = v < 0 ? 0 : (v > 255 ? 255 : v);
         rgb[k] = (uint8_t)v;
     }
@@ -1309,6 +1401,193 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
     const double inv = 1.0 / sqrt(n2);
     pos = f3((float)c.pos[0], (float)c.pos[1], (float)c.pos[2]);
     dir = f3((float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
+}
+
+// ---------------------------------------------------------------------------
+// Ray-pair march (Gaussian-bump metric, fixed-step RK4, mesh-free scenes):
+// march_fixed for two rays per thread.  The integrator and the metric run
+// packed (F2 / P3); the culling lookup, the chord test and the termination
+// bookkeeping run per ray on the unpacked halves with exactly march_fixed's
+// rules (kernel_impl.hpp:22-94).  The warp-uniform bump mask is the OR over
+// the 64 rays of the unit.
+#ifndef RR_X2_CALLS
+#define RR_X2_CALLS 0      // 1: chord test / jump length as real calls (one code copy for both rays)
+#endif
+#if RR_X2_CALLS
+__device__ __noinline__ bool intersect_call(const DevParams& P, F3 a, F3 b, float& s, int& prim, int& hid) {
+    float mfree = 0.f;
+    int mrec = 0;
+    return intersect<false>(P, a, b, s, prim, hid, mfree, mrec);
+}
+#define RR_JUMP_INLINE __noinline__
+#else
+#define RR_JUMP_INLINE __forceinline__
+#endif
+
+template <int PASS>
+__device__ RR_JUMP_INLINE int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
+                                          float light_d) {
+    const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
+    const float isp = rsqrtf(speed2);
+    float L = (float)(k - 1) * P.cell_min;
+    float te = 3.0e38f;   // parameter distance to the bounds exit along v
+    if (v.x != 0.f) te = fminf(te, __fdividef((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x, v.x));
+    if (v.y != 0.f) te = fminf(te, __fdividef((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y, v.y));
+    if (v.z != 0.f) te = fminf(te, __fdividef((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z, v.z));
+    L = fminf(L, te * speed2 * isp);
+    if (PASS == kPassShadow) {
+        const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
+        L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
+    }
+    const float n = floorf(L * isp * P.inv_h) - 1.f;   // fast division: the -1 step margin covers it
+    const int nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
+    return nj < 2 ? 0 : nj;
+}
+
+template <int PASS>
+__device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
+                                             int r, const RayResult& res);
+
+// Marches a ray pair.  Primary passes write each ray's output when it
+// terminates (emit_primary); every pass returns per-ray status and
+// reference-equivalent step counts.
+template <int NB, int PASS>
+__device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool live1, P3 p, P3 v,
+                                           LaneCounters& cnt, const DevLaunch& L, unsigned unit,
+                                           int (&status)[2], int (&steps)[2], float (&tout)[2],
+                                           F3 (&pout)[2], F3 q0 = F3{0.f, 0.f, 0.f},
+                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f) {
+    status[0] = status[1] = PASS == kPassShadow ? 1 : 0;
+    steps[0] = steps[1] = 0;
+    bool act[2] = {live0, live1};
+    int step[2] = {0, 0};
+    const F3 qq[2] = {q0, q1};
+    const float dd[2] = {d20, d21};
+    float light_d[2] = {0.f, 0.f};
+    if (PASS == kPassShadow) {
+        light_d[0] = sqrtf(d20);
+        light_d[1] = sqrtf(d21);
+    }
+    const float h = P.h;
+    const F2 half = bc2(0.5f * h), full = bc2(h), sixth = bc2(h / 6.f);
+    P3 c{bc2(0.f), bc2(0.f), bc2(0.f)};    // Kahan compensation of the position sums
+    for (;;) {
+        if (!__any_sync(kFull, act[0] || act[1])) break;
+        cnt.lane_slots += 2;
+        int nj[2] = {0, 0};
+        uint32_t lmo = 0u;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            uint32_t lm = 0u;
+            unsigned cell = 0;
+            if (act[r]) {
+                if (P.cull) {
+                    cell = cell_of(P, ray_of(p, r));
+                    lm = __ldg(P.cull_masks + cell);
+                } else {
+                    lm = P.all_mask;
+                }
+                if (P.skip && lm == 0u) {
+                    const int k = __ldg(P.skip_k + cell);
+                    if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r]);
+                }
+            }
+            lmo |= nj[r] ? 0u : lm;
+        }
+        const uint32_t um = __reduce_or_sync(kFull, lmo);
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(um);
+        P3 dp, vn;
+        const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
+        if (__all_sync(kFull, jw0 && jw1)) {                // whole warp jumps: no integration
+            dp = P3{bc2(0.f), bc2(0.f), bc2(0.f)};
+            vn = v;
+        } else {                                             // RK4 (integrate.hpp:63-93)
+            P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
+            P3 ps = p, vs = v;
+#pragma unroll 1
+            for (int st = 0; st < 4; ++st) {   // one call site: the bump block is inlined once
+                const P3 a = accel_bumps_x2<NB>(P, um, ps, vs);
+                const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
+                sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
+                sv = P3{fma2(wgt, a.x, sv.x), fma2(wgt, a.y, sv.y), fma2(wgt, a.z, sv.z)};
+                const F2 cc = st < 2 ? half : full;
+                ps = P3{fma2(cc, vs.x, p.x), fma2(cc, vs.y, p.y), fma2(cc, vs.z, p.z)};
+                vs = P3{fma2(cc, a.x, v.x), fma2(cc, a.y, v.y), fma2(cc, a.z, v.z)};
+            }
+            dp = P3{mul2(sixth, sx.x), mul2(sixth, sx.y), mul2(sixth, sx.z)};
+            vn = P3{fma2(sixth, sv.x, v.x), fma2(sixth, sv.y, v.y), fma2(sixth, sv.z, v.z)};
+        }
+        if (nj[0] | nj[1]) {                                 // straight jumps of nj steps
+            const F2 hn = mk2(h * (float)nj[0], h * (float)nj[1]);
+            const P3 dj{mul2(hn, v.x), mul2(hn, v.y), mul2(hn, v.z)};
+            const bool j0 = nj[0] != 0, j1 = nj[1] != 0;
+            dp = P3{sel2(j0, j1, dj.x, dp.x), sel2(j0, j1, dj.y, dp.y), sel2(j0, j1, dj.z, dp.z)};
+            vn = P3{sel2(j0, j1, v.x, vn.x), sel2(j0, j1, v.y, vn.y), sel2(j0, j1, v.z, vn.z)};
+        }
+        // compensated position update: pn = p + dp carrying the rounding error
+        const P3 yv{sub2(dp.x, c.x), sub2(dp.y, c.y), sub2(dp.z, c.z)};
+        const P3 pn{add2(p.x, yv.x), add2(p.y, yv.y), add2(p.z, yv.z)};
+        c = P3{sub2(sub2(pn.x, p.x), yv.x), sub2(sub2(pn.y, p.y), yv.y), sub2(sub2(pn.z, p.z), yv.z)};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (!act[r]) continue;
+            const F3 a = ray_of(p, r), b = ray_of(pn, r);
+            const int nsub = nj[r] ? nj[r] : 1;
+            cnt.steps_integrated += 1;
+            float s = 0.f, mfree = 0.f;
+            int prim = -1, hid = 0, mrec = 0;
+#if RR_X2_CALLS
+            const bool hit = intersect_call(P, a, b, s, prim, hid);
+#else
+            const bool hit = intersect<false>(P, a, b, s, prim, hid, mfree, mrec);
+#endif
+            if (hit) {                                       // kernel_impl.hpp:63-76
+                const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
+                const float sj = s * (float)nsub;            // hit position in reference steps
+                const int sub = min((int)sj, nsub - 1);
+                if constexpr (PASS == kPassShadow) {
+                    const F3 rr = f3(pt.x - qq[r].x, pt.y - qq[r].y, pt.z - qq[r].z);
+                    status[r] = (rr.x * rr.x + rr.y * rr.y + rr.z * rr.z) < dd[r] ? 0 : 1;
+                } else {
+                    if constexpr (PASS == kPassHits) {
+                        RayResult res{1, prim, 0, ((float)step[r] + sj) * h, pt, f3(0.f, 0.f, 0.f)};
+                        res.normal = hit_normal(P, hid, s, a, b, pt, mrec);
+                        emit_primary<PASS>(P, L, unit, r, res);
+                    } else {
+                        tout[r] = ((float)step[r] + sj) * h;
+                        pout[r] = pt;
+                    }
+                    status[r] = 1;
+                }
+                steps[r] = step[r] + sub + 1;
+                act[r] = false;
+            } else if (PASS == kPassShadow &&
+                       (b.x - qq[r].x) * (b.x - qq[r].x) + (b.y - qq[r].y) * (b.y - qq[r].y) +
+                               (b.z - qq[r].z) * (b.z - qq[r].z) >= dd[r]) {
+                status[r] = 1;                               // reached the light's sphere
+                steps[r] = step[r] + nsub;
+                act[r] = false;
+            } else {
+                step[r] += nsub;
+                const bool out = !inside_bounds(P, b);      // kernel_impl.hpp:77-82
+                if (out || step[r] >= P.max_steps) {         // kernel_impl.hpp:87-91
+                    status[r] = PASS == kPassShadow ? 1 : 0;
+                    steps[r] = out ? step[r] : P.max_steps;
+                    act[r] = false;
+                    if constexpr (PASS == kPassHits) {
+                        RayResult res{0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
+                        emit_primary<PASS>(P, L, unit, r, res);
+                    }
+                }
+                continue;
+            }
+            step[r] += nsub;
+        }
+        p = pn;
+        v = vn;
+    }
 }
 
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
@@ -1468,6 +1747,183 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
     if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
 }
 
+
+// ---------------------------------------------------------------------------
+// Ray-pair frame kernel (Gaussian bumps, RK4, no meshes; frame and tile
+// modes).  A unit is two consecutive micro-tiles of march_kernel's order
+// (ray 0 of a thread in micro-tile 2u, ray 1 in 2u+1, same lane position),
+// so tiles remain unions of units (byte-identical frames across shard
+// counts).  L.n_units counts micro-tiles; the kernel serves (n+1)/2 units.
+// With lights the shadow pass marches light by light (lpp = 1).
+__device__ __forceinline__ void pixel_of(const DevLaunch& L, unsigned mt, int lane, bool& inrange,
+                                         bool& live, int& px, int& py, unsigned long long& pix) {
+    inrange = mt < L.n_units;
+    const unsigned m = inrange ? mt : 0u;
+    const unsigned long long tile_k = m / L.micro_per_tile;
+    const unsigned micro = m % L.micro_per_tile;
+    const unsigned tile = L.shard + (unsigned)tile_k * L.n_shards;
+    const int tx = tile % L.tiles_x, ty = tile / L.tiles_x;
+    const int mpr = L.tile_w / kMicroW;
+    const int lx = (micro % mpr) * kMicroW + (lane & 7);
+    const int ly = (micro / mpr) * kMicroH + (lane >> 3);
+    px = tx * L.tile_w + lx;
+    py = ty * L.tile_h + ly;
+    live = inrange && px < L.width && py < L.height;
+    pix = L.mode == kModeFrame ? (unsigned long long)py * L.width + px
+                               : tile_k * L.tile_w * L.tile_h + (unsigned long long)ly * L.tile_w + lx;
+}
+
+// Output of a terminated primary ray of a pair unit (pixel recomputed from
+// the unit, so no output addresses stay live through the march).
+template <int PASS>
+__device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
+                                             int r, const RayResult& res) {
+    bool inr, live;
+    int px, py;
+    unsigned long long pix;
+    pixel_of(L, 2 * unit + r, threadIdx.x & 31, inr, live, px, py, pix);
+    if constexpr (PASS == kPassHits) {
+        HitRec h;
+        h.p[0] = res.point.x;
+        h.p[1] = res.point.y;
+        h.p[2] = res.point.z;
+        h.t = res.t;
+        h.n[0] = res.normal.x;
+        h.n[1] = res.normal.y;
+        h.n[2] = res.normal.z;
+        h.status = res.status;
+        L.hits[pix] = h;
+    } else if constexpr (PASS == kPassShade) {
+        shade(P, res, L.rgb + 3 * pix);
+    }
+}
+
+template <int NB, int PASS>
+__global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL : RR_MIN_BLOCKS_X2)
+march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
+    const int lane = threadIdx.x & 31;
+    const unsigned n_pairs = (L.n_units + 1) / 2;
+    for (;;) {
+        unsigned unit = 0;
+        if (lane == 0) unit = atomicAdd(L.counter, 1u);
+        unit = __shfl_sync(kFull, unit, 0);
+        if (unit >= n_pairs) break;
+
+        bool inr[2], live[2];
+        int px[2], py[2];
+        unsigned long long pix[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
+
+        LaneCounters cnt{0u, 0u, 0u};
+        unsigned ref_steps = 0, errs = 0, shadow_steps = 0, nrays = 0;
+        if constexpr (PASS == kPassShadow) {
+            // ---- EXTENSION: shadow geodesics (oracle/rro.c shadow_march), light by light
+            HitRec hr[2];
+            F3 q[2], n[2];
+            float contrib[2] = {0.f, 0.f};
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                hr[r] = HitRec{};
+                if (live[r]) hr[r] = L.hits[pix[r]];
+                q[r] = f3(hr[r].p[0], hr[r].p[1], hr[r].p[2]);
+                n[r] = f3(hr[r].n[0], hr[r].n[1], hr[r].n[2]);
+            }
+            for (int l = 0; l < P.n_lights; ++l) {
+                const DevLight& Lt = P.lights[l];
+                bool want[2];
+                float dist2[2], lam[2];
+                F3 x0[2], v0[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const F3 D = f3(Lt.pos[0] - q[r].x, Lt.pos[1] - q[r].y, Lt.pos[2] - q[r].z);
+                    dist2[r] = D.x * D.x + D.y * D.y + D.z * D.z;
+                    lam[r] = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(dist2[r]);
+                    want[r] = live[r] && hr[r].status == 1 && lam[r] > 0.f;
+                    x0[r] = v0[r] = f3(0.f, 0.f, 0.f);
+                    if (want[r]) {
+                        x0[r] = f3(fmaf(kShadowEps, n[r].x, q[r].x), fmaf(kShadowEps, n[r].y, q[r].y),
+                                   fmaf(kShadowEps, n[r].z, q[r].z));
+                        float g[6];
+                        bool ok;
+                        metric_at(P, x0[r], g, ok);
+                        const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
+                                         2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
+                        const float inv = rsqrtf(n2);
+                        v0[r] = f3(D.x * inv, D.y * inv, D.z * inv);
+                        want[r] = ok;
+                    }
+                }
+                int sst[2], sstp[2];
+                float tdum[2];
+                F3 pdum[2];
+                march_pair<NB, kPassShadow>(P, want[0], want[1], pair_of(x0[0], x0[1]),
+                                            pair_of(v0[0], v0[1]), cnt, L, unit, sst, sstp, tdum, pdum,
+                                            q[0], q[1],
+                                            dist2[0], dist2[1]);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    if (want[r]) shadow_steps += (unsigned)sstp[r];   // reference-equivalent steps
+                    if (want[r] && sst[r] == 1) contrib[r] = fmaf(Lt.intensity, lam[r], contrib[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (live[r]) {
+                    RayResult rr{hr[r].status, 0, 0, hr[r].t, q[r], n[r]};
+                    shade(P, rr, L.rgb + 3 * pix[r], P.ambient + contrib[r]);
+                } else if (inr[r] && L.mode == kModeTiles) {
+                    uint8_t* dst = L.rgb + 3 * pix[r];
+                    dst[0] = dst[1] = dst[2] = 0;
+                }
+            }
+        } else {
+            F3 pos[2], dir[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (live[r]) raygen(L.cam, px[r], py[r], L.width, L.height, pos[r], dir[r]);
+                else pos[r] = dir[r] = f3(0.f, 0.f, 0.f);
+            }
+            int st[2], stp[2];
+            float tt[2];
+            F3 pt[2];
+            march_pair<NB, PASS>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
+                                 cnt, L, unit, st, stp, tt, pt);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (live[r]) {
+                    ref_steps += (unsigned)stp[r];
+                    errs += st[r] == 2 ? 1u : 0u;
+                    nrays += 1;
+                    if constexpr (PASS == kPassShade) {
+                        RayResult res{st[r], 0, 0, tt[r], pt[r], f3(0.f, 0.f, 0.f)};
+                        shade(P, res, L.rgb + 3 * pix[r]);
+                    }
+                } else if (inr[r] && L.mode == kModeTiles && PASS == kPassShade) {
+                    uint8_t* dst = L.rgb + 3 * pix[r];                // zero partial-tile padding
+                    dst[0] = dst[1] = dst[2] = 0;
+                }
+            }
+        }
+        const unsigned steps = __reduce_add_sync(kFull, ref_steps);
+        const unsigned nerr = __reduce_add_sync(kFull, errs);
+        const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
+        const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
+        const unsigned nr = __reduce_add_sync(kFull, nrays);
+        const unsigned shs = __reduce_add_sync(kFull, shadow_steps);
+        const unsigned slots = __reduce_add_sync(kFull, cnt.lane_slots);
+        if (lane == 0) {
+            if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
+            if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
+            if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
+            if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
+            if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
+            if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
+            if (slots) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), (unsigned long long)slots);
+        }
+    }
+    if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
+}
 
 // ---------------------------------------------------------------------------
 // Culling grid build on the device (per scene upload, e.g. every animation
@@ -1668,6 +2124,38 @@ cudaError_t launch_pass(const DevParams& P, const DevLaunch& L, cudaStream_t s, 
     return cudaGetLastError();
 }
 
+template <int NB, int PASS>
+int occupancy_of2() {
+    static int occ = [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march2_kernel<NB, PASS>, kThreads, 0);
+        return n > 0 ? n : 1;
+    }();
+    return occ;
+}
+
+template <int NB, int PASS>
+cudaError_t launch_pass2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
+    const unsigned warps_needed = (L.n_units + 1) / 2;
+    unsigned blocks = (unsigned)(num_sms * occupancy_of2<NB, PASS>());
+    const unsigned max_useful = (warps_needed + 3) / 4;
+    if (blocks > max_useful) blocks = max_useful;
+    if (blocks == 0) blocks = 1;
+    march2_kernel<NB, PASS><<<blocks, kThreads, 0, s>>>(P, L);
+    return cudaGetLastError();
+}
+
+template <int NB>
+cudaError_t launch_variant2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
+    if (P.n_lights == 0) return launch_pass2<NB, kPassShade>(P, L, s, num_sms);
+    cudaError_t e = launch_pass2<NB, kPassHits>(P, L, s, num_sms);
+    if (e != cudaSuccess) return e;
+    DevLaunch L2 = L;
+    L2.counter = L.counter + 1;
+    L2.lpp = 1;
+    return launch_pass2<NB, kPassShadow>(P, L2, s, num_sms);
+}
+
 // Without lights: one fused launch.  With lights (EXTENSION): a hit-record
 // pass and a shadow+shade pass over the same units (each with its own unit
 // counter: L.counter[0] and L.counter[1]).  Scenes with meshes use the MESH
@@ -1696,6 +2184,26 @@ cudaError_t dispatch_kind(const DevParams& P, const DevLaunch& L, cudaStream_t s
             *name = MESH ? "march_kernel<euclid,mesh>" : "march_kernel<euclid>";
             return launch_variant<kEuclid, 0, SCHEME, MESH>(P, L, s, sms);
         case kBumps:
+#if RR_RAY_PAIRS
+            if constexpr (!MESH && SCHEME == 1) {   // ray-pair frames (RK4, mesh-free)
+                if (L.mode != kModeRays) {
+                    if (P.nb_slot <= 4) {
+                        *name = "march2_kernel<bumps4>";
+                        return launch_variant2<4>(P, L, s, sms);
+                    }
+                    if (P.nb_slot <= 8) {
+                        *name = "march2_kernel<bumps8>";
+                        return launch_variant2<8>(P, L, s, sms);
+                    }
+                    if (P.nb_slot <= 16) {
+                        *name = "march2_kernel<bumps16>";
+                        return launch_variant2<16>(P, L, s, sms);
+                    }
+                    *name = "march2_kernel<bumps32>";
+                    return launch_variant2<32>(P, L, s, sms);
+                }
+            }
+#endif
             if constexpr (!MESH && SCHEME != 2) {   // mesh / rk23 scenes use 16/32 slots only
                 if (P.nb_slot <= 4) {
                     *name = "march_kernel<bumps4>";

@@ -13,12 +13,12 @@ fi
 for v in "${variants[@]}"; do
   if [ $mode = libs ]; then
     name=$(basename $v .so)
-    RRAY_CUDA_LIB=$PWD/$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ab_$name.log 2>&1
+    RRAY_CUDA_LIB=$PWD/$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ab_$name.log 2>&1
   else
     name=$(echo "$v" | tr ' =' '_-')
     optargs=""
     for o in $v; do optargs="$optargs --opt $o"; done
-    timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline $optargs > gpurun_out/ab_$name.log 2>&1
+    timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras $optargs > gpurun_out/ab_$name.log 2>&1
   fi
   python - "$name" <<'PY'
 import json, sys
