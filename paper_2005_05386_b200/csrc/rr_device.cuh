@@ -97,7 +97,8 @@ struct DevHalf {          // scene.cpp:73-81: region dot(n, p) <= off
     float n[3];
     float off;
     int index;
-    int pad[3];
+    float inv_norm;       // 1 / |n| (free-distance bound)
+    int pad[2];
 };
 
 struct DevGrid {          // scene.cpp:36-54

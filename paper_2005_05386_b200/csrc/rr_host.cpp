@@ -326,6 +326,8 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
             d.n[1] = (float)q.normal.y;
             d.n[2] = (float)q.normal.z;
             d.off = (float)q.offset;
+            d.inv_norm = (float)(1.0 / std::sqrt(q.normal.x * q.normal.x + q.normal.y * q.normal.y +
+                                                 q.normal.z * q.normal.z));
             d.index = i;
         } else {
             rr::DevGrid& d = P.grids[P.n_grids++];

@@ -727,33 +727,74 @@ __device__ __forceinline__ bool consider(bool h, float s, int idx, int id, bool&
     return false;
 }
 
+// Free-distance budget of the analytic primitives (spheres, half-spaces):
+// `sfree` is a lower bound of the distance from the current chord start to
+// every sphere and half-space region.  A chord of length len < sfree cannot
+// reach any of them (so the exact tests could only report "no hit"); the
+// budget shrinks by len per skipped chord and is recomputed at the chord end
+// after every tested chord.  Inside-start chords have sfree <= 0 and are
+// always tested.  Results are identical to testing every chord.
+__device__ __forceinline__ float analytic_free(const DevParams& P, F3 b) {
+    float fr = 3.0e38f;
+#pragma unroll
+    for (int i = 0; i < kStaticSpheres; ++i)
+        if (i < P.n_spheres) {
+            const DevSphere& sp = P.spheres[i];
+            const float ox = b.x - sp.c[0], oy = b.y - sp.c[1], oz = b.z - sp.c[2];
+            fr = fminf(fr, sqrt_approx(fmaf(ox, ox, fmaf(oy, oy, oz * oz))) - sp.r);
+        }
+    for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
+        const DevSphere& sp = P.spheres[i];
+        const float ox = b.x - sp.c[0], oy = b.y - sp.c[1], oz = b.z - sp.c[2];
+        fr = fminf(fr, sqrt_approx(fmaf(ox, ox, fmaf(oy, oy, oz * oz))) - sp.r);
+    }
+#pragma unroll
+    for (int i = 0; i < kStaticHalves; ++i)
+        if (i < P.n_halves) {
+            const DevHalf& hs = P.halves[i];
+            fr = fminf(fr, (fmaf(hs.n[0], b.x, fmaf(hs.n[1], b.y, hs.n[2] * b.z)) - hs.off) * hs.inv_norm);
+        }
+    for (int i = kStaticHalves; i < P.n_halves; ++i) {
+        const DevHalf& hs = P.halves[i];
+        fr = fminf(fr, (fmaf(hs.n[0], b.x, fmaf(hs.n[1], b.y, hs.n[2] * b.z)) - hs.off) * hs.inv_norm);
+    }
+    // rounding margin of the FP32 distances (approximate sqrt, world units)
+    return fr - fmaf(2e-6f, fabsf(fr), 1e-5f) - 1e-6f * (fabsf(b.x) + fabsf(b.y) + fabsf(b.z));
+}
+
 template <bool MESH>
 __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
-                                          int& prim, int& hid, float& mfree, int& mrec) {
+                                          int& prim, int& hid, float& mfree, int& mrec,
+                                          float& sfree) {
     const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
     const float qa = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
     const float len = fmaf(sqrt_approx(qa), 1.0001f, 1e-30f);   // conservative chord length
     bool have = false;
     float s = 0.f;
+    if (len < sfree) {
+        sfree -= len;                     // no sphere / half-space within reach
+    } else {
 #pragma unroll
-    for (int i = 0; i < kStaticSpheres; ++i)
-        if (i < P.n_spheres) {
+        for (int i = 0; i < kStaticSpheres; ++i)
+            if (i < P.n_spheres) {
+                const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
+                consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
+            }
+        for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
             const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
             consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
         }
-    for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
-        const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
-        consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
-    }
 #pragma unroll
-    for (int i = 0; i < kStaticHalves; ++i)
-        if (i < P.n_halves) {
+        for (int i = 0; i < kStaticHalves; ++i)
+            if (i < P.n_halves) {
+                const bool h = hit_half_space(P.halves[i], a, d, s);
+                consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
+            }
+        for (int i = kStaticHalves; i < P.n_halves; ++i) {
             const bool h = hit_half_space(P.halves[i], a, d, s);
             consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
         }
-    for (int i = kStaticHalves; i < P.n_halves; ++i) {
-        const bool h = hit_half_space(P.halves[i], a, d, s);
-        consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
+        if (!have) sfree = analytic_free(P, b);
     }
     for (int i = 0; i < P.n_grids; ++i) {
         const bool h = hit_grid(P.grids[i], a, b, d, s);
@@ -913,6 +954,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
     int step = 0;                             // this lane's reference step index
     const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
     float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
+    float sfree = 0.f;                        // sphere / half-space free distance budget
     for (;;) {
         if (!__any_sync(kFull, active)) break;
         cnt.lane_slots += 1;
@@ -1028,7 +1070,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
                 res.status = PASS == kPassShadow ? 0 : 2;
                 res.steps = step;
                 active = false;
-            } else if (intersect<MESH>(P, p, pn, s, prim, hid, mfree, mrec)) { // kernel_impl.hpp:63-76
+            } else if (intersect<MESH>(P, p, pn, s, prim, hid, mfree, mrec, sfree)) { // kernel_impl.hpp:63-76
                 const F3 pt = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
                                  fmaf(s, pn.z - p.z, p.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
@@ -1085,7 +1127,7 @@ __device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool li
     const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
     float h = h0, t = 0.f;
     int steps = 0, attempts = 0;
-    float mfree = 0.f;
+    float mfree = 0.f, sfree = 0.f;
     bool have_k1 = false;
     F3 k1v = f3(0.f, 0.f, 0.f);
     for (;;) {
@@ -1215,7 +1257,7 @@ __device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool li
                 res.steps = steps;
                 active = false;
             } else if (accept) {
-                if (intersect<MESH>(P, p, xn, s, prim, hid, mfree, mrec)) {
+                if (intersect<MESH>(P, p, xn, s, prim, hid, mfree, mrec, sfree)) {
                     const F3 pt = f3(fmaf(s, xn.x - p.x, p.x), fmaf(s, xn.y - p.y, p.y),
                                      fmaf(s, xn.z - p.z, p.z));
                     const int sub = min((int)(s * (float)nsub), nsub - 1);
@@ -1410,22 +1452,8 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
 // bookkeeping run per ray on the unpacked halves with exactly march_fixed's
 // rules (kernel_impl.hpp:22-94).  The warp-uniform bump mask is the OR over
 // the 64 rays of the unit.
-#ifndef RR_X2_CALLS
-#define RR_X2_CALLS 0      // 1: chord test / jump length as real calls (one code copy for both rays)
-#endif
-#if RR_X2_CALLS
-__device__ __noinline__ bool intersect_call(const DevParams& P, F3 a, F3 b, float& s, int& prim, int& hid) {
-    float mfree = 0.f;
-    int mrec = 0;
-    return intersect<false>(P, a, b, s, prim, hid, mfree, mrec);
-}
-#define RR_JUMP_INLINE __noinline__
-#else
-#define RR_JUMP_INLINE __forceinline__
-#endif
-
 template <int PASS>
-__device__ RR_JUMP_INLINE int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
+__device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
                                           float light_d) {
     const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
     const float isp = rsqrtf(speed2);
@@ -1471,6 +1499,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
     const float h = P.h;
     const F2 half = bc2(0.5f * h), full = bc2(h), sixth = bc2(h / 6.f);
     P3 c{bc2(0.f), bc2(0.f), bc2(0.f)};    // Kahan compensation of the position sums
+    float sfree[2] = {0.f, 0.f};           // sphere / half-space free distance budgets
     for (;;) {
         if (!__any_sync(kFull, act[0] || act[1])) break;
         cnt.lane_slots += 2;
@@ -1538,11 +1567,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             cnt.steps_integrated += 1;
             float s = 0.f, mfree = 0.f;
             int prim = -1, hid = 0, mrec = 0;
-#if RR_X2_CALLS
-            const bool hit = intersect_call(P, a, b, s, prim, hid);
-#else
-            const bool hit = intersect<false>(P, a, b, s, prim, hid, mfree, mrec);
-#endif
+            const bool hit = intersect<false>(P, a, b, s, prim, hid, mfree, mrec, sfree[r]);
             if (hit) {                                       // kernel_impl.hpp:63-76
                 const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
