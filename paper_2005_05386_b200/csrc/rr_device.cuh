@@ -124,7 +124,7 @@ struct DevLight {
 
 constexpr float kShadowEps = 1e-4f;   // shadow-ray origin offset along the normal
 
-struct HitRec {           // EXTENSION: primary hit for the shadow pass (32 B)
+struct alignas(16) HitRec {   // EXTENSION: primary hit for the shadow pass (32 B)
     float p[3];
     float t;
     float n[3];           // outward unit normal
@@ -146,6 +146,7 @@ struct DevParams {
     int grid;             // culling voxels per axis
     float grid_lo[3], grid_inv[3];
     uint32_t all_mask;    // bits of every live bump (slot bits for kBumps)
+    uint32_t neg_mask;    // slots with a negative amplitude (kBumps)
     const uint32_t* cull_masks;   // grid^3 bump masks (device); rk23: 3 levels
     unsigned cull_cells;          // grid^3 (level stride)
     const uint8_t* skip_k;        // grid^3 Chebyshev distance (cells) to the nearest non-empty cell
@@ -186,6 +187,9 @@ struct DevLaunch {
     unsigned* counter;            // unit dispensers [2] (zeroed per launch)
     unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays [5] shadow steps
     HitRec* hits;                 // EXTENSION: hit records (lights present)
+    unsigned* done;               // EXTENSION: lights finished per ray-pair unit (zeroed per launch)
+    uint8_t* vis;                 // EXTENSION: light visibility per (pixel, light)
+    unsigned* ready;              // EXTENSION: fused launch: hit records of a pair unit written
 };
 
 } // namespace rr

@@ -57,7 +57,7 @@ struct Options {
         std::memset(&o, 0, sizeof o);
         o.cull = 1;
         o.cull_grid = 64;            // 1 MB mask table; measured best
-        o.cull_radius_sigma = 6.0;   // parity-neutral (profiles/r1_cull_radius_sweep.log)
+        o.cull_radius_sigma = 5.5;   // near parity-neutral (profiles/r1i_cull_sweep_960.log)
         o.block_x = 32;
         o.block_y = 32;
         o.persistent = 1;
@@ -101,7 +101,10 @@ struct rr_ctx {
     std::vector<void*> d_mesh;               // EXTENSION: BVH nodes + triangles per mesh
     void* d_hits = nullptr;                  // EXTENSION: hit records of the shadow pass
     size_t hits_cap = 0;
+    void* d_vis = nullptr;                   // EXTENSION: per-pair light counters + visibility bytes
+    size_t vis_cap = 0;
     const char* last_kernel = "";
+    int last_launches = 0;
 };
 
 namespace {
@@ -254,6 +257,7 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
         b.la = (float)std::log2(std::fabs(g.a));
         b.sgn = g.a < 0.0 ? -1.f : 1.f;
         if (slot < 32) P.all_mask |= 1u << slot;
+        if (slot < 32 && g.a < 0.0) P.neg_mask |= 1u << slot;
         slots_out[j] = slot;
     }
     for (int k = 0; k < 32; ++k) {                          // broadcast pairs (ray-pair march)
@@ -373,7 +377,7 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
         return RR_OK;
     }
     const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));
-    const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 6.0;
+    const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 5.5;
     const double dil = 1.5 * h;
     if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_dilation >= dil &&
         c->masks_levels == levels) {
@@ -596,12 +600,25 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
         const int rc = ensure_device_buffer(c, &c->d_hits, &c->hits_cap, pixels * sizeof(rr::HitRec));
         if (rc) return rc;
         L.hits = reinterpret_cast<rr::HitRec*>(c->d_hits);
+        // ray-pair shadow pass, one unit per (pixel pair-unit, light): per-unit
+        // completion counters (zeroed per launch) + one visibility byte per
+        // (pixel, light); the last light of a unit to finish shades it
+        // (+ the fused launch's per-unit ready flags)
+        const size_t pairs = ((size_t)L.n_units + 1) / 2;
+        const size_t flag_bytes = (2 * pairs * sizeof(unsigned) + 255) & ~size_t(255);
+        const int rv = ensure_device_buffer(c, &c->d_vis, &c->vis_cap,
+                                            flag_bytes + pixels * (size_t)c->P->n_lights);
+        if (rv) return rv;
+        L.done = reinterpret_cast<unsigned*>(c->d_vis);
+        L.ready = L.done + pairs;
+        L.vis = reinterpret_cast<uint8_t*>(c->d_vis) + flag_bytes;
+        RR_CUDA(c, cudaMemsetAsync(c->d_vis, 0, 2 * pairs * sizeof(unsigned), s));
     }
     RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * 8, s));
     L.counter = reinterpret_cast<unsigned*>(c->d_aux);
     L.stats = reinterpret_cast<unsigned long long*>(c->d_aux + 8);
     RR_CUDA(c, cudaEventRecord(c->ev0, s));
-    RR_CUDA(c, rr::launch_march(*c->P, L, s, c->num_sms, &c->last_kernel));
+    RR_CUDA(c, rr::launch_march(*c->P, L, s, c->num_sms, &c->last_kernel, &c->last_launches));
     RR_CUDA(c, cudaEventRecord(c->ev1, s));
     return RR_OK;
 }
@@ -622,7 +639,7 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->shadow_steps = (int64_t)c->h_stats[5];
         st->lane_slots = (int64_t)c->h_stats[6];
         st->shadow_lane_slots = (int64_t)c->h_stats[7];
-        st->kernel_launches = c->P->n_lights > 0 ? 2 : 1;
+        st->kernel_launches = c->last_launches;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
         st->wall_seconds = now - wall0_s;
@@ -731,6 +748,7 @@ void rr_destroy(rr_ctx* c) {
     if (c->d_out) cudaFree(c->d_out);
     if (c->d_rgb) cudaFree(c->d_rgb);
     if (c->d_hits) cudaFree(c->d_hits);
+    if (c->d_vis) cudaFree(c->d_vis);
     for (void* p : c->d_mesh) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);

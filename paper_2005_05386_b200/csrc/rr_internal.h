@@ -14,7 +14,7 @@ namespace rr {
 // bump capacity, scheme).  L.counter / L.stats must already be zeroed on
 // `stream`.  Returns cudaSuccess or the launch error.
 cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream,
-                         int num_sms, const char** kernel_name);
+                         int num_sms, const char** kernel_name, int* launches = nullptr);
 
 // Builds the culling grid (bump masks + Chebyshev distances) on the device:
 // d_gauss holds n records {cx, cy, cz, sigma_x, sigma_y, sigma_z, slot, pad}.

@@ -44,6 +44,19 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_X2_GROUP_LOOP
 #define RR_X2_GROUP_LOOP 0
 #endif
+#ifndef RR_X2_FUSED
+// ray-pair frames with lights: 1 = one launch (primary units, then
+// (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
+#define RR_X2_FUSED 1
+#endif
+#ifndef RR_X2_BITLOOP
+// ray-pair bump block as a rolled loop over the set bits of the warp mask:
+// 0 = unrolled slot tests, 1 = one bump per iteration, 2 = two per iteration,
+// 3 = one per iteration, positive then negative amplitudes with the sign in
+// the FFMA2 operand (default: C3 + 2 lights 19.16 -> 18.56 ms, primary-only
+// frame unchanged; profiles/r1i_shadow_frame.md)
+#define RR_X2_BITLOOP 3
+#endif
 #ifndef RR_MIN_BLOCKS_X2
 // ray-pair kernel occupancy (CUDA-event A/B, profiles/r1g_raypair.md): 7 CTAs
 // (<= 72 registers, ~200 B of spills) beat 5 and 6 on C3; the 4-slot
@@ -176,6 +189,14 @@ __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
     return r;
 }
+// c - a*b as ONE FFMA2 with a negated operand (ptxas folds the pair; f32x2
+// has no neg in PTX, and an xor would cost two ALU ops)
+__device__ __forceinline__ F2 fnma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("{\n\t.reg .b64 t;\n\tmul.rn.f32x2 t, %1, %2;\n\tsub.rn.f32x2 %0, %3, t;\n\t}"
+        : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
 __device__ __forceinline__ F2 ld2(const float2& f) { return F2{*reinterpret_cast<const u64*>(&f)}; }
 // select per ray: r0 ? a.lo : b.lo, r1 ? a.hi : b.hi
 __device__ __forceinline__ F2 sel2(bool r0, bool r1, F2 a, F2 b) {
@@ -224,7 +245,69 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
         Sy = fma2(v, ld2(b.ky), Sy);
         Sz = fma2(v, ld2(b.kz), Sz);
     };
-#if RR_X2_GROUP_LOOP
+#if RR_X2_BITLOOP == 3
+    // active slots only, positive amplitudes first, then negative ones with
+    // the sign folded into the accumulating FFMA2s (negated operand): one
+    // FMUL2 less per bump and two small loop bodies instead of NB slot tests
+    auto body_s = [&](const DevBumpB& b, bool neg) {
+        const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
+        const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
+        const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
+        const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
+        const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
+        const F2 et = mul2(e, t);
+        if (neg) {
+            Gx = fnma2(e, gx, Gx);
+            Gy = fnma2(e, gy, Gy);
+            Gz = fnma2(e, gz, Gz);
+            Q1 = fnma2(et, t, Q1);
+            Sx = fnma2(e, ld2(b.kx), Sx);
+            Sy = fnma2(e, ld2(b.ky), Sy);
+            Sz = fnma2(e, ld2(b.kz), Sz);
+        } else {
+            Gx = fma2(e, gx, Gx);
+            Gy = fma2(e, gy, Gy);
+            Gz = fma2(e, gz, Gz);
+            Q1 = fma2(et, t, Q1);
+            Sx = fma2(e, ld2(b.kx), Sx);
+            Sy = fma2(e, ld2(b.ky), Sy);
+            Sz = fma2(e, ld2(b.kz), Sz);
+        }
+    };
+    uint32_t m = um & ~P.neg_mask;
+#pragma unroll 1
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1u;
+        body_s(P.bumpsb[j], false);
+    }
+    m = um & P.neg_mask;
+#pragma unroll 1
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1u;
+        body_s(P.bumpsb[j], true);
+    }
+#elif RR_X2_BITLOOP
+    // active slots only, ascending (the accumulation order of the unrolled
+    // block): one small loop body instead of NB slot tests and bodies
+    uint32_t m = um;
+#pragma unroll 1
+    while (m) {
+        const int j0 = __ffs(m) - 1;
+        m &= m - 1u;
+#if RR_X2_BITLOOP == 2
+        if (m) {
+            const int j1 = __ffs(m) - 1;
+            m &= m - 1u;
+            body(P.bumpsb[j0]);
+            body(P.bumpsb[j1]);
+            continue;
+        }
+#endif
+        body(P.bumpsb[j0]);
+    }
+#elif RR_X2_GROUP_LOOP
     // groups of 4 slots in a rolled loop (uniform-indexed constant loads):
     // a quarter of the code footprint of the unrolled block
 #pragma unroll 1
@@ -927,7 +1010,7 @@ struct LaneCounters {
     unsigned lane_slots;       // loop iterations executed by this lane (active or not)
 };
 
-enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2 };
+enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3 };
 
 // ---------------------------------------------------------------------------
 // March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
@@ -1823,128 +1906,237 @@ __device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch
     }
 }
 
+// Per-warp accounting of one work unit, flushed with one atomic per field.
+struct UnitStats {
+    LaneCounters cnt;
+    unsigned ref_steps, errs, shadow_steps, nrays;
+};
+
+__device__ __forceinline__ void flush_unit_stats(const DevLaunch& L, const UnitStats& us, int lane,
+                                                 bool shadow) {
+    const unsigned steps = __reduce_add_sync(kFull, us.ref_steps);
+    const unsigned nerr = __reduce_add_sync(kFull, us.errs);
+    const unsigned integ = __reduce_add_sync(kFull, us.cnt.steps_integrated);
+    const unsigned evals = __reduce_add_sync(kFull, us.cnt.bump_evals);
+    const unsigned nr = __reduce_add_sync(kFull, us.nrays);
+    const unsigned shs = __reduce_add_sync(kFull, us.shadow_steps);
+    const unsigned slots = __reduce_add_sync(kFull, us.cnt.lane_slots);
+    if (lane == 0) {
+        if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
+        if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
+        if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
+        if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
+        if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
+        if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
+        if (slots) atomicAdd(L.stats + (shadow ? 7 : 6), (unsigned long long)slots);
+    }
+}
+
+// Primary rays of ray-pair unit `unit` (64 pixels: micro-tiles 2 unit, 2 unit
+// + 1): raygen, march, and either the fused shading (kPassShade) or hit
+// records for the shadow work (kPassHits).
+template <int NB, int PASS>
+__device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
+                                             int lane, UnitStats& us) {
+    bool inr[2], live[2];
+    int px[2], py[2];
+    unsigned long long pix[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
+    F3 pos[2], dir[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (live[r]) raygen(L.cam, px[r], py[r], L.width, L.height, pos[r], dir[r]);
+        else pos[r] = dir[r] = f3(0.f, 0.f, 0.f);
+    }
+    int st[2], stp[2];
+    float tt[2];
+    F3 pt[2];
+    march_pair<NB, PASS>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
+                         us.cnt, L, unit, st, stp, tt, pt);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (live[r]) {
+            us.ref_steps += (unsigned)stp[r];
+            us.errs += st[r] == 2 ? 1u : 0u;
+            us.nrays += 1;
+            if constexpr (PASS == kPassShade) {
+                RayResult res{st[r], 0, 0, tt[r], pt[r], f3(0.f, 0.f, 0.f)};
+                shade(P, res, L.rgb + 3 * pix[r]);
+            }
+        } else if (inr[r] && L.mode == kModeTiles && PASS == kPassShade) {
+            uint8_t* dst = L.rgb + 3 * pix[r];                // zero partial-tile padding
+            dst[0] = dst[1] = dst[2] = 0;
+        }
+    }
+}
+
+// ---- EXTENSION: shadow geodesics (oracle/rro.c shadow_march) of ray-pair
+// unit `unit` toward light `l`.  Each (unit, light) is its own work item, so
+// the expensive shadow work is split finely across warps; the visibility
+// byte of every (pixel, light) is published and the unit's LAST light to
+// finish (per-unit counter L.done) shades its 64 pixels, summing the lit
+// contributions in light order (shade_lit in oracle/rro.c).
+template <int NB>
+__device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch& L, unsigned unit,
+                                            int l, int nl, int lane, UnitStats& us) {
+    bool inr[2], live[2];
+    int px[2], py[2];
+    unsigned long long pix[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
+    int status[2] = {0, 0};
+    float thit[2] = {0.f, 0.f};
+    F3 q[2], n[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (live[r]) {   // L2 loads: in the fused kernel the records were written by other SMs
+            const float4* hp = reinterpret_cast<const float4*>(L.hits + pix[r]);
+            a = __ldcg(hp);
+            b = __ldcg(hp + 1);
+        }
+        q[r] = f3(a.x, a.y, a.z);
+        thit[r] = a.w;
+        n[r] = f3(b.x, b.y, b.z);
+        status[r] = __float_as_int(b.w);
+    }
+    const DevLight& Lt = P.lights[l];
+    bool want[2];
+    float dist2[2];
+    F3 x0[2], v0[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const F3 D = f3(Lt.pos[0] - q[r].x, Lt.pos[1] - q[r].y, Lt.pos[2] - q[r].z);
+        dist2[r] = D.x * D.x + D.y * D.y + D.z * D.z;
+        const float lam = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(dist2[r]);
+        want[r] = live[r] && status[r] == 1 && lam > 0.f;
+        x0[r] = v0[r] = f3(0.f, 0.f, 0.f);
+        if (want[r]) {
+            x0[r] = f3(fmaf(kShadowEps, n[r].x, q[r].x), fmaf(kShadowEps, n[r].y, q[r].y),
+                       fmaf(kShadowEps, n[r].z, q[r].z));
+            float g[6];
+            bool ok;
+            metric_at(P, x0[r], g, ok);
+            const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
+                             2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
+            const float inv = rsqrtf(n2);
+            v0[r] = f3(D.x * inv, D.y * inv, D.z * inv);
+            want[r] = ok;
+        }
+    }
+    int sst[2], sstp[2];
+    float tdum[2];
+    F3 pdum[2];
+    march_pair<NB, kPassShadow>(P, want[0], want[1], pair_of(x0[0], x0[1]), pair_of(v0[0], v0[1]),
+                                us.cnt, L, unit, sst, sstp, tdum, pdum, q[0], q[1], dist2[0], dist2[1]);
+    bool vis[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (want[r]) us.shadow_steps += (unsigned)sstp[r];   // reference-equivalent steps
+        vis[r] = want[r] && sst[r] == 1;
+    }
+    bool last = true;
+    if (nl > 1) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (live[r]) L.vis[pix[r] * (unsigned)nl + l] = vis[r] ? 1 : 0;
+        __threadfence();
+        __syncwarp();
+        unsigned before = 0;
+        if (lane == 0) before = atomicAdd(L.done + unit, 1u);
+        before = __shfl_sync(kFull, before, 0);
+        last = before == (unsigned)nl - 1u;
+        if (last) __threadfence();
+    }
+    if (!last) return;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (live[r]) {
+            float contrib = 0.f;
+            if (status[r] == 1) {
+                for (int k = 0; k < nl; ++k) {
+                    const bool lit = k == l ? vis[r] : __ldcg(L.vis + pix[r] * (unsigned)nl + k) != 0;
+                    if (!lit) continue;
+                    const DevLight& Lk = P.lights[k];
+                    const F3 D = f3(Lk.pos[0] - q[r].x, Lk.pos[1] - q[r].y, Lk.pos[2] - q[r].z);
+                    const float d2 = D.x * D.x + D.y * D.y + D.z * D.z;
+                    const float lam = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(d2);
+                    contrib = fmaf(Lk.intensity, lam, contrib);
+                }
+            }
+            RayResult rr{status[r], 0, 0, thit[r], q[r], n[r]};
+            shade(P, rr, L.rgb + 3 * pix[r], P.ambient + contrib);
+        } else if (inr[r] && L.mode == kModeTiles) {
+            uint8_t* dst = L.rgb + 3 * pix[r];
+            dst[0] = dst[1] = dst[2] = 0;
+        }
+    }
+}
+
+// Ray-pair persistent kernel.  Work items are dispensed by one atomic
+// counter:
+//   kPassShade  : n_pairs primary units with fused shading (no lights);
+//   kPassHits   : n_pairs primary units writing hit records;
+//   kPassShadow : n_pairs x n_lights shadow units (after a kPassHits launch);
+//   kPassFused  : the two above in ONE launch — primary units first, then the
+//                 shadow units; a shadow unit waits (rarely: it was dispensed
+//                 n_pairs items later) for its primary unit's ready flag, so
+//                 the frame has one tail instead of two and no launch gap.
+//                 No deadlock: a flag's producer already holds a running warp
+//                 and waits on nothing.
 template <int NB, int PASS>
 __global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL : RR_MIN_BLOCKS_X2)
 march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     const unsigned n_pairs = (L.n_units + 1) / 2;
-    for (;;) {
-        unsigned unit = 0;
-        if (lane == 0) unit = atomicAdd(L.counter, 1u);
-        unit = __shfl_sync(kFull, unit, 0);
-        if (unit >= n_pairs) break;
-
-        bool inr[2], live[2];
-        int px[2], py[2];
-        unsigned long long pix[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
-
-        LaneCounters cnt{0u, 0u, 0u};
-        unsigned ref_steps = 0, errs = 0, shadow_steps = 0, nrays = 0;
-        if constexpr (PASS == kPassShadow) {
-            // ---- EXTENSION: shadow geodesics (oracle/rro.c shadow_march), light by light
-            HitRec hr[2];
-            F3 q[2], n[2];
-            float contrib[2] = {0.f, 0.f};
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                hr[r] = HitRec{};
-                if (live[r]) hr[r] = L.hits[pix[r]];
-                q[r] = f3(hr[r].p[0], hr[r].p[1], hr[r].p[2]);
-                n[r] = f3(hr[r].n[0], hr[r].n[1], hr[r].n[2]);
+    constexpr bool kShadowWork = PASS == kPassShadow || PASS == kPassFused;
+    const int nl = kShadowWork ? P.n_lights : 1;
+    const unsigned n_primary = PASS == kPassShadow ? 0u : n_pairs;
+    const unsigned n_work = n_primary + (kShadowWork ? n_pairs * (unsigned)nl : 0u);
+    auto fetch = [&]() {
+        unsigned w = 0;
+        if (lane == 0) w = atomicAdd(L.counter, 1u);
+        return __shfl_sync(kFull, w, 0);
+    };
+    // Two sequential loops (no if/else between the unit kinds inside one
+    // loop body: that made ptxas treat the bump loops as divergent and drop
+    // their uniform-datapath constant loads).  The warp whose fetch crosses
+    // n_primary carries that item into the shadow loop.
+    unsigned work = fetch();
+    if constexpr (PASS != kPassShadow) {
+        constexpr int kPrim = PASS == kPassFused ? kPassHits : PASS;
+        while (work < n_primary) {
+            UnitStats us{};
+            pair_primary<NB, kPrim>(P, L, work, lane, us);
+            if constexpr (PASS == kPassFused) {                 // publish the hit records
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicExch(L.ready + work, 1u);
             }
-            for (int l = 0; l < P.n_lights; ++l) {
-                const DevLight& Lt = P.lights[l];
-                bool want[2];
-                float dist2[2], lam[2];
-                F3 x0[2], v0[2];
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const F3 D = f3(Lt.pos[0] - q[r].x, Lt.pos[1] - q[r].y, Lt.pos[2] - q[r].z);
-                    dist2[r] = D.x * D.x + D.y * D.y + D.z * D.z;
-                    lam[r] = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(dist2[r]);
-                    want[r] = live[r] && hr[r].status == 1 && lam[r] > 0.f;
-                    x0[r] = v0[r] = f3(0.f, 0.f, 0.f);
-                    if (want[r]) {
-                        x0[r] = f3(fmaf(kShadowEps, n[r].x, q[r].x), fmaf(kShadowEps, n[r].y, q[r].y),
-                                   fmaf(kShadowEps, n[r].z, q[r].z));
-                        float g[6];
-                        bool ok;
-                        metric_at(P, x0[r], g, ok);
-                        const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
-                                         2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
-                        const float inv = rsqrtf(n2);
-                        v0[r] = f3(D.x * inv, D.y * inv, D.z * inv);
-                        want[r] = ok;
-                    }
-                }
-                int sst[2], sstp[2];
-                float tdum[2];
-                F3 pdum[2];
-                march_pair<NB, kPassShadow>(P, want[0], want[1], pair_of(x0[0], x0[1]),
-                                            pair_of(v0[0], v0[1]), cnt, L, unit, sst, sstp, tdum, pdum,
-                                            q[0], q[1],
-                                            dist2[0], dist2[1]);
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    if (want[r]) shadow_steps += (unsigned)sstp[r];   // reference-equivalent steps
-                    if (want[r] && sst[r] == 1) contrib[r] = fmaf(Lt.intensity, lam[r], contrib[r]);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (live[r]) {
-                    RayResult rr{hr[r].status, 0, 0, hr[r].t, q[r], n[r]};
-                    shade(P, rr, L.rgb + 3 * pix[r], P.ambient + contrib[r]);
-                } else if (inr[r] && L.mode == kModeTiles) {
-                    uint8_t* dst = L.rgb + 3 * pix[r];
-                    dst[0] = dst[1] = dst[2] = 0;
-                }
-            }
-        } else {
-            F3 pos[2], dir[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (live[r]) raygen(L.cam, px[r], py[r], L.width, L.height, pos[r], dir[r]);
-                else pos[r] = dir[r] = f3(0.f, 0.f, 0.f);
-            }
-            int st[2], stp[2];
-            float tt[2];
-            F3 pt[2];
-            march_pair<NB, PASS>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
-                                 cnt, L, unit, st, stp, tt, pt);
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (live[r]) {
-                    ref_steps += (unsigned)stp[r];
-                    errs += st[r] == 2 ? 1u : 0u;
-                    nrays += 1;
-                    if constexpr (PASS == kPassShade) {
-                        RayResult res{st[r], 0, 0, tt[r], pt[r], f3(0.f, 0.f, 0.f)};
-                        shade(P, res, L.rgb + 3 * pix[r]);
-                    }
-                } else if (inr[r] && L.mode == kModeTiles && PASS == kPassShade) {
-                    uint8_t* dst = L.rgb + 3 * pix[r];                // zero partial-tile padding
-                    dst[0] = dst[1] = dst[2] = 0;
-                }
-            }
+            flush_unit_stats(L, us, lane, false);
+            work = fetch();
         }
-        const unsigned steps = __reduce_add_sync(kFull, ref_steps);
-        const unsigned nerr = __reduce_add_sync(kFull, errs);
-        const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
-        const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
-        const unsigned nr = __reduce_add_sync(kFull, nrays);
-        const unsigned shs = __reduce_add_sync(kFull, shadow_steps);
-        const unsigned slots = __reduce_add_sync(kFull, cnt.lane_slots);
-        if (lane == 0) {
-            if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
-            if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
-            if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
-            if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
-            if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
-            if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
-            if (slots) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), (unsigned long long)slots);
+    }
+    if constexpr (kShadowWork) {
+        while (work < n_work) {
+            const unsigned w = work - n_primary;
+            const unsigned unit = w / (unsigned)nl;
+            if constexpr (PASS == kPassFused) {
+                // whole-warp polling of the unit's ready flag (dispensed
+                // n_pairs items after its primary unit: normally already set)
+                for (;;) {
+                    unsigned f = 0;
+                    if (lane == 0) f = atomicAdd(L.ready + unit, 0u);
+                    if (__shfl_sync(kFull, f, 0)) break;
+                    __nanosleep(256);
+                }
+                __threadfence();
+            }
+            UnitStats us{};
+            pair_shadow<NB>(P, L, unit, (int)(w % (unsigned)nl), nl, lane, us);
+            flush_unit_stats(L, us, lane, true);
+            work = fetch();
         }
     }
     if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
@@ -2173,6 +2365,9 @@ cudaError_t launch_pass2(const DevParams& P, const DevLaunch& L, cudaStream_t s,
 template <int NB>
 cudaError_t launch_variant2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
     if (P.n_lights == 0) return launch_pass2<NB, kPassShade>(P, L, s, num_sms);
+#if RR_X2_FUSED
+    return launch_pass2<NB, kPassFused>(P, L, s, num_sms);
+#endif
     cudaError_t e = launch_pass2<NB, kPassHits>(P, L, s, num_sms);
     if (e != cudaSuccess) return e;
     DevLaunch L2 = L;
@@ -2315,10 +2510,18 @@ cudaError_t launch_accel_points(const DevParams& P, const double* pos, const dou
 }
 
 cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream, int num_sms,
-                         const char** kernel_name) {
+                         const char** kernel_name, int* launches) {
     const char* dummy;
     if (!kernel_name) kernel_name = &dummy;
+    if (launches) *launches = 0;
     if (L.n_units == 0) return cudaSuccess;
+    if (launches) {
+        // with lights: hit + shadow launches, except the fused ray-pair kernel
+        const bool lit = P.n_lights > 0 && L.mode != kModeRays;
+        const bool fused = RR_RAY_PAIRS && RR_X2_FUSED && P.kind == kBumps && P.scheme == 1 &&
+                           P.n_meshes == 0;
+        *launches = lit && !fused ? 2 : 1;
+    }
     if (P.scheme == 2) return dispatch_scheme<2>(P, L, stream, num_sms, kernel_name);
     return P.scheme == 0 ? dispatch_scheme<0>(P, L, stream, num_sms, kernel_name)
                          : dispatch_scheme<1>(P, L, stream, num_sms, kernel_name);

@@ -52,7 +52,10 @@ def test_shadow_frame_parity_vs_oracle(renderer, oracle_lib, name, integ, w, h):
     rgb, st = renderer.render(cam, cfg.integrator, w, h)
     rep = compare_rgb(rgb, ref_rgb, flags)
     assert rep.ok, rep.summary()
-    assert st["kernel_launches"] == 2
+    # ray-pair Gaussian-bump RK4 frames fuse the hit and shadow work into one
+    # launch; the other kernels use a hit-record launch + a shadow launch
+    fused = cfg.integrator.scheme == "rk4" and renderer.last_kernel.startswith("march2_kernel")
+    assert st["kernel_launches"] == (1 if fused else 2)
     # shadow work is counted and close to the oracle's
     assert abs(st["shadow_steps"] - ref_st["shadow_steps"]) <= 0.02 * max(1, ref_st["shadow_steps"])
 

@@ -2,6 +2,7 @@
 # A/B timing of build/exp/librray_*.so variants on the GPU box (run under gpurun).
 cd "$(dirname "$0")/.."
 # Either A/B library variants (default) or option sets: tools/ab.sh --opts "cull_grid=32" "cull_grid=64"
+# (AB_ARGS="--opt cull_radius_sigma=5.5" adds bench options to every library run)
 if [ "$1" = "--opts" ]; then
   shift
   variants=("$@")
@@ -13,7 +14,7 @@ fi
 for v in "${variants[@]}"; do
   if [ $mode = libs ]; then
     name=$(basename $v .so)
-    RRAY_CUDA_LIB=$PWD/$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ab_$name.log 2>&1
+    RRAY_CUDA_LIB=$PWD/$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras $AB_ARGS > gpurun_out/ab_$name.log 2>&1
   else
     name=$(echo "$v" | tr ' =' '_-')
     optargs=""

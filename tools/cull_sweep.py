@@ -19,16 +19,20 @@ from paper_2005_05386_b200.render import Renderer  # noqa: E402
 w, h = int(sys.argv[1]) if len(sys.argv) > 1 else 320, int(sys.argv[2]) if len(sys.argv) > 2 else 180
 orc = Oracle()
 r = Renderer(0)
-for name in ["c3_bumps16_1080p", "c1_gauss1_512"]:
+radii = [float(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else \
+    [3.0, 4.0, 5.0, 5.5, 6.0, 6.5, 7.0, 8.0, 0.0]
+names = sys.argv[4].split(",") if len(sys.argv) > 4 else ["c3_bumps16_1080p", "c1_gauss1_512"]
+for name in names:
     cfg = load_config(os.path.join(ROOT, "configs", name + ".json"))
-    cfg.scene.lights = []
+    if "shadows" not in name:
+        cfg.scene.lights = []
     t0 = time.time()
     ref_rgb, ref_out, _, flags = orc.render(cfg, w, h, with_flags=True)
     rays = orc.primary_rays(orc.camera(cfg), w, h)
     print(f"{name} {w}x{h}: oracle {time.time() - t0:.1f}s, exempt {(flags & 5 != 0).sum()}", flush=True)
     r.set_config(cfg)
     cam = r.build_camera(cfg.camera)
-    for R in [3.0, 4.0, 5.0, 5.5, 6.0, 6.5, 7.0, 8.0, 0.0]:
+    for R in radii:
         r.set_options(cull=1 if R > 0 else 0, cull_radius_sigma=R if R > 0 else 7.0)
         rgb, st = r.render(cam, cfg.integrator, w, h)
         out = r.march(cfg.integrator, rays)
