@@ -388,6 +388,34 @@ def run_b200(args, cfg):
                             "avg_steps_per_ray": est["total_steps"] / (ew * eh),
                             "kernel": r.last_kernel}
             del ebuf
+        # BASELINE configs[4] as an animation: every frame a NEW scene (bump
+        # centres move, cli.animated_config), so each frame pays the scene
+        # upload and the device culling-grid rebuild before its render.
+        # Wall clock per frame (host upload work included), device-synchronised.
+        from paper_2005_05386_b200.cli import animated_config
+        acfg = load_config(os.path.join(ROOT, "configs", "c5_bumps16_4k.json"))
+        aw, ah = acfg.output.width, acfg.output.height
+        abuf = torch.empty((ah, aw, 3), dtype=torch.uint8, device="cuda")
+        r.set_config(acfg)
+        acam = r.build_camera(acfg.camera)
+        r.render_device(acam, acfg.integrator, aw, ah, abuf, stream=sp)
+        frames = [animated_config(acfg, k, 30.0, 2.0, 0.3) for k in range(1, 7)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        asteps = 0
+        for fc in frames:
+            r.set_config(fc)
+            ast = r.render_device(acam, fc.integrator, aw, ah, abuf, stream=sp, with_stats=True)
+            asteps += ast["total_steps"]
+        torch.cuda.synchronize()
+        ams = (time.perf_counter() - t0) * 1e3 / len(frames)
+        extras["c5_anim_4k"] = {"size": f"{aw}x{ah}", "frames": len(frames),
+                                "ms_per_frame": ams, "fps": 1e3 / ams,
+                                "steps_per_s": asteps / (ams * 1e-3 * len(frames)),
+                                "timing": "wall clock per frame: scene upload + device culling-grid "
+                                          "rebuild + render (the render's stats D2H syncs each frame)",
+                                "kernel": r.last_kernel}
+        del abuf
         r.set_config(cfg)
 
     # ---- e2e through the public API with host buffers (rank 0 only, N=1 path)

@@ -56,7 +56,7 @@ struct Options {
     Options() {
         std::memset(&o, 0, sizeof o);
         o.cull = 1;
-        o.cull_grid = 64;            // 1 MB mask table; measured best
+        o.cull_grid = 128;           // 8 MB mask table (L2-resident); profiles/r1i_shadow_frame.md
         o.cull_radius_sigma = 5.5;   // near parity-neutral (profiles/r1i_cull_sweep_960.log)
         o.block_x = 32;
         o.block_y = 32;

@@ -36,6 +36,7 @@ def cfg_of(name, **edits):
 def check(renderer, oracle_lib, cfg, w, h, opts=None):
     from oracle.parity import compare_outcomes, compare_rgb
     ref_rgb, ref_out, ref_st, flags = oracle_lib.render(cfg, w, h, with_flags=True)
+    saved = renderer.options()
     if opts:
         renderer.set_options(**opts)
     try:
@@ -46,7 +47,7 @@ def check(renderer, oracle_lib, cfg, w, h, opts=None):
         out = renderer.march(cfg.integrator, rays)
     finally:
         if opts:
-            renderer.set_options(cull=1, cull_grid=64, cull_radius_sigma=6.0, skip=1)
+            renderer.set_options(**saved)
     rep = compare_outcomes(out, ref_out, flags)
     rep = compare_rgb(rgb, ref_rgb, flags, rep)
     assert rep.ok, rep.summary() + " " + "; ".join(rep.details)
