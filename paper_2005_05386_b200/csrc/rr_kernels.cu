@@ -420,6 +420,24 @@ __device__ __forceinline__ F3 accel_graph_general(const DevParams& P, F3 p, F3 y
 // ---------------------------------------------------------------------------
 // Diffeo pull-back metric: directional jet folded innermost-first.
 __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float& valid) {
+    if (P.n_stages == 1 && P.stages[0].kind == kStageTwist) {
+        // Single twist (C4): J = [[R, b], [0, 1]] with R the rotation by z, so
+        // J^-1 q = [R^T (q_xy - q_z b); q_z] and q_z = 0 for the twist:
+        // a = -R^T (d0, d1) / det — the general fold below, specialised
+        float sn, cs;
+#if RR_FAST_SINCOS
+        __sincosf(p.z, &sn, &cs);
+#else
+        sincosf(p.z, &sn, &cs);
+#endif
+        const float j02 = -(p.x * sn) - p.y * cs, j12 = p.x * cs - p.y * sn;
+        const float d0 = -y.z * (2.f * (y.x * sn + y.y * cs) + y.z * j12);
+        const float d1 = y.z * (2.f * (y.x * cs - y.y * sn) + y.z * j02);
+        const float det = cs * cs + sn * sn;
+        valid = fminf(valid, fabsf(det));
+        const float id = -rcp_approx(det);
+        return f3(id * (cs * d0 + sn * d1), id * (cs * d1 - sn * d0), 0.f);
+    }
     float x0 = p.x, x1 = p.y, x2 = p.z;          // current point
     float w0 = y.x, w1 = y.y, w2 = y.z;          // J_inner y
     float q0 = 0.f, q1 = 0.f, q2 = 0.f;          // D^2 Phi_inner[y, y]
@@ -549,7 +567,7 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
     const float c22 = J[0] * J[4] - J[1] * J[3];
     const float d = J[0] * c00 + J[1] * c10 + J[2] * c20;
     valid = fminf(valid, fminf(vmin, fabsf(d)));
-    const float id = -1.f / d;
+    const float id = -rcp_approx(d);
     return f3(id * (c00 * q0 + c01 * q1 + c02 * q2), id * (c10 * q0 + c11 * q1 + c12 * q2),
               id * (c20 * q0 + c21 * q1 + c22 * q2));
 }
