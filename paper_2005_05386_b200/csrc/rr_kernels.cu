@@ -1137,8 +1137,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
         } else {                                             // RK4 (integrate.hpp:63-93)
             F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
             F3 ps = p, vs = v;
-#pragma unroll 1
-            for (int st = 0; st < 4; ++st) {   // one call site: the bump block is inlined once
+            auto stage = [&](int st) {
                 const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
                 const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
                 sx = f3(fmaf(wgt, vs.x, sx.x), fmaf(wgt, vs.y, sx.y), fmaf(wgt, vs.z, sx.z));
@@ -1146,6 +1145,13 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
                 const float c = st < 2 ? half : h;
                 ps = f3(fmaf(c, vs.x, p.x), fmaf(c, vs.y, p.y), fmaf(c, vs.z, p.z));
                 vs = f3(fmaf(c, a.x, v.x), fmaf(c, a.y, v.y), fmaf(c, a.z, v.z));
+            };
+            if constexpr (KIND == kDiffeo) {   // small accel: unrolled stages
+#pragma unroll
+                for (int st = 0; st < 4; ++st) stage(st);
+            } else {
+#pragma unroll 1
+                for (int st = 0; st < 4; ++st) stage(st);   // one call site: the bump block is inlined once
             }
             dp = f3(sixth * sx.x, sixth * sx.y, sixth * sx.z);
             vn = f3(fmaf(sixth, sv.x, v.x), fmaf(sixth, sv.y, v.y), fmaf(sixth, sv.z, v.z));
