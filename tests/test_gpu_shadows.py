@@ -101,3 +101,30 @@ def test_larger_frame_parity_with_shadows(renderer, oracle_lib):
     assert rep.ok, rep.summary()
     assert rep.exempt < 0.01 * w * h and rep.endpoint_max_rel < 1e-4
     print("C3 384x216 parity:", rep.summary())
+
+
+@pytest.mark.parametrize("lights", [
+    LIGHTS[:1],                                                    # nl == 1: no visibility bytes
+    LIGHTS + [{"position": [4.0, 0.0, 6.0], "intensity": 0.3},    # 5 lights: the unit's last
+              {"position": [1.0, -3.0, 2.0], "intensity": 0.2},   # finisher sums 4 published
+              {"position": [8.0, 2.0, 1.5], "intensity": 0.25}],  # visibility bytes
+    [{"position": [4.0, 0.0, -3.0], "intensity": 0.9}],            # below the floor: all blocked
+])
+def test_light_count_parity_fused_launch(renderer, oracle_lib, lights):
+    """The fused lit launch (one work item per (pixel unit, light), the unit's
+    last light to finish shades) against the oracle's shade_lit for 1, 5 and
+    an occluded light, plus byte-identity across repeated frames."""
+    from oracle.parity import compare_rgb
+    cfg = _cfg("c3_bumps16_shadows_1080p", lights=lights)
+    w, h = 160, 90
+    ref_rgb, _, ref_st, flags = oracle_lib.render(cfg, w, h, with_flags=True)
+    renderer.set_config(cfg)
+    cam = renderer.build_camera(cfg.camera)
+    rgb, st = renderer.render(cam, cfg.integrator, w, h)
+    rep = compare_rgb(rgb, ref_rgb, flags)
+    assert rep.ok, rep.summary()
+    assert st["kernel_launches"] == 1 and renderer.last_kernel.startswith("march2_kernel")
+    assert abs(st["shadow_steps"] - ref_st["shadow_steps"]) <= 0.02 * max(1, ref_st["shadow_steps"])
+    for _ in range(2):
+        again, _ = renderer.render(cam, cfg.integrator, w, h)
+        assert np.array_equal(again, rgb)
