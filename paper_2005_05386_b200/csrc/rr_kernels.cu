@@ -61,10 +61,15 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_X2_BITLOOP 3
 #endif
 #ifndef RR_MIN_BLOCKS_X2
-// ray-pair kernel occupancy (CUDA-event A/B, profiles/r1g_raypair.md): 7 CTAs
-// (<= 72 registers, ~200 B of spills) beat 5 and 6 on C3; the 4-slot
-// variant (C1) prefers 6.
-#define RR_MIN_BLOCKS_X2 7
+// ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
+// and unrolled RK4 stages, 6 CTAs (80 registers, 132 B of spills) beat 7
+// (72 registers, 208 B of spills in the per-step code) on the unlit frame,
+// 9.39 vs 9.63 ms; the fused lit launch keeps 7 (16.16 vs 16.35 ms)
+// (profiles/r1i_shadow_frame.md).  The 4-slot variant (C1) uses 6.
+#define RR_MIN_BLOCKS_X2 6
+#endif
+#ifndef RR_MIN_BLOCKS_X2_FUSED
+#define RR_MIN_BLOCKS_X2_FUSED 7
 #endif
 #ifndef RR_MIN_BLOCKS_X2_SMALL
 #define RR_MIN_BLOCKS_X2_SMALL 6
@@ -2117,7 +2122,9 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
 //                 No deadlock: a flag's producer already holds a running warp
 //                 and waits on nothing.
 template <int NB, int PASS>
-__global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL : RR_MIN_BLOCKS_X2)
+__global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
+                                               : (PASS == kPassFused ? RR_MIN_BLOCKS_X2_FUSED
+                                                                     : RR_MIN_BLOCKS_X2))
 march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     const unsigned n_pairs = (L.n_units + 1) / 2;
