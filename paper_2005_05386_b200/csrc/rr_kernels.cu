@@ -2196,7 +2196,7 @@ __global__ void cull_mask_kernel(const double* __restrict__ g, int n, int G, dou
     const double lo[3] = {lo0, lo1, lo2}, cell[3] = {c0, c1, c2};
     uint32_t m = 0;
     for (int j = 0; j < n; ++j) {
-        const double* b = g + 8 * j;   // cx, cy, cz, sx, sy, sz, slot, pad
+        const double* b = g + 8 * j;   // cx, cy, cz, sx, sy, sz, slot, R_j^2
         double u2 = 0.0;
         for (int k = 0; k < 3; ++k) {
             const double a = id[k] == 0 ? -1e30 : lo[k] + id[k] * cell[k] - dil;
@@ -2205,7 +2205,7 @@ __global__ void cull_mask_kernel(const double* __restrict__ g, int n, int G, dou
             const double u = (nr - b[k]) / b[3 + k];
             u2 += u * u;
         }
-        if (u2 < R2) m |= 1u << (int)b[6];
+        if (u2 < fmin(R2, b[7])) m |= 1u << (int)b[6];
     }
     masks[idx] = m;
 }

@@ -33,7 +33,8 @@ for name in names:
     r.set_config(cfg)
     cam = r.build_camera(cfg.camera)
     for R in radii:
-        r.set_options(cull=1 if R > 0 else 0, cull_radius_sigma=R if R > 0 else 7.0)
+        mode = int(os.environ.get("CULL_MODE", "1"))   # 1 uniform radius, 2 equal-error radii
+        r.set_options(cull=mode if R > 0 else 0, cull_radius_sigma=R if R > 0 else 7.0)
         rgb, st = r.render(cam, cfg.integrator, w, h)
         out = r.march(cfg.integrator, rays)
         rep = compare_outcomes(out, ref_out, flags)
