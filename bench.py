@@ -15,8 +15,10 @@ intersection -> shading for all 2,073,600 pixels.
   fps    = frames per second of `value`'s timing.
 
 python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Under torchrun (N>1) every rank renders a cyclic share of 32x32 tiles, the
-tiles are gathered to rank 0 with one NCCL gather and de-tiled there.
+Under torchrun (N>1) every rank renders a cyclic share of 32x32 tiles and its
+shade epilogue stores them straight into rank 0's frame (CUDA IPC over
+NVLink; one 4-byte NCCL all-reduce per frame as the completion barrier), with
+an NCCL gather + de-tile fallback.  The roofline is per GPU (rank 0's shard).
 """
 from __future__ import annotations
 
@@ -307,6 +309,7 @@ def run_b200(args, cfg):
     else:
         st = r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp,
                             with_stats=True)
+        st_local = dict(st)
         keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors", "lane_slots"]
         t = torch.tensor([st[k] for k in keys], dtype=torch.float64, device=cdev)
         dist.all_reduce(t)
@@ -316,9 +319,10 @@ def run_b200(args, cfg):
     fps = args.steps / (total_ms * 1e-3)
 
     # roofline of the march kernel (the dominant kernel): algorithmic FLOP per
-    # launch / mean launch time (launch = the single-GPU frame kernel)
+    # launch / mean launch time, per GPU (N > 1: this rank's shard and its own
+    # launch time against its own GPU's peak)
     kernel_ms = statistics.mean(times_ms)
-    flop_launch = algorithmic_flops(st, integ.scheme)
+    flop_launch = algorithmic_flops(st if world == 1 else st_local, integ.scheme)
     peak = r.fp32_peak_tflops()
     achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
     traffic = load_traffic().get(r.last_kernel)
