@@ -32,18 +32,6 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // (march2_kernel); 0: one ray per thread (march_kernel) for every scene.
 #define RR_RAY_PAIRS 1
 #endif
-#ifndef RR_X2_SLOTS
-#define RR_X2_SLOTS 1      // slots evaluated per test in the ray-pair bump block: 1, 2 or 4
-#endif
-#ifndef RR_X2_SIGNXOR
-#define RR_X2_SIGNXOR 0
-#endif
-#ifndef RR_X2_TTRICK
-#define RR_X2_TTRICK 0
-#endif
-#ifndef RR_X2_GROUP_LOOP
-#define RR_X2_GROUP_LOOP 0
-#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -51,14 +39,6 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_RK4_UNROLL
 #define RR_X2_RK4_UNROLL 1   // 4 RK4 stages unrolled (4 small bump loops): C3 10.32 -> 9.91 ms, lights 16.94 -> 16.66
-#endif
-#ifndef RR_X2_BITLOOP
-// ray-pair bump block as a rolled loop over the set bits of the warp mask:
-// 0 = unrolled slot tests, 1 = one bump per iteration, 2 = two per iteration,
-// 3 = one per iteration, positive then negative amplitudes with the sign in
-// the FFMA2 operand (default: C3 + 2 lights 19.16 -> 18.56 ms, primary-only
-// frame unchanged; profiles/r1i_shadow_frame.md)
-#define RR_X2_BITLOOP 3
 #endif
 #ifndef RR_MIN_BLOCKS_X2
 // ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
@@ -217,47 +197,17 @@ struct P3 {           // a 3-vector for a ray pair
 __device__ __forceinline__ F3 ray_of(const P3& v, int r) { return f3(get2(v.x, r), get2(v.y, r), get2(v.z, r)); }
 __device__ __forceinline__ P3 pair_of(F3 a, F3 b) { return P3{mk2(a.x, b.x), mk2(a.y, b.y), mk2(a.z, b.z)}; }
 
-// accel_bumps for a ray pair (same factored form, same slot tests on the
-// warp-uniform mask of the 64 rays).
+// accel_bumps for a ray pair (same factored form) over the warp-uniform mask
+// of the 64 rays: a uniform-datapath loop over the active slots, positive
+// amplitudes first, then negative ones with the sign folded into the
+// accumulating FFMA2s (negated operand).  Measured alternatives (unrolled
+// slot tests, pairs/groups of slots per test, the sign as an XOR, G = p.S - T,
+// compact or shared-memory slots): profiles/r1g_raypair.md, r1i_shadow_frame.md.
 template <int NB>
 __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, const P3& p, const P3& y) {
     F2 Gx = bc2(0.f), Gy = bc2(0.f), Gz = bc2(0.f), Q1 = bc2(0.f);
     F2 Sx = bc2(0.f), Sy = bc2(0.f), Sz = bc2(0.f);
-#if RR_X2_TTRICK
-    // G = sum_j v_j K_j (p - c_j) = p (.) S - T with T = sum_j v_j (K_j c_j):
-    // the G update reads one register pair instead of three
-    F2 Tx = bc2(0.f), Ty = bc2(0.f), Tz = bc2(0.f);
-#endif
-    auto body = [&](const DevBumpB& b) {
-        const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
-        const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
-        const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
-#if RR_X2_SIGNXOR
-        F2 v = mk2(ex2(lo2(q)), ex2(hi2(q)));            // sign applied as a bit flip (ALU pipe)
-        asm("xor.b64 %0, %0, %1;" : "+l"(v.v) : "l"(*reinterpret_cast<const u64*>(&b.sgnbit)));
-#else
-        const F2 v = mul2(mk2(ex2(lo2(q)), ex2(hi2(q))), ld2(b.sgn));
-#endif
-#if RR_X2_TTRICK
-        Tx = fma2(v, ld2(b.kcx), Tx);
-        Ty = fma2(v, ld2(b.kcy), Ty);
-        Tz = fma2(v, ld2(b.kcz), Tz);
-#else
-        Gx = fma2(v, gx, Gx);
-        Gy = fma2(v, gy, Gy);
-        Gz = fma2(v, gz, Gz);
-#endif
-        const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
-        Q1 = fma2(mul2(v, t), t, Q1);
-        Sx = fma2(v, ld2(b.kx), Sx);
-        Sy = fma2(v, ld2(b.ky), Sy);
-        Sz = fma2(v, ld2(b.kz), Sz);
-    };
-#if RR_X2_BITLOOP == 3
-    // active slots only, positive amplitudes first, then negative ones with
-    // the sign folded into the accumulating FFMA2s (negated operand): one
-    // FMUL2 less per bump and two small loop bodies instead of NB slot tests
-    auto body_s = [&](const DevBumpB& b, bool neg) {
+    auto body = [&](const DevBumpB& b, bool neg) {
         const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
         const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
         const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
@@ -287,77 +237,15 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
     while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1u;
-        body_s(P.bumpsb[j], false);
+        body(P.bumpsb[j], false);
     }
     m = um & P.neg_mask;
 #pragma unroll 1
     while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1u;
-        body_s(P.bumpsb[j], true);
+        body(P.bumpsb[j], true);
     }
-#elif RR_X2_BITLOOP
-    // active slots only, ascending (the accumulation order of the unrolled
-    // block): one small loop body instead of NB slot tests and bodies
-    uint32_t m = um;
-#pragma unroll 1
-    while (m) {
-        const int j0 = __ffs(m) - 1;
-        m &= m - 1u;
-#if RR_X2_BITLOOP == 2
-        if (m) {
-            const int j1 = __ffs(m) - 1;
-            m &= m - 1u;
-            body(P.bumpsb[j0]);
-            body(P.bumpsb[j1]);
-            continue;
-        }
-#endif
-        body(P.bumpsb[j0]);
-    }
-#elif RR_X2_GROUP_LOOP
-    // groups of 4 slots in a rolled loop (uniform-indexed constant loads):
-    // a quarter of the code footprint of the unrolled block
-#pragma unroll 1
-    for (int g = 0; g < NB; g += 4) {
-        const uint32_t gm = (um >> g) & 0xFu;
-        if (!gm) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (gm & (1u << j)) body(P.bumpsb[g + j]);
-    }
-#else
-#pragma unroll
-    for (int g = 0; g < NB; g += 4) {
-#if RR_GROUP_TESTS
-        if (!((um >> g) & 0xFu)) continue;
-#endif
-#if RR_X2_SLOTS == 2
-        // slot pairs: both slots of a pair with a bit in um (independent
-        // bodies in one block, so their dependency chains interleave)
-#pragma unroll
-        for (int j = g; j < g + 4; j += 2)
-            if ((um >> j) & 3u) {
-                body(P.bumpsb[j]);
-                body(P.bumpsb[j + 1]);
-            }
-#elif RR_X2_SLOTS == 4
-        body(P.bumpsb[g]);                     // whole group of 4
-        body(P.bumpsb[g + 1]);
-        body(P.bumpsb[g + 2]);
-        body(P.bumpsb[g + 3]);
-#else
-#pragma unroll
-        for (int j = g; j < g + 4; ++j)
-            if (um & (1u << j)) body(P.bumpsb[j]);
-#endif
-    }
-#endif
-#if RR_X2_TTRICK
-    Gx = fma2(p.x, Sx, mul2(bc2(-1.f), Tx));
-    Gy = fma2(p.y, Sy, mul2(bc2(-1.f), Ty));
-    Gz = fma2(p.z, Sz, mul2(bc2(-1.f), Tz));
-#endif
     const F2 ys = fma2(mul2(y.x, y.x), Sx, fma2(mul2(y.y, y.y), Sy, mul2(mul2(y.z, y.z), Sz)));
     const F2 Q = fma2(bc2(kBeta * kBeta), Q1, mul2(bc2(-kBeta), ys));
     const F2 w = fma2(bc2(kBeta * kBeta), fma2(Gx, Gx, fma2(Gy, Gy, mul2(Gz, Gz))), bc2(1.f));
