@@ -316,20 +316,13 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
     if (P.n_stages == 1 && P.stages[0].kind == kStageTwist) {
         // Single twist (C4): J = [[R, b], [0, 1]] with R the rotation by z, so
         // J^-1 q = [R^T (q_xy - q_z b); q_z] and q_z = 0 for the twist:
-        // a = -R^T (d0, d1) / det — the general fold below, specialised
-        float sn, cs;
-#if RR_FAST_SINCOS
-        __sincosf(p.z, &sn, &cs);
-#else
-        sincosf(p.z, &sn, &cs);
-#endif
-        const float j02 = -(p.x * sn) - p.y * cs, j12 = p.x * cs - p.y * sn;
-        const float d0 = -y.z * (2.f * (y.x * sn + y.y * cs) + y.z * j12);
-        const float d1 = y.z * (2.f * (y.x * cs - y.y * sn) + y.z * j02);
-        const float det = cs * cs + sn * sn;
-        valid = fminf(valid, fabsf(det));
-        const float id = -rcp_approx(det);
-        return f3(id * (cs * d0 + sn * d1), id * (cs * d1 - sn * d0), 0.f);
+        // a = -R^T (d0, d1) / det — the general fold below, specialised.
+        // Expanding R^T (d0, d1) with cs^2 + sn^2 = det = 1 (diffeo.hpp:165-171)
+        // the rotation cancels: a = (z'(2y' + z'x), z'(z'y - 2x'), 0), the
+        // rotating-frame Coriolis + centrifugal terms.  No sincos, no
+        // reciprocal; |det J| = 1 so the validity bound is unchanged.
+        valid = fminf(valid, 1.f);
+        return f3(y.z * fmaf(y.z, p.x, 2.f * y.y), y.z * fmaf(y.z, p.y, -2.f * y.x), 0.f);
     }
     float x0 = p.x, x1 = p.y, x2 = p.z;          // current point
     float w0 = y.x, w1 = y.y, w2 = y.z;          // J_inner y
