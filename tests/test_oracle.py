@@ -74,6 +74,24 @@ def test_accel_known_answers(oracle_lib, metric, pos, vel, want):
     assert val == 1.0
 
 
+def test_single_twist_closed_form_matches_oracle(oracle_lib):
+    """The GPU's single-twist fast path (csrc/rr_kernels.cu accel_diffeo)
+    uses a = (z'(2y' + z'x), z'(z'y - 2x'), 0): -J^-1 D^2phi[v, v] of the
+    twist (diffeo.hpp:143-173) with the rotation cancelled.  Pin the identity
+    against the oracle's general FP64 jet fold at random states."""
+    from paper_2005_05386_b200.config import parse_config
+    import json
+    cfg = parse_config(json.dumps({"metric": {"kind": "diffeo", "map": {"kind": "twist"}}}))
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        p = rng.uniform(-10, 10, 3)
+        v = rng.normal(size=3)
+        acc, val = oracle_lib.flow_accel(cfg, p, v)
+        want = [v[2] * (v[2] * p[0] + 2 * v[1]), v[2] * (v[2] * p[1] - 2 * v[0]), 0.0]
+        assert np.allclose(acc, want, rtol=1e-12, atol=1e-12)
+        assert val > 1e-14
+
+
 def test_euler_step_known_answer(oracle_lib):
     """test_geodesics.cpp:57-65"""
     from paper_2005_05386_b200.config import parse_config
