@@ -661,6 +661,12 @@ __device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
 
 // Distance from p to the nearest leaf box (capped): no triangle lies closer.
 // Nearest-child-first descent so the bound tightens early.
+#ifndef RR_TWIST_RK4
+#define RR_TWIST_RK4 1     // z-free RK4 for a single-twist metric (march_fixed)
+#endif
+#ifndef RR_MESH_FREE_CAP
+#define RR_MESH_FREE_CAP 2.f
+#endif
 __device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
     float best2 = cap * cap;
     int stack[48];
@@ -801,7 +807,7 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
                     mrec = rec;
             }
             float fr = 3.0e38f;
-            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, 2.f));
+            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, RR_MESH_FREE_CAP));
             mfree = fr;
         }
     }
@@ -945,6 +951,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
     const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
     float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
     float sfree = 0.f;                        // sphere / half-space free distance budget
+    const bool twist1 = KIND == kDiffeo && P.n_stages == 1 && P.stages[0].kind == kStageTwist;
     for (;;) {
         if (!__any_sync(kFull, active)) break;
         cnt.lane_slots += 1;
@@ -1020,6 +1027,26 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
             const F3 a = accel<KIND, NB>(P, um, p, v, valid);
             dp = f3(h * v.x, h * v.y, h * v.z);
             vn = f3(fmaf(h, a.x, v.x), fmaf(h, a.y, v.y), fmaf(h, a.z, v.z));
+        } else if (KIND == kDiffeo && RR_TWIST_RK4 && twist1) {
+            // RK4 of the single twist (integrate.hpp:63-93 with accel_diffeo's
+            // closed form): a_z = 0 and a does not depend on z, so z' stays
+            // constant, the stage points need no z and dz = h z'.
+            float sxx = 0.f, sxy = 0.f, svx = 0.f, svy = 0.f;
+            float px = p.x, py = p.y, vx = v.x, vy = v.y;
+            const float vz = v.z;
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                const float ax = vz * fmaf(vz, px, 2.f * vy), ay = vz * fmaf(vz, py, -2.f * vx);
+                const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
+                sxx = fmaf(wgt, vx, sxx); sxy = fmaf(wgt, vy, sxy);
+                svx = fmaf(wgt, ax, svx); svy = fmaf(wgt, ay, svy);
+                const float c = st < 2 ? half : h;
+                px = fmaf(c, vx, p.x); py = fmaf(c, vy, p.y);
+                vx = fmaf(c, ax, v.x); vy = fmaf(c, ay, v.y);
+            }
+            valid = 1.f;
+            dp = f3(sixth * sxx, sixth * sxy, h * vz);
+            vn = f3(fmaf(sixth, svx, v.x), fmaf(sixth, svy, v.y), vz);
         } else {                                             // RK4 (integrate.hpp:63-93)
             F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
             F3 ps = p, vs = v;
