@@ -2120,23 +2120,26 @@ __global__ void cull_mask_kernel(const double* __restrict__ g, int n, int G, dou
 
 // One separable pass of the Chebyshev (L-inf) distance transform along axis
 // `ax`: out(x) = min_y max(|x - y|, in(y)) over the grid line through x.
-// Pass 0 reads the masks (0 where non-empty, infinity elsewhere).
+// Pass 0 reads the masks (0 where non-empty, infinity elsewhere).  One CTA
+// per grid line: the line is staged in shared memory once and every thread
+// scans it for its own x (an O(G) scan per cell, no global re-reads; the
+// first build read each line G times from global memory, 0.6 ms per pass at
+// G = 128).
 __global__ void cheb_pass_kernel(const uint32_t* __restrict__ masks, const uint16_t* __restrict__ in,
                                  uint16_t* __restrict__ out, uint8_t* __restrict__ out8, int G, int ax) {
-    const int line = blockIdx.x * blockDim.x + threadIdx.x;
-    if (line >= G * G) return;
+    extern __shared__ int line_v[];
+    const int line = blockIdx.x;
     const int a = line % G, b = line / G;
     int stride, base;
     if (ax == 0) { stride = 1; base = (b * G + a) * G; }
     else if (ax == 1) { stride = G; base = b * G * G + a; }
     else { stride = G * G; base = b * G + a; }
-    for (int x = 0; x < G; ++x) {
-        int best = 0x7fff;
-        for (int y = 0; y < G; ++y) {
-            const int v = masks ? (masks[base + y * stride] ? 0 : 0x7fff) : in[base + y * stride];
-            const int d = max(abs(x - y), v);
-            best = min(best, d);
-        }
+    for (int y = threadIdx.x; y < G; y += blockDim.x)
+        line_v[y] = masks ? (masks[base + y * stride] ? 0 : 0x7fff) : in[base + y * stride];
+    __syncthreads();
+    for (int x = threadIdx.x; x < G; x += blockDim.x) {
+        int best = line_v[x];
+        for (int y = 0; y < G; ++y) best = min(best, max(abs(x - y), line_v[y]));
         if (out8) out8[base + x * stride] = (uint8_t)min(best, 255);
         else out[base + x * stride] = (uint16_t)best;
     }
@@ -2480,9 +2483,9 @@ cudaError_t launch_cull_build(const double* d_gauss, int n, int G, const double 
     cull_mask_kernel<<<(cells + 255) / 256, 256, 0, s>>>(d_gauss, n, G, lo[0], lo[1], lo[2], cell[0],
                                                           cell[1], cell[2], R * R, dil, masks);
     const int lines = G * G;
-    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(masks, nullptr, scratch, nullptr, G, 0);
-    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(nullptr, scratch, scratch + cells, nullptr, G, 1);
-    cheb_pass_kernel<<<(lines + 127) / 128, 128, 0, s>>>(nullptr, scratch + cells, nullptr, skip, G, 2);
+    cheb_pass_kernel<<<lines, 128, G * sizeof(int), s>>>(masks, nullptr, scratch, nullptr, G, 0);
+    cheb_pass_kernel<<<lines, 128, G * sizeof(int), s>>>(nullptr, scratch, scratch + cells, nullptr, G, 1);
+    cheb_pass_kernel<<<lines, 128, G * sizeof(int), s>>>(nullptr, scratch + cells, nullptr, skip, G, 2);
     return cudaGetLastError();
 }
 
