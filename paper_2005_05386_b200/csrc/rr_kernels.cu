@@ -661,6 +661,10 @@ __device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
 
 // Distance from p to the nearest leaf box (capped): no triangle lies closer.
 // Nearest-child-first descent so the bound tightens early.
+#ifndef RR_DIFFEO_RK4_UNROLL
+#define RR_DIFFEO_RK4_UNROLL 0   // general diffeo chains: 1 = RK4 stages unrolled (4 copies of the fold);
+                                 // rolled is faster (I-cache: bend 58.0 -> 50.5 ms, profiles/r1k_unroll_ab.log)
+#endif
 #ifndef RR_TWIST_RK4
 #define RR_TWIST_RK4 1     // z-free RK4 for a single-twist metric (march_fixed)
 #endif
@@ -1059,7 +1063,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
                 ps = f3(fmaf(c, vs.x, p.x), fmaf(c, vs.y, p.y), fmaf(c, vs.z, p.z));
                 vs = f3(fmaf(c, a.x, v.x), fmaf(c, a.y, v.y), fmaf(c, a.z, v.z));
             };
-            if constexpr (KIND == kDiffeo) {   // small accel: unrolled stages
+            if constexpr (KIND == kDiffeo && RR_DIFFEO_RK4_UNROLL) {   // unrolled stages
 #pragma unroll
                 for (int st = 0; st < 4; ++st) stage(st);
             } else {
