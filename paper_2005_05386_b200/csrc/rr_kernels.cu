@@ -60,6 +60,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_MIN_BLOCKS
 #define RR_MIN_BLOCKS 7   // <= 72 registers: 7 CTAs = 28 warps per SM (measured best)
 #endif
+#ifndef RR_MIN_BLOCKS_MESH
+// mesh variants (BVH stack + free-distance ball): 6 CTAs, C4 twist + mesh
+// 12.85 vs 13.2-13.4 ms at 7, 13.1-13.2 at 5, 14.4-14.7 at 8; bend neutral
+// (profiles/r1k_minblocks_ab.log)
+#define RR_MIN_BLOCKS_MESH 6
+#endif
 
 struct F3 {
     float x, y, z;
@@ -1647,7 +1653,8 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
 }
 
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23 : RR_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23
+                                         : (MESH ? RR_MIN_BLOCKS_MESH : RR_MIN_BLOCKS))
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     for (;;) {
