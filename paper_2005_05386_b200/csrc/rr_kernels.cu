@@ -675,7 +675,8 @@ __device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
 #define RR_TWIST_RK4 1     // z-free RK4 for a single-twist metric (march_fixed)
 #endif
 #ifndef RR_MESH_FREE_CAP
-#define RR_MESH_FREE_CAP 0.5f   // measured: C4 twist 0.25: 13.76, 0.5: 13.91, 1: 14.8, 2: 15.4 ms; twist+bend 60.0 / 58.1 / 57.1 / 56.4 ms
+#define RR_MESH_FREE_CAP 0.5f   // re-measured with rolled diffeo stages + 6 CTAs/SM (profiles/r1k_freecap_ab.log):
+                                // caps 0.25 / 0.5 / 1 / 2: C4 twist 13.0 / 12.8 / 13.3 / 14.2 ms, twist+bend 50.7 / 50.5 / 51.1 / 51.5 ms
 #endif
 __device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
     float best2 = cap * cap;
