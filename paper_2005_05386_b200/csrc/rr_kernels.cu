@@ -63,7 +63,8 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_MIN_BLOCKS_MESH
 // mesh variants (BVH stack + free-distance ball): 6 CTAs, C4 twist + mesh
 // 12.85 vs 13.2-13.4 ms at 7, 13.1-13.2 at 5, 14.4-14.7 at 8; bend neutral
-// (profiles/r1k_minblocks_ab.log)
+// (profiles/r1k_minblocks_ab.log); the mesh-free twist stays at 7 (8.09 vs
+// 8.32 ms at 6, profiles/r1l_minblocks_nomesh_ab.log)
 #define RR_MIN_BLOCKS_MESH 6
 #endif
 
