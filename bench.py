@@ -57,6 +57,8 @@ def parse_args():
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-shadows", action="store_true")
+    p.add_argument("--no-parity", action="store_true",
+                   help="skip the untimed full-frame parity checks against the reference / oracle")
     p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                    help="gloo: host-synchronised collectives (dry runs of the N>1 path on fewer GPUs)")
     p.add_argument("--no-extras", action="store_true",
@@ -181,11 +183,169 @@ def run_reference(args, cfg):
 
 # ---- own arm ----------------------------------------------------------------------
 def algorithmic_flops(stats, scheme):
+    """SURVEY App. A per integrated step: RK4 combination + 4 fixed accel
+    terms + 36 per evaluated bump, and the chord test.  A straight jump
+    through metric-free space (jump_steps) is charged its chord test only:
+    no RK4 or metric work runs for it."""
     evals_per_step = 4 if scheme == "rk4" else 1
     comb = FLOP_RK4 if scheme == "rk4" else 12
     steps = stats["integrated_steps"]
-    return (stats["bump_evals"] * FLOP_BUMP + steps * evals_per_step * FLOP_ACCEL +
-            steps * (comb + FLOP_ISECT))
+    rk = steps - stats.get("jump_steps", 0) - stats.get("shadow_jump_steps", 0)
+    return (stats["bump_evals"] * FLOP_BUMP + rk * (evals_per_step * FLOP_ACCEL + comb) +
+            steps * FLOP_ISECT)
+
+
+def simt(stats):
+    """Lane efficiency of the persistent warp loop: integrated ray-steps per
+    lane slot (32 x warp loop iterations), per pass."""
+    out = {}
+    prim = stats["integrated_steps"] - stats["shadow_integrated_steps"]
+    if stats["lane_slots"]:
+        out["primary"] = prim / stats["lane_slots"]
+    if stats["shadow_lane_slots"]:
+        out["shadow"] = stats["shadow_integrated_steps"] / stats["shadow_lane_slots"]
+    return out
+
+
+def rk4_steps(st):
+    """Integrated steps that ran the integrator (straight jumps excluded)."""
+    return st["integrated_steps"] - st["jump_steps"] - st["shadow_jump_steps"]
+
+
+def spill_report():
+    """ptxas -v registers / spill bytes of the dominant kernels
+    (paper_2005_05386_b200/csrc/ptxas.log, written by the build)."""
+    import re
+    path = os.path.join(ROOT, "paper_2005_05386_b200", "csrc", "ptxas.log")
+    want = {"march2_kernel<16,shade>": "march2_kernelILi16ELi0EE",
+            "march2_kernel<16,fused_lit>": "march2_kernelILi16ELi3EE",
+            "march_kernel<diffeo,rk4,mesh>": "march_kernelILi3ELi0ELi1ELi0ELb1EE"}
+    out = {}
+    try:
+        lines = open(path).read().split("\n")
+    except OSError:
+        return None
+    cur = None
+    for i, ln in enumerate(lines):
+        m = re.search(r"Compiling entry function '(\S+)'", ln)
+        if m:
+            cur = m.group(1)
+            continue
+        for label, key in want.items():
+            if cur and key in cur and "Used" in ln and "registers" in ln:
+                regs = int(re.search(r"Used (\d+) registers", ln).group(1))
+                sp = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", lines[i - 1])
+                out[label] = {"registers": regs, "spill_stores": int(sp.group(1)) if sp else 0,
+                              "spill_loads": int(sp.group(2)) if sp else 0}
+    return out
+
+
+def e2e_frames(r, cfg, w, h, n, steps_of):
+    """The metric end to end through the public host API: per frame the scene
+    upload (unchanged scene: parameter-block compare, no re-upload), camera
+    build and rr_render into PINNED host memory (the kernel's 16-B stores
+    travel straight into it), stats read back."""
+    import torch
+    host = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
+    r.set_config(cfg)
+    r.render(r.build_camera(cfg.camera), cfg.integrator, w, h, out=host)   # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        r.set_config(cfg)                              # scene upload (params + cull grid)
+        cam_e = r.build_camera(cfg.camera)
+        _, est = r.render(cam_e, cfg.integrator, w, h, out=host)  # frame -> pinned host + stats
+    e2e_s = (time.perf_counter() - t0) / n
+    # per frame host->device: the kernel parameter blocks (scene program +
+    # camera); device->host: the frame + the stats block
+    info = r.lib.rr_build_info().decode()
+    param_bytes = int(info.split("param_bytes=")[1].split()[0]) if "param_bytes=" in info else 0
+    return {"value": steps_of(est) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": param_bytes,
+            "d2h_bytes_per_step": 3 * w * h + 8 * 11, "fps": 1.0 / e2e_s,
+            "output": "kernel stores into pinned host memory (UVA)"}
+
+
+def cpu_sample(kind, cfg, w, h, target_s=4.0, kernel="avx2", workers=0):
+    """A bounded CPU sample of a workload (~target_s of host time): every k-th
+    row of the same frame, k calibrated on a sparse pass.  kind "reference":
+    the reference's own render() row work item (oracle/_ref); kind "oracle":
+    the FP64 oracle extension (oracle/rro.c) for paths the reference lacks
+    (shadow geodesics, meshes, rk23).  steps/s counts reference-equivalent
+    steps (primary + shadow)."""
+    try:
+        from oracle import Oracle, Reference
+        if kind == "reference":
+            lib = Reference()
+
+            def run(step):
+                _, st = lib.render_rows(cfg, w, h, 0, step, kernel=kernel, workers=workers)
+                return st["wall_seconds"], st["total_steps"], st["workers"]
+        else:
+            lib = Oracle()
+
+            def run(step):
+                _, _, st = lib.render_rows(cfg, w, h, 0, step, threads=workers)
+                return st["wall_seconds"], st["total_steps"] + st["shadow_steps"], workers or lib.threads
+        step0 = max(1, h // 64)
+        wall, _, _ = run(step0)
+        per_row = wall / len(range(0, h, step0))
+        step = max(1, min(h, math.ceil(h * per_row / target_s)))
+        wall, steps, cores = run(step)
+        rows = len(range(0, h, step))
+        label = (f"reference render() row work items, KernelKind::{kernel.capitalize()}"
+                 if kind == "reference" else
+                 "FP64 oracle extension (oracle/rro.c; the reference has no counterpart)")
+        return {"value": steps / wall, "unit": UNIT, "cores": cores,
+                "kind": "reference" if kind == "reference" else "port",
+                "sample": f"every {step}th row ({rows} of {h} rows, {rows * w} rays) of the same "
+                          f"frame, {label}, {cores} threads",
+                "fps_extrapolated": (rows / h) / wall, "wall_s": wall}
+    except Exception as e:   # checker build absent on this box
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": kind, "sample": f"unavailable: {e}"}
+
+
+def frame_parity(r, cfg, w, h, kind, row_step=1):
+    """Untimed per-pixel parity of the benchmarked frame: the production frame
+    kernel with its PixelOutcome sink (rr_render_outcomes) against the
+    reference's own MarchFn (kind "reference", AVX2, all host threads) or the
+    FP64 oracle (kind "oracle": the shadow extension), every row_step-th row;
+    flags (GRAZING / LIMIT / SHADOW exemptions) computed by the oracle for the
+    differing pixels (oracle.parity.check_frame)."""
+    t0 = time.perf_counter()
+    try:
+        import numpy as np
+        from oracle import Oracle, Reference
+        from oracle.parity import check_frame
+        r.set_config(cfg)
+        cam = r.build_camera(cfg.camera)
+        rgb, out, _ = r.render_outcomes(cam, cfg.integrator, w, h)
+        kern = r.last_kernel
+        orc = Oracle()
+        if kind == "reference":
+            ref_rgb, ref_out, _ = Reference().render_rows(cfg, w, h, 0, row_step, kernel="avx2",
+                                                          with_outcomes=True)
+        else:
+            ref_rgb, ref_out, _ = orc.render_rows(cfg, w, h, 0, row_step)
+        rows = np.arange(0, h, row_step)
+        g_out = out.reshape(h, w)[::row_step].reshape(-1)
+        g_rgb = rgb[::row_step]
+
+        def flag_fn(idx):
+            pix = rows[idx // w].astype(np.int64) * w + idx % w
+            return orc.flags_pixels(cfg, w, h, pix, ref_out[idx])
+
+        rep, _, cand = check_frame(g_out, ref_out, g_rgb, ref_rgb, flag_fn)
+        return {"ok": rep.ok, "pixels": rep.n, "rows": f"every {row_step} of {h}",
+                "against": ("reference MarchFn (oracle/_ref, KernelKind::Avx2)" if kind == "reference"
+                            else "FP64 oracle extension (oracle/rro.c)"),
+                "kernel": kern + " + PixelOutcome sink",
+                "status_mm": rep.status_mismatch, "prim_mm": rep.prim_mismatch,
+                "endpoint_max": rep.endpoint_max_rel, "endpoint_p99": rep.endpoint_p99_rel,
+                "endpoint_fail": rep.endpoint_fail, "rgb_max": rep.rgb_max, "rgb_fail": rep.rgb_fail,
+                "magenta": [rep.magenta_gpu, rep.magenta_ref], "exempt": rep.exempt,
+                "flagged_candidates": cand, "host_s": time.perf_counter() - t0}
+    except Exception as e:
+        return {"ok": None, "unavailable": f"{type(e).__name__}: {e}"}
 
 
 def load_traffic():
@@ -227,6 +387,22 @@ def run_b200(args, cfg):
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def device_time(fn, n, warm):
+        """CUDA-event times (ms) of n calls of fn on the bench stream, L2
+        flushed (untimed) before each."""
+        for _ in range(warm):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(n)]
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
 
     frame = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
     exchange = None
@@ -310,7 +486,8 @@ def run_b200(args, cfg):
         st = r.render_tiles(cam, integ, w, h, TILE, TILE, rank, world, tiles, stream=sp,
                             with_stats=True)
         st_local = dict(st)
-        keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors", "lane_slots"]
+        keys = ["total_steps", "integrated_steps", "bump_evals", "pixel_errors", "lane_slots",
+                "jump_steps", "shadow_jump_steps", "shadow_integrated_steps", "shadow_lane_slots"]
         t = torch.tensor([st[k] for k in keys], dtype=torch.float64, device=cdev)
         dist.all_reduce(t)
         st.update({k: int(v) for k, v in zip(keys, t.tolist())})
@@ -327,70 +504,82 @@ def run_b200(args, cfg):
     achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
     traffic = load_traffic().get(r.last_kernel)
 
-    # ---- EXTENSION: the same frame with shadow geodesics to 2 point lights
-    #      (BASELINE configs[2] headline target), device-timed the same way
+    # ---- EXTENSION: the north-star frame — the same 1080p frame with shadow
+    #      geodesics to 2 point lights (BASELINE configs[2] as specified), one
+    #      fused launch, device-timed the same way, with its own roofline,
+    #      e2e, CPU baseline (FP64 oracle extension) and parity
     shadows = None
-    if world == 1 and not args.no_shadows:
+    single = world == 1
+    if single and not args.no_shadows:
         from paper_2005_05386_b200.config import load_config
         scfg = load_config(SHADOW_CONFIG)
         r.set_config(scfg)
         scam = r.build_camera(scfg.camera)
-        for _ in range(max(2, args.warmup)):
-            r.render_device(scam, scfg.integrator, w, h, frame, stream=sp)
-        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.zero_()
-            sev[i][0].record(stream)
-            r.render_device(scam, scfg.integrator, w, h, frame, stream=sp)
-            sev[i][1].record(stream)
-        torch.cuda.synchronize()
-        sms = [a.elapsed_time(b) for a, b in sev]
+        sms = device_time(lambda: r.render_device(scam, scfg.integrator, w, h, frame, stream=sp),
+                          args.steps, max(2, args.warmup))
         sst = r.render_device(scam, scfg.integrator, w, h, frame, stream=sp, with_stats=True)
+        s_ms = statistics.mean(sms)
+        s_flop = algorithmic_flops(sst, integ.scheme)
+        s_ach = s_flop / (s_ms * 1e-3) / 1e12
         shadows = {"workload": "c3_bumps16_shadows_1080p", "lights": len(scfg.scene.lights),
-                   "ms_per_frame": statistics.mean(sms), "fps": 1e3 / statistics.mean(sms),
+                   "ms_per_frame": s_ms, "fps": 1e3 / s_ms,
                    "primary_steps": sst["total_steps"], "shadow_steps": sst["shadow_steps"],
                    "integrated_steps": sst["integrated_steps"],
-                   "steps_per_s": (sst["total_steps"] + sst["shadow_steps"]) /
-                                  (statistics.mean(sms) * 1e-3),
-                   "achieved_tflops": algorithmic_flops(sst, integ.scheme) /
-                                      (statistics.mean(sms) * 1e-3) / 1e12,
-                   "simt_efficiency_shadow": (sst["integrated_steps"] - st["integrated_steps"]) /
-                                             max(1, sst["shadow_lane_slots"]),
-                   "launches_per_frame": sst["kernel_launches"]}
+                   "steps_per_s": (sst["total_steps"] + sst["shadow_steps"]) / (s_ms * 1e-3),
+                   "rk4_steps_per_s": rk4_steps(sst) / (s_ms * 1e-3),
+                   "roofline": {"bound": "fp32", "achieved": s_ach, "peak": peak, "unit": "TFLOP/s",
+                                "frac": s_ach / peak, "frac_nominal": s_ach / NOMINAL_FP32_TFLOPS,
+                                "traffic": load_traffic().get(r.last_kernel + "+lights"),
+                                "flop_per_launch": s_flop, "kernel": r.last_kernel + " (fused lit)"},
+                   "simt_efficiency": simt(sst),
+                   "launches_per_frame": sst["kernel_launches"],
+                   "e2e": e2e_frames(r, scfg, w, h, max(3, args.steps),
+                                     lambda st: st["total_steps"] + st["shadow_steps"])}
+        if not args.no_cpu_baseline:
+            shadows["cpu_baseline"] = cpu_sample("oracle", scfg, w, h)
+        if not args.no_parity:
+            shadows["parity"] = frame_parity(r, scfg, w, h, "oracle", row_step=4)
         r.set_config(cfg)
 
     # ---- the other BASELINE.json configs, device-timed the same way (secondary)
     extras = None
-    if world == 1 and not args.no_extras:
+    if single and not args.no_extras:
         from paper_2005_05386_b200.config import load_config
         extras = {}
-        for name in ("c1_gauss1_512", "c2_flat_1080p", "c4_twist_mesh_1080p", "c5_bumps16_4k",
-                     "c3_bumps16_rk23_1080p"):
+        for name, cpu_kind in (("c1_gauss1_512", "reference"), ("c2_flat_1080p", "reference"),
+                               ("c4_twist_1080p", "reference"), ("c4_twist_mesh_1080p", "oracle"),
+                               ("c5_bumps16_4k", "reference"), ("c3_bumps16_rk23_1080p", "oracle")):
             ecfg = load_config(os.path.join(ROOT, "configs", name + ".json"))
             ew, eh = ecfg.output.width, ecfg.output.height
             ebuf = torch.empty((eh, ew, 3), dtype=torch.uint8, device="cuda")
             r.set_config(ecfg)
             ecam = r.build_camera(ecfg.camera)
-            r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp)
-            n = 3
-            eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(n)]
-            torch.cuda.synchronize()
-            for i in range(n):
-                flush.zero_()
-                eev[i][0].record(stream)
-                r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp)
-                eev[i][1].record(stream)
-            torch.cuda.synchronize()
-            ems = statistics.mean(a.elapsed_time(b) for a, b in eev)
+            ems = statistics.mean(device_time(
+                lambda: r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp), 3, 1))
             est = r.render_device(ecam, ecfg.integrator, ew, eh, ebuf, stream=sp, with_stats=True)
-            extras[name] = {"size": f"{ew}x{eh}", "scheme": ecfg.integrator.scheme,
-                            "h": ecfg.integrator.h, "ms_per_frame": ems, "fps": 1e3 / ems,
-                            "steps_per_s": est["total_steps"] / (ems * 1e-3),
-                            "avg_steps_per_ray": est["total_steps"] / (ew * eh),
-                            "kernel": r.last_kernel}
+            ent = {"size": f"{ew}x{eh}", "scheme": ecfg.integrator.scheme,
+                   "h": ecfg.integrator.h, "max_steps": ecfg.integrator.max_steps,
+                   "ms_per_frame": ems, "fps": 1e3 / ems,
+                   "steps_per_s": est["total_steps"] / (ems * 1e-3),
+                   "integrated_steps_per_s": est["integrated_steps"] / (ems * 1e-3),
+                   "avg_steps_per_ray": est["total_steps"] / (ew * eh),
+                   "simt_efficiency": simt(est),
+                   "kernel": r.last_kernel}
+            if ecfg.metric.kind == "euclidean":
+                # Euclidean rays jump straight to their exit/hit: the reference-
+                # equivalent steps/s is mostly skipped work, not throughput
+                ent["note"] = ("steps_per_s counts reference-equivalent steps; Gamma = 0 rays "
+                               "jump straight to their exit or hit (integrated_steps_per_s is "
+                               "the work done)")
+            else:
+                ent["rk4_steps_per_s"] = rk4_steps(est) / (ems * 1e-3)
+                eflop = algorithmic_flops(est, ecfg.integrator.scheme)
+                if ecfg.metric.kind == "graph":
+                    ent["achieved_tflops"] = eflop / (ems * 1e-3) / 1e12
+                    ent["frac"] = ent["achieved_tflops"] / peak
+            if not args.no_cpu_baseline:
+                ent["cpu_baseline"] = cpu_sample(cpu_kind, ecfg, ew, eh)
+            extras[name] = ent
             del ebuf
         # BASELINE configs[4] as an animation: every frame a NEW scene (bump
         # centres move, cli.animated_config), so each frame pays the scene
@@ -423,40 +612,26 @@ def run_b200(args, cfg):
         r.set_config(cfg)
 
     # ---- e2e through the public API with host buffers (rank 0 only, N=1 path)
-    e2e = None
-    if world == 1:
-        host = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
-        from paper_2005_05386_b200.render import Renderer as _R  # noqa: F401
-        e2e_frames = max(3, args.steps)
-        r.render(cam, integ, w, h, out=host)   # warm
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_frames):
-            r.set_config(cfg)                              # scene upload (params + cull grid)
-            cam_e = r.build_camera(cfg.camera)
-            _, est = r.render(cam_e, integ, w, h, out=host)  # frame -> pinned host + stats
-        e2e_s = (time.perf_counter() - t0) / e2e_frames
-        # per frame host->device: the kernel parameter blocks (scene program +
-        # camera; an unchanged scene is not re-uploaded and the culling grid
-        # is built on the device); device->host: the frame (stored straight
-        # into the pinned buffer by the kernel) + the 64-B stats block
-        info = r.lib.rr_build_info().decode()
-        param_bytes = int(info.split("param_bytes=")[1].split()[0]) if "param_bytes=" in info else 0
-        e2e = {"value": est["total_steps"] / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": param_bytes,
-               "d2h_bytes_per_step": 3 * w * h + 64, "fps": 1.0 / e2e_s,
-               "output": "kernel stores into pinned host memory (UVA)"}
+    e2e = e2e_frames(r, cfg, w, h, max(3, args.steps), lambda st: st["total_steps"]) if single else None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            info = reference_sample(cfg, args.cpu_row_step)
-            cpu = {"value": info["steps_per_s"], "unit": UNIT, "cores": info["cores"],
-                   "kind": "reference", "sample": info["sample"],
-                   "fps_extrapolated": info["fps_extrapolated"]}
-        except Exception as e:   # reference build absent on this box
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+    parity = None
+    if rank == 0 and single:
+        if not args.no_cpu_baseline:
+            try:
+                info = reference_sample(cfg, args.cpu_row_step)
+                cpu = {"value": info["steps_per_s"], "unit": UNIT, "cores": info["cores"],
+                       "kind": "reference", "sample": info["sample"],
+                       "fps_extrapolated": info["fps_extrapolated"],
+                       "scalar_1thread": cpu_sample("reference", cfg, w, h, target_s=3.0,
+                                                    kernel="scalar", workers=1)}
+            except Exception as e:   # reference build absent on this box
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {e}"}
+        if not args.no_parity:
+            # the headline frame, every pixel, against the reference's own
+            # MarchFn (AVX2, all host threads); untimed
+            parity = frame_parity(r, cfg, w, h, "reference", row_step=1)
 
     if rank == 0:
         n_eff = st["bump_evals"] / max(1, 4 * st["integrated_steps"])
@@ -474,16 +649,21 @@ def run_b200(args, cfg):
             "frame_steps": steps_per_frame,
             "avg_steps_per_ray": steps_per_frame / (w * h),
             "n_eff_bumps": n_eff,
+            "rk4_steps_per_s": rk4_steps(st) * args.steps / (total_ms * 1e-3),
+            "integrated_steps_per_s": st["integrated_steps"] * args.steps / (total_ms * 1e-3),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "frac_nominal": achieved / NOMINAL_FP32_TFLOPS,
+                         "traffic": traffic,
                          "peak_source": "measured FFMA microbenchmark (rr_measure_fp32_peak)",
                          "peak_nominal": NOMINAL_FP32_TFLOPS,
                          "flop_per_launch": flop_launch, "kernel": r.last_kernel},
+            "spills": spill_report(),
             "e2e": e2e,
+            "parity": parity,
             "shadows": shadows,
             "workloads": extras,
             "gpu_launches": args.steps * (1 if world == 1 or exchange == "p2p-epilogue" else 2),
-            "simt_efficiency": {"primary": st["integrated_steps"] / max(1, st["lane_slots"])},
+            "simt_efficiency": simt(st),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

@@ -27,7 +27,11 @@
  *
  * Thread safety: a context may be used from many host threads at once (the
  * reference calls MarchFn concurrently from RRAY_THREADS workers,
- * render.cpp:117-156); calls on one context are serialised internally.
+ * render.cpp:29-37, :67-104); calls on one context are serialised
+ * internally, and every call sets the context's device first, whatever the
+ * calling thread's current device.  Asynchronous *_device calls on one
+ * context may use different streams: a launch on a new stream waits for the
+ * context's previous launch (they share the dispatch counter and scratch).
  */
 #ifndef RRAY_CUDA_H
 #define RRAY_CUDA_H
@@ -208,12 +212,17 @@ typedef struct rr_stats {
     int64_t pixel_errors;             /* magenta pixels */
     /* extensions (device-side accounting) */
     double device_ms;                 /* CUDA-event time of the march launch(es) */
-    int64_t integrated_steps;         /* steps the device actually integrated */
+    int64_t integrated_steps;         /* steps the device actually integrated (a straight jump
+                                         through metric-free space counts once), all passes */
     int64_t bump_evals;               /* Gaussian-term evaluations executed (N_eff accounting) */
     int64_t shadow_steps;             /* steps spent on shadow geodesics (EXT) */
     int64_t kernel_launches;          /* launches issued by the call */
     int64_t lane_slots;               /* primary: warp loop iterations x 32 (SIMT efficiency = integrated / slots) */
     int64_t shadow_lane_slots;        /* same for the shadow pass (EXT) */
+    int64_t jump_steps;               /* primary integrated steps that were straight jumps through
+                                         metric-free space (no RK4 / metric evaluation) */
+    int64_t shadow_jump_steps;        /* same for the shadow pass (EXT) */
+    int64_t shadow_integrated_steps;  /* the shadow pass's share of integrated_steps (EXT) */
 } rr_stats;
 
 /* ---- tuning knobs (extension; defaults are parity-safe) ------------------- */
@@ -271,6 +280,15 @@ int rr_march_device(rr_ctx* ctx, const rr_integrator* integ, const rr_ray_start*
  * mapping; pageable buffers get a device->host copy after the kernel. */
 int rr_render(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
               int height, uint8_t* rgb_out, rr_stats* stats);
+
+/* Whole frame with per-pixel outcomes (parity entry of the frame path): the
+ * SAME frame kernel rr_render launches (device raygen, march, shade) also
+ * writes each pixel's render::PixelOutcome record (kernel.hpp:33-39, the
+ * records render.cpp:68-84 shades), row-major, into `out` (w*h records).
+ * `rgb_out` (3*w*h bytes) may be NULL.  With lights the outcome is the
+ * primary ray's (the shadow pass only shades). */
+int rr_render_outcomes(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* integ, int width,
+                       int height, uint8_t* rgb_out, rr_pixel_outcome* out, rr_stats* stats);
 
 /* Whole-frame render into a DEVICE buffer on a caller stream.  When `stats`
  * is non-NULL the call synchronises the stream to fill it; pass NULL for
@@ -343,6 +361,11 @@ int rr_diffeo_image(rr_ctx* ctx, const double* p, double* image);
 /* Microbenchmark of the FP32 FMA pipe (roofline denominator): returns the
  * measured dense FFMA throughput of this device in TFLOP/s. */
 int rr_measure_fp32_peak(rr_ctx* ctx, double* tflops);
+
+/* Diagnostics: name of the kernel variant the context's last launch used
+ * (e.g. "march2_kernel<bumps16>"); "" before the first launch.  The
+ * reference has no counterpart (its KernelKind is chosen, not reported). */
+const char* rr_last_kernel(const rr_ctx* ctx);
 
 #ifdef __cplusplus
 }

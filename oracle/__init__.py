@@ -60,6 +60,14 @@ class Oracle:
         lib.rro_flags.argtypes = [C.POINTER(abi.rr_metric_desc), C.POINTER(abi.rr_scene_desc),
                                   C.POINTER(abi.rr_camera), C.POINTER(abi.rr_integrator),
                                   C.c_int, C.c_int, P, C.c_double, C.c_double, P, C.c_int]
+        lib.rro_render_rows.argtypes = [C.POINTER(abi.rr_metric_desc), C.POINTER(abi.rr_scene_desc),
+                                        C.POINTER(abi.rr_camera), C.POINTER(abi.rr_integrator),
+                                        C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                                        C.POINTER(abi.rr_stats), C.c_int]
+        lib.rro_flags_pixels.argtypes = [C.POINTER(abi.rr_metric_desc), C.POINTER(abi.rr_scene_desc),
+                                         C.POINTER(abi.rr_camera), C.POINTER(abi.rr_integrator),
+                                         C.c_int, C.c_int, P, P, C.c_size_t, C.c_double, C.c_double,
+                                         P, C.c_int]
         lib.rro_set_mesh_bruteforce.argtypes = [C.c_int]
         self.lib = lib
         self.threads = os.cpu_count() or 1
@@ -119,6 +127,38 @@ class Oracle:
                                w, h, _ptr(out), perturb, wrap_eps, _ptr(flags), self.threads)
         return rgb, out, st.as_dict(), flags
 
+    def render_rows(self, cfg: RunConfig, w: int, h: int, row0: int, row_step: int,
+                    camera_cfg: RunConfig = None, threads: int = 0):
+        """Rows row0, row0+row_step, ... of the w x h frame (lights included)
+        -> (rgb[rows,w,3], outcomes[rows*w], stats with wall_seconds)."""
+        md, sd = MetricDesc(cfg.metric), SceneDesc(cfg.scene)
+        integ = cfg.integrator.to_abi()
+        cam = self.camera(camera_cfg if camera_cfg is not None else cfg)
+        rows = len(range(row0, h, row_step))
+        rgb = np.zeros((rows, w, 3), np.uint8)
+        out = np.zeros(rows * w, abi.OUTCOME_DTYPE)
+        st = abi.rr_stats()
+        self.lib.rro_render_rows(C.byref(md.desc), C.byref(sd.desc), C.byref(cam), C.byref(integ),
+                                 w, h, row0, row_step, _ptr(rgb), _ptr(out), C.byref(st),
+                                 threads or self.threads)
+        return rgb, out, st.as_dict()
+
+    def flags_pixels(self, cfg: RunConfig, w: int, h: int, pix, outcomes, perturb: float = 1e-4,
+                     wrap_eps: float = 1e-4, camera_cfg: RunConfig = None) -> np.ndarray:
+        """rro_flags for the listed pixels only (row-major indices of the w x h
+        frame; outcomes = their FP64 outcomes)."""
+        md, sd = MetricDesc(cfg.metric), SceneDesc(cfg.scene)
+        integ = cfg.integrator.to_abi()
+        cam = self.camera(camera_cfg if camera_cfg is not None else cfg)
+        pix = np.ascontiguousarray(pix, np.int64)
+        outcomes = np.ascontiguousarray(outcomes, abi.OUTCOME_DTYPE)
+        flags = np.zeros(len(pix), np.uint8)
+        if len(pix):
+            self.lib.rro_flags_pixels(C.byref(md.desc), C.byref(sd.desc), C.byref(cam),
+                                      C.byref(integ), w, h, _ptr(pix), _ptr(outcomes), len(pix),
+                                      perturb, wrap_eps, _ptr(flags), self.threads)
+        return flags
+
     def flow_accel(self, cfg: RunConfig, pos, vel):
         md = MetricDesc(cfg.metric)
         acc = (C.c_double * 3)()
@@ -166,7 +206,7 @@ class Reference:
         lib.refc_render.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, P,
                                     C.POINTER(refc_stats), C.c_char_p]
         lib.refc_render_rows.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                         C.c_int, P, C.POINTER(refc_stats)]
+                                         C.c_int, P, P, C.POINTER(refc_stats)]
         lib.refc_camera.argtypes = [C.c_char_p, D]
         lib.refc_primary_rays.argtypes = [C.c_char_p, C.c_int, C.c_int, P]
         lib.refc_march.argtypes = [C.c_char_p, C.c_int, P, P, C.c_size_t]
@@ -203,13 +243,20 @@ class Reference:
         self._check(self.lib.refc_render(j, KERNELS[kernel], workers, w, h, _ptr(rgb), C.byref(st), cj))
         return rgb, {n: getattr(st, n) for n, _ in refc_stats._fields_}
 
-    def render_rows(self, cfg, w, h, row0, row_step, kernel="auto", workers=0):
+    def render_rows(self, cfg, w, h, row0, row_step, kernel="auto", workers=0,
+                    with_outcomes=False):
+        """Rows row0, row0+row_step, ... of the w x h frame through the
+        reference's row work item -> (rgb[rows,w,3], stats) or, with
+        with_outcomes, (rgb, outcomes[rows*w], stats)."""
         rows = len(range(row0, h, row_step))
         rgb = np.zeros((rows, w, 3), np.uint8)
+        out = np.zeros(rows * w, abi.OUTCOME_DTYPE) if with_outcomes else None
         st = refc_stats()
         self._check(self.lib.refc_render_rows(self._json(cfg), KERNELS[kernel], workers, w, h, row0,
-                                              row_step, _ptr(rgb), C.byref(st)))
-        return rgb, {n: getattr(st, n) for n, _ in refc_stats._fields_}
+                                              row_step, _ptr(rgb),
+                                              _ptr(out) if out is not None else None, C.byref(st)))
+        stats = {n: getattr(st, n) for n, _ in refc_stats._fields_}
+        return (rgb, out, stats) if with_outcomes else (rgb, stats)
 
     def camera(self, cfg):
         out = (C.c_double * 19)()

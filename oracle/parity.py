@@ -22,7 +22,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import FLAG_GRAZING, FLAG_LIMIT, FLAG_SHADOW, FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z
+from . import (FLAG_GRAZING, FLAG_LIMIT, FLAG_SHADOW, FLAG_WRAP, FLAG_WRAP_X, FLAG_WRAP_Y,
+               FLAG_WRAP_Z)
 
 ENDPOINT_RTOL = 1e-4
 RGB_TOL = 1
@@ -103,3 +104,58 @@ def compare_rgb(gpu_rgb: np.ndarray, ref_rgb: np.ndarray, flags: np.ndarray | No
     rep.magenta_gpu = magenta(g)
     rep.magenta_ref = magenta(r)
     return rep
+
+
+# ---- full-size frames --------------------------------------------------------
+# Flags only ever EXEMPT a difference, so a full-size check needs the
+# (expensive, 4-12 extra FP64 marches per pixel) GRAZING / LIMIT / SHADOW
+# flags of the pixels whose GPU result differs from the oracle's, and nothing
+# else: WRAP (a coordinate test on the FP64 outcome) is computed everywhere,
+# the candidates are the pixels that fail any rule with WRAP alone, and the
+# oracle flags exactly those (rro_flags_pixels).  The report is then the
+# ordinary compare_outcomes / compare_rgb report over the whole frame.
+
+def wrap_flags(ref: np.ndarray, eps: float = 1e-4) -> np.ndarray:
+    """rro.c near_integer per hit coordinate (render.cpp:18's frac wrap)."""
+    f = np.zeros(len(ref), np.uint8)
+    hit = ref["status"] == 1
+    for k, bit in enumerate((FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z)):
+        c = ref["point"][:, k]
+        near = np.abs(c - np.rint(c)) < eps
+        f |= np.where(hit & near, np.uint8(bit | FLAG_WRAP), np.uint8(0))
+    return f
+
+
+def failing_pixels(gpu: np.ndarray, ref: np.ndarray, gpu_rgb, ref_rgb, flags) -> np.ndarray:
+    """Pixels that break a parity rule under `flags` (the per-pixel version of
+    compare_outcomes + compare_rgb)."""
+    keep = (flags & (FLAG_GRAZING | FLAG_LIMIT)) == 0
+    bad = (gpu["status"] != ref["status"]) & keep
+    hit = (ref["status"] == 1) & (gpu["status"] == 1) & keep
+    bad |= (gpu["prim"] != ref["prim"]) & hit
+    d = np.linalg.norm(gpu["point"] - ref["point"], axis=1)
+    nrm = np.maximum(np.linalg.norm(ref["point"], axis=1), 1e-300)
+    bad |= hit & (d / nrm > ENDPOINT_RTOL)
+    if gpu_rgb is not None:
+        g = gpu_rgb.reshape(-1, 3).astype(np.int32)
+        r = ref_rgb.reshape(-1, 3).astype(np.int32)
+        diff = np.abs(g - r)
+        for ch, bit in enumerate((FLAG_WRAP_X, FLAG_WRAP_Y, FLAG_WRAP_Z)):
+            diff[(flags & bit) != 0, ch] = 0
+        keep_rgb = (flags & (FLAG_GRAZING | FLAG_LIMIT | FLAG_SHADOW)) == 0
+        bad |= (diff.max(axis=1) > RGB_TOL) & keep_rgb
+    return bad
+
+
+def check_frame(gpu_out: np.ndarray, ref_out: np.ndarray, gpu_rgb, ref_rgb, flag_fn):
+    """Full-frame (or row-subsample) parity.  flag_fn(idx) -> the oracle's
+    flags of the listed pixels (indices into the arrays given here).
+    Returns (ParityReport, flags, candidates)."""
+    flags = wrap_flags(ref_out)
+    cand = np.nonzero(failing_pixels(gpu_out, ref_out, gpu_rgb, ref_rgb, flags))[0]
+    if len(cand):
+        flags[cand] |= flag_fn(cand)
+    rep = compare_outcomes(gpu_out, ref_out, flags)
+    if gpu_rgb is not None:
+        rep = compare_rgb(gpu_rgb, ref_rgb, flags, rep)
+    return rep, flags, int(len(cand))

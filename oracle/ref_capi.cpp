@@ -127,7 +127,8 @@ int refc_render(const char* json, int kernel, int workers, int width, int height
 // a pool of `workers` threads; used to time the reference on frames too
 // large to render whole inside the bench budget.
 int refc_render_rows(const char* json, int kernel, int workers, int width, int height,
-                     int row0, int row_step, std::uint8_t* rgb_rows, refc_stats* st) {
+                     int row0, int row_step, std::uint8_t* rgb_rows, void* outcome_rows,
+                     refc_stats* st) {
     return guarded([&] {
         config::RunConfig cfg = config::parse_config(json);
         if (width > 0) cfg.output.width = width;
@@ -157,6 +158,10 @@ int refc_render_rows(const char* json, int kernel, int workers, int width, int h
                     rays[px] = render::RayStart{cam.position,
                                                 render::pixel_direction(cam, px, py, w, h)};
                 march(ctx, rays.data(), res.data(), rays.size());
+                if (outcome_rows)   // the row's PixelOutcome records, as render() shades them
+                    std::memcpy(static_cast<render::PixelOutcome*>(outcome_rows) +
+                                    static_cast<std::size_t>(k) * w,
+                                res.data(), sizeof(render::PixelOutcome) * w);
                 std::uint8_t* row = rgb_rows + static_cast<std::size_t>(k) * 3 * w;
                 for (int px = 0; px < w; ++px) {
                     const auto& o = res[px];

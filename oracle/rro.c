@@ -7,6 +7,7 @@
  * (proj/CMakeLists.txt:12-13).  Reference paths below are relative to
  * /root/reference/proj.
  */
+#define _POSIX_C_SOURCE 200809L
 #include "rro.h"
 
 #include <math.h>
@@ -15,6 +16,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 static _Thread_local char g_err[256];
 const char* rro_last_error(void) { return g_err; }
@@ -1193,12 +1195,14 @@ typedef struct {
     const rr_metric_desc* m; const rr_scene_desc* sc; const rr_camera* cam;
     const rr_integrator* in; int w, h; uint8_t* rgb; rr_pixel_outcome* outcomes;
     atomic_llong total_steps, errors, shadow_steps;
+    int row0, row_step;     /* work item k = row row0 + k row_step, stored at row k */
 } RenderArgs;
 
 static void render_rows(void* p, long lo, long hi) {
     RenderArgs* a = (RenderArgs*)p;
     long long steps = 0, errors = 0, sh_steps = 0;
-    for (long py = lo; py < hi; ++py) {
+    for (long k = lo; k < hi; ++k) {
+        const long py = a->row0 + k * a->row_step;
         for (int px = 0; px < a->w; ++px) {
             rr_ray_start ray;
             double d[3];
@@ -1210,7 +1214,7 @@ static void render_rows(void* p, long lo, long hi) {
             rr_pixel_outcome o;
             V3 n = v3(0.0, 0.0, 0.0);
             march_one_n(a->m, a->sc, a->in, &ray, &o, &n);
-            const size_t i = (size_t)py * a->w + px;
+            const size_t i = (size_t)k * a->w + px;
             if (a->outcomes) a->outcomes[i] = o;
             steps += o.steps;
             if (o.status == RR_FAILED) ++errors;
@@ -1232,11 +1236,46 @@ void rro_render(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camer
     atomic_init(&a.total_steps, 0);
     atomic_init(&a.errors, 0);
     atomic_init(&a.shadow_steps, 0);
+    a.row0 = 0;
+    a.row_step = 1;
     prepare_meshes(sc);
     parallel_for(h, 1, threads, render_rows, &a);
     if (stats) {
         memset(stats, 0, sizeof *stats);
         stats->rays = (int64_t)w * h;
+        stats->total_steps = atomic_load(&a.total_steps);
+        stats->pixel_errors = atomic_load(&a.errors);
+        stats->integrated_steps = stats->total_steps;
+        stats->shadow_steps = atomic_load(&a.shadow_steps);
+    }
+}
+
+/* Rows row0, row0 + row_step, ... of the w x h frame (row k of the outputs
+ * = frame row row0 + k row_step): the deterministic row subsample used for
+ * full-size parity checks and for timing frames too large to render whole
+ * on the CPU.  stats->wall_seconds is the wall time. */
+void rro_render_rows(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+                     const rr_integrator* integ, int w, int h, int row0, int row_step,
+                     uint8_t* rgb_rows, rr_pixel_outcome* outcome_rows, rr_stats* stats,
+                     int threads) {
+    RenderArgs a;
+    a.m = m; a.sc = sc; a.cam = cam; a.in = integ; a.w = w; a.h = h;
+    a.rgb = rgb_rows; a.outcomes = outcome_rows;
+    a.row0 = row0;
+    a.row_step = row_step > 0 ? row_step : 1;
+    atomic_init(&a.total_steps, 0);
+    atomic_init(&a.errors, 0);
+    atomic_init(&a.shadow_steps, 0);
+    const long rows = row0 < h ? (h - 1 - row0) / a.row_step + 1 : 0;
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    prepare_meshes(sc);
+    parallel_for(rows, 1, threads, render_rows, &a);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        stats->wall_seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+        stats->rays = (int64_t)rows * w;
         stats->total_steps = atomic_load(&a.total_steps);
         stats->pixel_errors = atomic_load(&a.errors);
         stats->integrated_steps = stats->total_steps;
@@ -1251,17 +1290,16 @@ typedef struct {
     const rr_metric_desc* m; const rr_scene_desc* sc; const rr_camera* cam;
     const rr_integrator* in; int w, h; const rr_pixel_outcome* outcomes;
     double perturb, wrap_eps; uint8_t* flags;
+    const int64_t* pix;     /* rro_flags_pixels: pixel indices (row-major) */
 } FlagArgs;
 
-static void flag_rows(void* p, long lo, long hi) {
-    FlagArgs* a = (FlagArgs*)p;
+/* Flags of pixel (px, py) whose FP64 outcome is *o (see rro.h). */
+static uint8_t flag_pixel(const FlagArgs* a, int px, int py, const rr_pixel_outcome* o) {
     const rr_camera* cam = a->cam;
     const S3 g = {cam->g[0], cam->g[1], cam->g[2], cam->g[3], cam->g[4], cam->g[5]};
     const V3 up = vfrom(cam->frame[1]), right = vfrom(cam->frame[2]);
-    for (long py = lo; py < hi; ++py) {
-        for (int px = 0; px < a->w; ++px) {
-            const size_t i = (size_t)py * a->w + px;
-            const rr_pixel_outcome* o = &a->outcomes[i];
+    {
+        {
             uint8_t f = 0;
             if (o->status == RR_HIT) {
                 if (near_integer(o->point.x, a->wrap_eps)) f |= RRO_FLAG_WRAP | RRO_FLAG_WRAP_X;
@@ -1344,15 +1382,44 @@ static void flag_rows(void* p, long lo, long hi) {
                         }
                 }
             }
-            a->flags[i] = f;
+            return f;
         }
     }
+}
+
+static void flag_rows(void* p, long lo, long hi) {
+    FlagArgs* a = (FlagArgs*)p;
+    for (long py = lo; py < hi; ++py)
+        for (int px = 0; px < a->w; ++px) {
+            const size_t i = (size_t)py * a->w + px;
+            a->flags[i] = flag_pixel(a, px, (int)py, &a->outcomes[i]);
+        }
 }
 
 void rro_flags(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
                const rr_integrator* integ, int w, int h, const rr_pixel_outcome* outcomes,
                double perturb_rad, double wrap_eps, uint8_t* flags, int threads) {
-    FlagArgs a = {m, sc, cam, integ, w, h, outcomes, perturb_rad, wrap_eps, flags};
+    FlagArgs a = {m, sc, cam, integ, w, h, outcomes, perturb_rad, wrap_eps, flags, NULL};
     prepare_meshes(sc);
     parallel_for(h, 1, threads, flag_rows, &a);
+}
+
+static void flag_list(void* p, long lo, long hi) {
+    FlagArgs* a = (FlagArgs*)p;
+    for (long k = lo; k < hi; ++k) {
+        const int64_t i = a->pix[k];
+        a->flags[k] = flag_pixel(a, (int)(i % a->w), (int)(i / a->w), &a->outcomes[k]);
+    }
+}
+
+/* Flags of a list of pixels only (outcomes[k] = FP64 outcome of pixel
+ * pix[k]): a full-size parity check flags just the pixels whose GPU result
+ * differs, since flags only ever exempt a difference. */
+void rro_flags_pixels(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+                      const rr_integrator* integ, int w, int h, const int64_t* pix,
+                      const rr_pixel_outcome* outcomes, size_t n, double perturb_rad,
+                      double wrap_eps, uint8_t* flags, int threads) {
+    FlagArgs a = {m, sc, cam, integ, w, h, outcomes, perturb_rad, wrap_eps, flags, pix};
+    prepare_meshes(sc);
+    parallel_for((long)n, 1, threads, flag_list, &a);
 }

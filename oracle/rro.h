@@ -65,6 +65,19 @@ void rro_flags(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera
                const rr_integrator* integ, int w, int h, const rr_pixel_outcome* outcomes,
                double perturb_rad, double wrap_eps, uint8_t* flags, int threads);
 
+/* Rows row0, row0 + row_step, ... of the w x h frame (output row k = frame
+ * row row0 + k row_step); rgb_rows / outcome_rows may be NULL. */
+void rro_render_rows(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+                     const rr_integrator* integ, int w, int h, int row0, int row_step,
+                     uint8_t* rgb_rows, rr_pixel_outcome* outcome_rows, rr_stats* stats,
+                     int threads);
+/* Parity flags of a list of pixels (row-major indices pix[k], FP64 outcome
+ * outcomes[k]); same flags as rro_flags. */
+void rro_flags_pixels(const rr_metric_desc* m, const rr_scene_desc* sc, const rr_camera* cam,
+                      const rr_integrator* integ, int w, int h, const int64_t* pix,
+                      const rr_pixel_outcome* outcomes, size_t n, double perturb_rad,
+                      double wrap_eps, uint8_t* flags, int threads);
+
 /* Test hook: 1 = mesh intersection scans every triangle (no BVH pruning). */
 void rro_set_mesh_bruteforce(int on);
 

@@ -110,7 +110,8 @@ class rr_stats(C.Structure):
                 ("device_ms", C.c_double), ("integrated_steps", C.c_int64),
                 ("bump_evals", C.c_int64), ("shadow_steps", C.c_int64),
                 ("kernel_launches", C.c_int64), ("lane_slots", C.c_int64),
-                ("shadow_lane_slots", C.c_int64)]
+                ("shadow_lane_slots", C.c_int64), ("jump_steps", C.c_int64),
+                ("shadow_jump_steps", C.c_int64), ("shadow_integrated_steps", C.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -135,7 +136,7 @@ EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
     "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
     "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 24,
-    "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 88,
+    "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 112,
     "rr_options": 32,
 }
 
@@ -170,6 +171,9 @@ SIGNATURES = {
                             C.c_int, _P, C.POINTER(rr_stats)]),
     "rr_render_device": (C.c_int, [_P, C.POINTER(rr_camera), C.POINTER(rr_integrator),
                                    C.c_int, C.c_int, _P, C.POINTER(rr_stats), _P]),
+    "rr_render_outcomes": (C.c_int, [_P, C.POINTER(rr_camera), C.POINTER(rr_integrator),
+                                     C.c_int, C.c_int, _P, _P, C.POINTER(rr_stats)]),
+    "rr_last_kernel": (C.c_char_p, [_P]),
     "rr_shard_tile_count": (C.c_int, [C.c_int] * 6),
     "rr_render_tiles": (C.c_int, [_P, C.POINTER(rr_camera), C.POINTER(rr_integrator),
                                   C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P,

@@ -42,6 +42,7 @@ constexpr int kMaxLights = 8;     // point lights (EXTENSION)
 constexpr int kMaxMeshes = 4;     // triangle-mesh primitives (EXTENSION)
 constexpr int kUnit = 32;         // rays per warp unit
 constexpr int kMicroW = 8, kMicroH = 4;   // pixel micro-tile of one warp
+constexpr int kStatSlots = 11;    // 64-bit device counters per launch (DevLaunch::stats)
 
 // g = beta * g' where g'_k = d_k * K_k, K_k = -(1/2) log2(e) / sigma_k^2.
 constexpr float kBeta = -1.3862943611198906f;   // -2 ln 2
@@ -182,10 +183,15 @@ struct DevLaunch {
     int lpp;                      // shadow pass: lights marched per pixel in one unit (1/2/4)
     uint8_t* rgb;                 // frame (row-major) or tile-major buffer
     const double* rays;           // RAYS: 6 doubles per ray (RayStart)
-    uint8_t* outcomes;            // RAYS: 48-byte PixelOutcome records
+    uint8_t* outcomes;            // 48-byte PixelOutcome records: RAYS (by ray), frames when
+                                  // non-null (outcome sink, row-major pixel index)
+    int vec16;                    // ray-pair epilogue may store 16x4 RGB blocks as 16-B words
     unsigned long long n_rays;
     unsigned* counter;            // unit dispensers [2] (zeroed per launch)
-    unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays [5] shadow steps
+    unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays
+                                  // [5] shadow steps [6] lane slots [7] shadow lane slots
+                                  // [8] jumps [9] shadow jumps [10] shadow integrated
+                                  // (kStatSlots entries)
     HitRec* hits;                 // EXTENSION: hit records (lights present)
     unsigned* done;               // EXTENSION: lights finished per ray-pair unit (zeroed per launch)
     uint8_t* vis;                 // EXTENSION: light visibility per (pixel, light)

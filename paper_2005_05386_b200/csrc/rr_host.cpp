@@ -91,7 +91,7 @@ struct rr_ctx {
     double masks_radius = 0.0;
     int masks_mode = 0;
     // scratch
-    uint8_t* d_aux = nullptr;                // [0,8): counter, [8,8+8*8): stats
+    uint8_t* d_aux = nullptr;                // [0,8): counters, [8,8+8*kStatSlots): stats
     unsigned long long* h_stats = nullptr;   // pinned
     void* d_rays = nullptr;
     void* d_out = nullptr;
@@ -106,6 +106,12 @@ struct rr_ctx {
     size_t vis_cap = 0;
     const char* last_kernel = "";
     int last_launches = 0;
+    // Launches on one context may come on different caller streams; they
+    // share the dispatch counter, the stats block, the culling grid and the
+    // hit/visibility scratch, so a launch on a new stream first waits for
+    // the previous launch (ev1, recorded after it).
+    bool launched = false;
+    cudaStream_t last_stream = nullptr;
 };
 
 namespace {
@@ -440,8 +446,10 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
     // a previous grid build on `s` may still read the records: order the copy
     // after it (scene changes only; static scenes never get here)
     RR_CUDA(c, cudaStreamSynchronize(s));
-    RR_CUDA(c, cudaMemcpy(c->d_cull_gauss, g.data(), 8 * (size_t)n * sizeof(double),
-                          cudaMemcpyHostToDevice));
+    // stream-ordered before the build kernels on `s` (a legacy-stream copy
+    // would not be ordered against a non-blocking stream)
+    RR_CUDA(c, cudaMemcpyAsync(c->d_cull_gauss, g.data(), 8 * (size_t)n * sizeof(double),
+                               cudaMemcpyHostToDevice, s));
     double lo[3], cell[3];
     for (int k = 0; k < 3; ++k) {
         lo[k] = P.lo[k];
@@ -602,7 +610,11 @@ int ensure_device_buffer(rr_ctx* c, void** buf, size_t* cap, size_t need) {
 }
 
 int check_ready(rr_ctx* c, const rr_integrator* integ, cudaStream_t s) {
+    // every launch and allocation below targets the context's device,
+    // whatever the calling thread's current device is
+    RR_CUDA(c, cudaSetDevice(c->device));
     if (!c->has_scene) return set_err(c, RR_ERR_CONFIG, "no scene: call rr_set_scene first");
+    if (c->launched && s != c->last_stream) RR_CUDA(c, cudaStreamWaitEvent(s, c->ev1, 0));
     if (!integ || !(integ->h > 0.0)) return set_err(c, RR_ERR_CONFIG, "integrator.h: must be > 0");
     if (integ->max_steps < 1) return set_err(c, RR_ERR_CONFIG, "integrator.max_steps: must be >= 1");
     if (integ->scheme != RR_SCHEME_EULER && integ->scheme != RR_SCHEME_RK4 &&
@@ -641,17 +653,19 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
         L.vis = reinterpret_cast<uint8_t*>(c->d_vis) + flag_bytes;
         RR_CUDA(c, cudaMemsetAsync(c->d_vis, 0, 2 * pairs * sizeof(unsigned), s));
     }
-    RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * 8, s));
+    RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * rr::kStatSlots, s));
     L.counter = reinterpret_cast<unsigned*>(c->d_aux);
     L.stats = reinterpret_cast<unsigned long long*>(c->d_aux + 8);
     RR_CUDA(c, cudaEventRecord(c->ev0, s));
     RR_CUDA(c, rr::launch_march(*c->P, L, s, c->num_sms, &c->last_kernel, &c->last_launches));
     RR_CUDA(c, cudaEventRecord(c->ev1, s));
+    c->launched = true;
+    c->last_stream = s;
     return RR_OK;
 }
 
 int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
-    RR_CUDA(c, cudaMemcpyAsync(c->h_stats, c->d_aux + 8, 8 * 8, cudaMemcpyDeviceToHost, s));
+    RR_CUDA(c, cudaMemcpyAsync(c->h_stats, c->d_aux + 8, 8 * rr::kStatSlots, cudaMemcpyDeviceToHost, s));
     RR_CUDA(c, cudaStreamSynchronize(s));
     if (st) {
         std::memset(st, 0, sizeof *st);
@@ -666,6 +680,9 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->shadow_steps = (int64_t)c->h_stats[5];
         st->lane_slots = (int64_t)c->h_stats[6];
         st->shadow_lane_slots = (int64_t)c->h_stats[7];
+        st->jump_steps = (int64_t)c->h_stats[8];
+        st->shadow_jump_steps = (int64_t)c->h_stats[9];
+        st->shadow_integrated_steps = (int64_t)c->h_stats[10];
         st->kernel_launches = c->last_launches;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -708,6 +725,14 @@ int setup_frame_launch(rr_ctx* c, const rr_camera* cam, int width, int height, i
     if (units > 0xffffffffLL) return set_err(c, RR_ERR_CONFIG, "frame too large");
     L.n_units = (unsigned)units;
     L.rgb = rgb;
+    // 16x4 RGB blocks of the ray-pair epilogue as 16-B stores: rows must be
+    // 16-B aligned and micro-tiles 2u, 2u+1 side by side in one tile row
+    const bool even_mpr = (tile_w / rr::kMicroW) % 2 == 0;
+    const bool aligned = (reinterpret_cast<uintptr_t>(rgb) & 15u) == 0;
+    if (mode == rr::kModeFrame)
+        L.vec16 = even_mpr && aligned && ((size_t)3 * width) % 16 == 0;
+    else
+        L.vec16 = even_mpr && aligned && (3 * tile_w) % 16 == 0 && (3 * tile_w * tile_h) % 16 == 0;
     return RR_OK;
 }
 
@@ -755,8 +780,8 @@ int rr_create(rr_ctx** out, int device) {
         return fail(e, "cudaStreamCreate");
     if ((e = cudaEventCreate(&c->ev0)) != cudaSuccess) return fail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&c->ev1)) != cudaSuccess) return fail(e, "cudaEventCreate");
-    if ((e = cudaMalloc(&c->d_aux, 8 + 8 * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
-    if ((e = cudaMallocHost(&c->h_stats, 8 * 8)) != cudaSuccess) return fail(e, "cudaMallocHost");
+    if ((e = cudaMalloc(&c->d_aux, 8 + 8 * rr::kStatSlots)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMallocHost(&c->h_stats, 8 * rr::kStatSlots)) != cudaSuccess) return fail(e, "cudaMallocHost");
     *out = c;
     return RR_OK;
 }
@@ -858,7 +883,15 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
     fill_params(prog, sc, *np, slots);
     const bool same = c->has_scene && c->P_key && std::memcmp(c->P_key, np, sizeof *np) == 0;
     if (!same) {
-        // meshes: build BVHs on the host, upload to device buffers
+        // meshes: build BVHs on the host, upload to device buffers (on this
+        // context's device, whatever the calling thread's current device)
+        cudaError_t de = cudaSetDevice(c->device);
+        if (de != cudaSuccess) {
+            delete np;
+            return cuda_err(c, de, "cudaSetDevice");
+        }
+        // a launch in flight may still read the previous scene's buffers
+        if (c->launched) cudaEventSynchronize(c->ev1);
         for (void* p : c->d_mesh) cudaFree(p);
         c->d_mesh.clear();
         int m = 0;
@@ -871,9 +904,13 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
             cudaError_t e = cudaMalloc(&dn, bvh.nodes.size() * sizeof(float));
             if (e == cudaSuccess) e = cudaMalloc(&dt, bvh.tris.size() * sizeof(float));
             if (e == cudaSuccess)
-                e = cudaMemcpy(dn, bvh.nodes.data(), bvh.nodes.size() * sizeof(float), cudaMemcpyHostToDevice);
+                e = cudaMemcpyAsync(dn, bvh.nodes.data(), bvh.nodes.size() * sizeof(float),
+                                    cudaMemcpyHostToDevice, c->stream);
             if (e == cudaSuccess)
-                e = cudaMemcpy(dt, bvh.tris.data(), bvh.tris.size() * sizeof(float), cudaMemcpyHostToDevice);
+                e = cudaMemcpyAsync(dt, bvh.tris.data(), bvh.tris.size() * sizeof(float),
+                                    cudaMemcpyHostToDevice, c->stream);
+            // launches may use caller streams: the BVH must be resident first
+            if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
             if (dn) c->d_mesh.push_back(dn);
             if (dt) c->d_mesh.push_back(dt);
             if (e != cudaSuccess) {
@@ -999,64 +1036,99 @@ int rr_march(rr_ctx* c, const rr_integrator* integ, const rr_ray_start* rays,
     return RR_OK;
 }
 
-int rr_render_device(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
-                     int height, uint8_t* d_rgb, rr_stats* stats, void* stream) {
-    if (!c) return RR_ERR_CONFIG;
-    std::lock_guard<std::mutex> lk(c->mu);
-    const double t0 = now_s();
-    int rc = check_ready(c, integ, stream ? (cudaStream_t)stream : c->stream);
+}  // extern "C"
+
+namespace {
+
+// Whole frame on the device (caller holds c->mu).  `d_out` (optional): the
+// frame kernel's PixelOutcome sink, row-major by pixel.
+int render_device_locked(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                         int height, uint8_t* d_rgb, rr_pixel_outcome* d_out, rr_stats* stats,
+                         cudaStream_t s, double t0) {
+    int rc = check_ready(c, integ, s);
     if (rc) return rc;
     if (!d_rgb) return set_err(c, RR_ERR_CONFIG, "rgb: required");
-    RR_CUDA(c, cudaSetDevice(c->device));
     rr::DevLaunch L;
     const int tw = c->opt.o.block_x > 0 ? c->opt.o.block_x : 32;
     const int th = c->opt.o.block_y > 0 ? c->opt.o.block_y : 32;
     if ((rc = setup_frame_launch(c, cam, width, height, tw, th, 0, 1, rr::kModeFrame, d_rgb, L)))
         return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    L.outcomes = reinterpret_cast<uint8_t*>(d_out);
     if ((rc = run_launch(c, L, s))) return rc;
     if (stats) return collect_stats(c, s, stats, t0);
     return RR_OK;
 }
 
-int rr_render(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width, int height,
-              uint8_t* rgb_out, rr_stats* stats) {
-    if (!c) return RR_ERR_CONFIG;
+// Host-buffer frame (caller holds c->mu): pinned caller memory is written by
+// the kernel through its UVA mapping, pageable memory gets a D2H copy.
+int render_host_locked(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                       int height, uint8_t* rgb_out, rr_pixel_outcome* out, rr_stats* stats) {
     const double t0 = now_s();
+    if (!rgb_out && !out) return set_err(c, RR_ERR_CONFIG, "rgb: required");
+    if (width < 1 || height < 1) return set_err(c, RR_ERR_CONFIG, "output.width/height: must be >= 1");
+    RR_CUDA(c, cudaSetDevice(c->device));
     uint8_t* target = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(c->mu);
-        if (!rgb_out) return set_err(c, RR_ERR_CONFIG, "rgb: required");
-        if (width < 1 || height < 1)
-            return set_err(c, RR_ERR_CONFIG, "output.width/height: must be >= 1");
-        RR_CUDA(c, cudaSetDevice(c->device));
-        // Pinned (page-locked, UVA-mapped) caller memory: the shade epilogue
-        // stores each pixel straight into it (~0.5 GB/s of PCIe/C2C writes
-        // spread over the kernel), so no separate device->host copy follows.
-        cudaPointerAttributes pa;
-        if (cudaPointerGetAttributes(&pa, rgb_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-            pa.devicePointer)
-            target = static_cast<uint8_t*>(pa.devicePointer);
-        else
-            cudaGetLastError();   // pageable memory: not an error
-        if (!target) {
-            const size_t bytes = (size_t)3 * width * height;
-            void* buf = c->d_rgb;
-            int rc = ensure_device_buffer(c, &buf, &c->rgb_cap, bytes);
-            c->d_rgb = (uint8_t*)buf;
-            if (rc) return rc;
-        }
+    if (rgb_out) {
+    // Pinned (page-locked, UVA-mapped) caller memory: the shade epilogue
+    // stores each pixel straight into it (16-B stores per 16x4 block over
+    // PCIe/C2C, spread over the kernel), so no separate copy follows.
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, rgb_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+        target = static_cast<uint8_t*>(pa.devicePointer);
+    else
+        cudaGetLastError();   // pageable memory: not an error
     }
-    int rc = rr_render_device(c, cam, integ, width, height, target ? target : c->d_rgb, nullptr,
-                              c->stream);
+    const size_t bytes = (size_t)3 * width * height;
+    int rc;
+    if (!target) {
+        void* buf = c->d_rgb;
+        rc = ensure_device_buffer(c, &buf, &c->rgb_cap, bytes);
+        c->d_rgb = (uint8_t*)buf;
+        if (rc) return rc;
+    }
+    rr_pixel_outcome* d_out = nullptr;
+    const size_t obytes = (size_t)width * height * sizeof(rr_pixel_outcome);
+    if (out) {
+        if ((rc = ensure_device_buffer(c, &c->d_out, &c->out_cap, obytes))) return rc;
+        d_out = static_cast<rr_pixel_outcome*>(c->d_out);
+    }
+    rc = render_device_locked(c, cam, integ, width, height, target ? target : c->d_rgb, d_out,
+                              nullptr, c->stream, t0);
     if (rc) return rc;
-    std::lock_guard<std::mutex> lk(c->mu);
-    if (!target)
-        RR_CUDA(c, cudaMemcpyAsync(rgb_out, c->d_rgb, (size_t)3 * width * height,
-                                   cudaMemcpyDeviceToHost, c->stream));
+    if (!target && rgb_out)
+        RR_CUDA(c, cudaMemcpyAsync(rgb_out, c->d_rgb, bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (out) RR_CUDA(c, cudaMemcpyAsync(out, d_out, obytes, cudaMemcpyDeviceToHost, c->stream));
     rc = collect_stats(c, c->stream, stats, t0);   // synchronises the stream
     if (rc == RR_OK && stats) stats->rays = (int64_t)width * height;
     return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rr_render_device(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                     int height, uint8_t* d_rgb, rr_stats* stats, void* stream) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    return render_device_locked(c, cam, integ, width, height, d_rgb, nullptr, stats,
+                                stream ? (cudaStream_t)stream : c->stream, now_s());
+}
+
+int rr_render(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width, int height,
+              uint8_t* rgb_out, rr_stats* stats) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);   // the whole call: buffers, launch, copy, stats
+    return render_host_locked(c, cam, integ, width, height, rgb_out, nullptr, stats);
+}
+
+int rr_render_outcomes(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ, int width,
+                       int height, uint8_t* rgb_out, rr_pixel_outcome* out, rr_stats* stats) {
+    if (!c) return RR_ERR_CONFIG;
+    if (!out) return set_err(c, RR_ERR_CONFIG, "outcomes: required");
+    std::lock_guard<std::mutex> lk(c->mu);
+    return render_host_locked(c, cam, integ, width, height, rgb_out, out, stats);
 }
 
 int rr_shard_tile_count(int width, int height, int tile_w, int tile_h, int shard, int n_shards) {

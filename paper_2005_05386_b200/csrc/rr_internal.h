@@ -16,6 +16,19 @@ namespace rr {
 cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t stream,
                          int num_sms, const char** kernel_name, int* launches = nullptr);
 
+// Per-family march launchers (one translation unit each, see rr_march.cuh);
+// launch_march dispatches on P.kind.
+cudaError_t launch_family_pair(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                               const char** name);
+cudaError_t launch_family_bumps(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                const char** name);
+cudaError_t launch_family_diffeo(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                 const char** name);
+cudaError_t launch_family_euclid(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                 const char** name);
+cudaError_t launch_family_graph(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                const char** name);
+
 // Builds the culling grid (bump masks + Chebyshev distances) on the device:
 // d_gauss holds n records {cx, cy, cz, sigma_x, sigma_y, sigma_z, slot, pad}.
 // scratch needs 2*G^3 uint16.  4 launches on `s`.

@@ -1,2105 +1,12 @@
-// rr_kernels.cu — sm_100a kernels of the B200 geodesic tracer.
-//
-// K1 raygen (fused prologue)  <- pixel_direction   src/render/camera.cpp:22-29
-// K2 march                    <- march_group       include/rray/render/detail/kernel_impl.hpp:22-94
-//                                + flow_step_t     include/rray/geodesics/integrate.hpp:46-99
-//                                + christoffel_eval include/rray/metrics/metric.hpp:69-105
-//                                + intersect_segment src/render/scene.cpp:15-109
-// K3 shade (fused epilogue)   <- shade             src/render/render.cpp:14-25
-// K6 detile                   <- (none: the reference is single-process)
-// See rr_device.cuh for the math and DESIGN.md for the roofline.
-#include <cuda_runtime.h>
-
-#include <cstdint>
-#include <mutex>
-
-#include "rr_device.cuh"
-#include "rr_internal.h"
+// rr_kernels.cu — launch dispatch and the small kernels of the B200 geodesic
+// tracer (sm_100a): culling-grid build, detile, FFMA probe, geodesic export
+// (trace) and flow_accel points.  The march kernels are instantiated per
+// metric family in rr_k_pair.cu (ray-pair Gaussian-bump RK4), rr_k_bumps.cu,
+// rr_k_diffeo.cu and rr_k_flat.cu (Euclidean + general graph fields).
+#include "rr_march.cuh"
 
 namespace rr {
 namespace {
-
-constexpr unsigned kFull = 0xffffffffu;
-constexpr int kThreads = 128;   // 4 warps per CTA
-#ifndef RR_FAST_SINCOS
-#define RR_FAST_SINCOS 1
-#endif
-#ifndef RR_GROUP_TESTS
-#define RR_GROUP_TESTS 1
-#endif
-#ifndef RR_RAY_PAIRS
-// 1: Gaussian-bump frames march two rays per thread with packed FP32
-// (march2_kernel); 0: one ray per thread (march_kernel) for every scene.
-#define RR_RAY_PAIRS 1
-#endif
-#ifndef RR_X2_FUSED
-// ray-pair frames with lights: 1 = one launch (primary units, then
-// (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
-#define RR_X2_FUSED 1
-#endif
-#ifndef RR_X2_RK4_UNROLL
-#define RR_X2_RK4_UNROLL 1   // 4 RK4 stages unrolled (4 small bump loops): C3 10.32 -> 9.91 ms, lights 16.94 -> 16.66
-#endif
-#ifndef RR_MIN_BLOCKS_X2
-// ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
-// and unrolled RK4 stages, 6 CTAs (80 registers, 132 B of spills) beat 7
-// (72 registers, 208 B of spills in the per-step code) on the unlit frame,
-// 9.39 vs 9.63 ms; the fused lit launch keeps 7 (16.16 vs 16.35 ms)
-// (profiles/r1i_shadow_frame.md).  The 4-slot variant (C1) uses 6.
-#define RR_MIN_BLOCKS_X2 6
-#endif
-#ifndef RR_MIN_BLOCKS_X2_FUSED
-#define RR_MIN_BLOCKS_X2_FUSED 7
-#endif
-#ifndef RR_MIN_BLOCKS_X2_SMALL
-#define RR_MIN_BLOCKS_X2_SMALL 6
-#endif
-#ifndef RR_MIN_BLOCKS_RK23
-#define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
-#endif
-#ifndef RR_MIN_BLOCKS
-#define RR_MIN_BLOCKS 7   // <= 72 registers: 7 CTAs = 28 warps per SM (measured best)
-#endif
-#ifndef RR_MIN_BLOCKS_MESH
-// mesh variants (BVH stack + free-distance ball): 6 CTAs, C4 twist + mesh
-// 12.85 vs 13.2-13.4 ms at 7, 13.1-13.2 at 5, 14.4-14.7 at 8; bend neutral
-// (profiles/r1k_minblocks_ab.log); the mesh-free twist stays at 7 (8.09 vs
-// 8.32 ms at 6, profiles/r1l_minblocks_nomesh_ab.log)
-#define RR_MIN_BLOCKS_MESH 6
-#endif
-
-struct F3 {
-    float x, y, z;
-};
-
-__device__ __forceinline__ F3 f3(float x, float y, float z) { return F3{x, y, z}; }
-
-__device__ __forceinline__ float ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float sqrt_approx(float x) {
-    float y;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// ---------------------------------------------------------------------------
-// Graph metric, Gaussian bumps only (factored form, rr_device.cuh header).
-// `um` is warp-uniform: bit j set <=> bump slot j is evaluated by the whole
-// warp this step.  Slot tests cost 2 issue slots each, so NB is the smallest
-// of 4/8/16/32 holding the field (a sign-split slot layout was measured
-// slower: it doubles the slots tested per evaluation).
-template <int NB>
-__device__ __forceinline__ F3 accel_bumps(const DevParams& P, uint32_t um, F3 p, F3 y) {
-    float Gx = 0.f, Gy = 0.f, Gz = 0.f, Q1 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f;
-#pragma unroll
-    for (int g = 0; g < NB; g += 4) {
-#if RR_GROUP_TESTS
-        // slots are sorted by centre x on the host, so a ray's active bumps
-        // cluster and whole groups of 4 are skipped with one test
-        if (!((um >> g) & 0xFu)) continue;
-#endif
-#pragma unroll
-        for (int j = g; j < g + 4; ++j) {
-            if (um & (1u << j)) {
-                const DevBump& b = P.bumps[j];
-                const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
-                const float gx = dx * b.kx, gy = dy * b.ky, gz = dz * b.kz;
-                const float q = fmaf(dx, gx, fmaf(dy, gy, fmaf(dz, gz, b.la)));
-                const float v = ex2(q) * b.sgn;
-                Gx = fmaf(v, gx, Gx);
-                Gy = fmaf(v, gy, Gy);
-                Gz = fmaf(v, gz, Gz);
-                const float t = fmaf(y.x, gx, fmaf(y.y, gy, y.z * gz));
-                Q1 = fmaf(v * t, t, Q1);
-                Sx = fmaf(v, b.kx, Sx);
-                Sy = fmaf(v, b.ky, Sy);
-                Sz = fmaf(v, b.kz, Sz);
-            }
-        }
-    }
-    // G = beta G';  Q = beta^2 Q1 - beta (Y . S');  a = (Q / (1 + |G|^2)) G
-    const float ys = fmaf(y.x * y.x, Sx, fmaf(y.y * y.y, Sy, y.z * y.z * Sz));
-    const float Q = fmaf(kBeta * kBeta, Q1, -kBeta * ys);
-    const float w = fmaf(kBeta * kBeta, fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)), 1.f);
-    const float r = Q * rcp_approx(w) * kBeta;
-    return f3(r * Gx, r * Gy, r * Gz);
-}
-
-// ---------------------------------------------------------------------------
-// Ray pairs (packed FP32: FADD2 / FMUL2 / FFMA2).  The march is bound by
-// issue slots; a thread that carries TWO rays evaluates every per-ray
-// operation of both with one packed instruction, with the per-bump constants
-// as broadcast 64-bit uniform operands (DevBumpB).  Measured on the bump body
-// alone (tools/microbench/bump_body.cu, profiles/r1g_raypair.md): 0.88 vs
-// 1.10-1.15 ps per ray-bump at 8 active bumps.  (Pairing two bump SLOTS of one
-// ray instead was measured slower: profiles/r1e_ffma2.md.)
-typedef unsigned long long u64;
-struct F2 {           // (ray 0, ray 1)
-    u64 v;
-};
-__device__ __forceinline__ F2 mk2(float a, float b) {
-    F2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ F2 bc2(float a) { return mk2(a, a); }
-__device__ __forceinline__ float lo2(F2 x) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
-    return a;
-}
-__device__ __forceinline__ float hi2(F2 x) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
-    return b;
-}
-__device__ __forceinline__ float get2(F2 x, int r) { return r ? hi2(x) : lo2(x); }
-__device__ __forceinline__ F2 add2(F2 a, F2 b) {
-    F2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
-    F2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
-    F2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
-// c - a*b as ONE FFMA2 with a negated operand (ptxas folds the pair; f32x2
-// has no neg in PTX, and an xor would cost two ALU ops)
-__device__ __forceinline__ F2 fnma2(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("{\n\t.reg .b64 t;\n\tmul.rn.f32x2 t, %1, %2;\n\tsub.rn.f32x2 %0, %3, t;\n\t}"
-        : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
-__device__ __forceinline__ F2 ld2(const float2& f) { return F2{*reinterpret_cast<const u64*>(&f)}; }
-// select per ray: r0 ? a.lo : b.lo, r1 ? a.hi : b.hi
-__device__ __forceinline__ F2 sel2(bool r0, bool r1, F2 a, F2 b) {
-    return mk2(r0 ? lo2(a) : lo2(b), r1 ? hi2(a) : hi2(b));
-}
-
-struct P3 {           // a 3-vector for a ray pair
-    F2 x, y, z;
-};
-__device__ __forceinline__ F3 ray_of(const P3& v, int r) { return f3(get2(v.x, r), get2(v.y, r), get2(v.z, r)); }
-__device__ __forceinline__ P3 pair_of(F3 a, F3 b) { return P3{mk2(a.x, b.x), mk2(a.y, b.y), mk2(a.z, b.z)}; }
-
-// accel_bumps for a ray pair (same factored form) over the warp-uniform mask
-// of the 64 rays: a uniform-datapath loop over the active slots, positive
-// amplitudes first, then negative ones with the sign folded into the
-// accumulating FFMA2s (negated operand).  Measured alternatives (unrolled
-// slot tests, pairs/groups of slots per test, the sign as an XOR, G = p.S - T,
-// compact or shared-memory slots): profiles/r1g_raypair.md, r1i_shadow_frame.md.
-template <int NB>
-__device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, const P3& p, const P3& y) {
-    F2 Gx = bc2(0.f), Gy = bc2(0.f), Gz = bc2(0.f), Q1 = bc2(0.f);
-    F2 Sx = bc2(0.f), Sy = bc2(0.f), Sz = bc2(0.f);
-    auto body = [&](const DevBumpB& b, bool neg) {
-        const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
-        const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
-        const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
-        const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
-        const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
-        const F2 et = mul2(e, t);
-        if (neg) {
-            Gx = fnma2(e, gx, Gx);
-            Gy = fnma2(e, gy, Gy);
-            Gz = fnma2(e, gz, Gz);
-            Q1 = fnma2(et, t, Q1);
-            Sx = fnma2(e, ld2(b.kx), Sx);
-            Sy = fnma2(e, ld2(b.ky), Sy);
-            Sz = fnma2(e, ld2(b.kz), Sz);
-        } else {
-            Gx = fma2(e, gx, Gx);
-            Gy = fma2(e, gy, Gy);
-            Gz = fma2(e, gz, Gz);
-            Q1 = fma2(et, t, Q1);
-            Sx = fma2(e, ld2(b.kx), Sx);
-            Sy = fma2(e, ld2(b.ky), Sy);
-            Sz = fma2(e, ld2(b.kz), Sz);
-        }
-    };
-    uint32_t m = um & ~P.neg_mask;
-#pragma unroll 1
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1u;
-        body(P.bumpsb[j], false);
-    }
-    m = um & P.neg_mask;
-#pragma unroll 1
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1u;
-        body(P.bumpsb[j], true);
-    }
-    const F2 ys = fma2(mul2(y.x, y.x), Sx, fma2(mul2(y.y, y.y), Sy, mul2(mul2(y.z, y.z), Sz)));
-    const F2 Q = fma2(bc2(kBeta * kBeta), Q1, mul2(bc2(-kBeta), ys));
-    const F2 w = fma2(bc2(kBeta * kBeta), fma2(Gx, Gx, fma2(Gy, Gy, mul2(Gz, Gz))), bc2(1.f));
-    const F2 r = mul2(mul2(Q, mk2(rcp_approx(lo2(w)), rcp_approx(hi2(w)))), bc2(kBeta));
-    return P3{mul2(r, Gx), mul2(r, Gy), mul2(r, Gz)};
-}
-
-// ---------------------------------------------------------------------------
-// Graph metric, general field: any number of bumps (<= kMaxBumps) plus
-// polynomial terms (scalar_field.hpp:128-161); full gradient + Hessian.
-__device__ __forceinline__ F3 accel_graph_general(const DevParams& P, F3 p, F3 y) {
-    float fx = 0.f, fy = 0.f, fz = 0.f;                               // grad f
-    float hxx = 0.f, hxy = 0.f, hxz = 0.f, hyy = 0.f, hyz = 0.f, hzz = 0.f;
-    for (int j = 0; j < P.n_bumps; ++j) {
-        const DevBump& b = P.bumps[j];
-        const float dx = p.x - b.cx, dy = p.y - b.cy, dz = p.z - b.cz;
-        const float gx = dx * b.kx * kBeta, gy = dy * b.ky * kBeta, gz = dz * b.kz * kBeta;
-        const float v = ex2(fmaf(dx * b.kx, dx, fmaf(dy * b.ky, dy, fmaf(dz * b.kz, dz, b.la)))) * b.sgn;
-        fx = fmaf(-v, gx, fx);
-        fy = fmaf(-v, gy, fy);
-        fz = fmaf(-v, gz, fz);
-        hxx = fmaf(v, fmaf(gx, gx, -b.kx * kBeta), hxx);
-        hyy = fmaf(v, fmaf(gy, gy, -b.ky * kBeta), hyy);
-        hzz = fmaf(v, fmaf(gz, gz, -b.kz * kBeta), hzz);
-        hxy = fmaf(v, gx * gy, hxy);
-        hxz = fmaf(v, gx * gz, hxz);
-        hyz = fmaf(v, gy * gz, hyz);
-    }
-    if (P.n_poly > 0) {
-        float xp[5], yp[5], zp[5];
-        xp[0] = yp[0] = zp[0] = 1.f;
-#pragma unroll
-        for (int k = 1; k < 5; ++k) {
-            xp[k] = xp[k - 1] * p.x;
-            yp[k] = yp[k - 1] * p.y;
-            zp[k] = zp[k - 1] * p.z;
-        }
-        for (int i = 0; i < P.n_poly; ++i) {
-            const DevPoly& t = P.poly[i];
-            const int a = t.a, b = t.b, c = t.c;
-            const float xa = xp[a], yb = yp[b], zc = zp[c];
-            const float xa1 = a > 0 ? xp[a - 1] : 0.f, yb1 = b > 0 ? yp[b - 1] : 0.f;
-            const float zc1 = c > 0 ? zp[c - 1] : 0.f;
-            const float xa2 = a > 1 ? xp[a - 2] : 0.f, yb2 = b > 1 ? yp[b - 2] : 0.f;
-            const float zc2 = c > 1 ? zp[c - 2] : 0.f;
-            fx = fmaf(t.coef * a, xa1 * yb * zc, fx);
-            fy = fmaf(t.coef * b, xa * yb1 * zc, fy);
-            fz = fmaf(t.coef * c, xa * yb * zc1, fz);
-            hxx = fmaf(t.coef * (a * (a - 1)), xa2 * yb * zc, hxx);
-            hyy = fmaf(t.coef * (b * (b - 1)), xa * yb2 * zc, hyy);
-            hzz = fmaf(t.coef * (c * (c - 1)), xa * yb * zc2, hzz);
-            hxy = fmaf(t.coef * (a * b), xa1 * yb1 * zc, hxy);
-            hxz = fmaf(t.coef * (a * c), xa1 * yb * zc1, hxz);
-            hyz = fmaf(t.coef * (b * c), xa * yb1 * zc1, hyz);
-        }
-    }
-    // Q = y^T H y;  a = -(Q / (1 + |grad f|^2)) grad f   (metric.hpp:74-83)
-    const float Q = hxx * y.x * y.x + hyy * y.y * y.y + hzz * y.z * y.z +
-                    2.f * (hxy * y.x * y.y + hxz * y.x * y.z + hyz * y.y * y.z);
-    const float w = 1.f + fx * fx + fy * fy + fz * fz;
-    const float r = -Q * rcp_approx(w);
-    return f3(r * fx, r * fy, r * fz);
-}
-
-// ---------------------------------------------------------------------------
-// Diffeo pull-back metric: directional jet folded innermost-first.
-__device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float& valid) {
-    if (P.n_stages == 1 && P.stages[0].kind == kStageTwist) {
-        // Single twist (C4): J = [[R, b], [0, 1]] with R the rotation by z, so
-        // J^-1 q = [R^T (q_xy - q_z b); q_z] and q_z = 0 for the twist:
-        // a = -R^T (d0, d1) / det — the general fold below, specialised.
-        // Expanding R^T (d0, d1) with cs^2 + sn^2 = det = 1 (diffeo.hpp:165-171)
-        // the rotation cancels: a = (z'(2y' + z'x), z'(z'y - 2x'), 0), the
-        // rotating-frame Coriolis + centrifugal terms.  No sincos, no
-        // reciprocal; |det J| = 1 so the validity bound is unchanged.
-        valid = fminf(valid, 1.f);
-        return f3(y.z * fmaf(y.z, p.x, 2.f * y.y), y.z * fmaf(y.z, p.y, -2.f * y.x), 0.f);
-    }
-    float x0 = p.x, x1 = p.y, x2 = p.z;          // current point
-    float w0 = y.x, w1 = y.y, w2 = y.z;          // J_inner y
-    float q0 = 0.f, q1 = 0.f, q2 = 0.f;          // D^2 Phi_inner[y, y]
-    float J[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
-    float vmin = 3.0e38f, dprod = 1.f;
-    for (int s = 0; s < P.n_stages; ++s) {
-        const DevStage& st = P.stages[s];
-        float det;
-        if (st.kind == kStageAffine) {                       // diffeo.hpp:133-141
-            const float* m = st.v;
-            const float n0 = m[0] * x0 + m[1] * x1 + m[2] * x2 + m[9];
-            const float n1 = m[3] * x0 + m[4] * x1 + m[5] * x2 + m[10];
-            const float n2 = m[6] * x0 + m[7] * x1 + m[8] * x2 + m[11];
-            const float a0 = m[0] * q0 + m[1] * q1 + m[2] * q2;
-            const float a1 = m[3] * q0 + m[4] * q1 + m[5] * q2;
-            const float a2 = m[6] * q0 + m[7] * q1 + m[8] * q2;
-            q0 = a0; q1 = a1; q2 = a2;
-            const float b0 = m[0] * w0 + m[1] * w1 + m[2] * w2;
-            const float b1 = m[3] * w0 + m[4] * w1 + m[5] * w2;
-            const float b2 = m[6] * w0 + m[7] * w1 + m[8] * w2;
-            w0 = b0; w1 = b1; w2 = b2;
-            float R[9];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                R[c] = m[0] * J[c] + m[1] * J[3 + c] + m[2] * J[6 + c];
-                R[3 + c] = m[3] * J[c] + m[4] * J[3 + c] + m[5] * J[6 + c];
-                R[6 + c] = m[6] * J[c] + m[7] * J[3 + c] + m[8] * J[6 + c];
-            }
-#pragma unroll
-            for (int k = 0; k < 9; ++k) J[k] = R[k];
-            x0 = n0; x1 = n1; x2 = n2;
-            det = st.det;
-        } else if (st.kind == kStageTwist) {                 // diffeo.hpp:143-173
-            float sn, cs;
-#if RR_FAST_SINCOS
-            __sincosf(x2, &sn, &cs);   // MUFU.SIN/COS: |z| <= ~10 in chart units
-#else
-            sincosf(x2, &sn, &cs);
-#endif
-            const float j02 = -(x0 * sn) - x1 * cs;          // d(image_0)/dz
-            const float j12 = x0 * cs - x1 * sn;             // d(image_1)/dz
-            // w^T H[0] w and w^T H[1] w (H[2] = 0)
-            const float d0 = -w2 * (2.f * (w0 * sn + w1 * cs) + w2 * j12);
-            const float d1 = w2 * (2.f * (w0 * cs - w1 * sn) + w2 * j02);
-            const float a0 = d0 + cs * q0 - sn * q1 + j02 * q2;
-            const float a1 = d1 + sn * q0 + cs * q1 + j12 * q2;
-            q0 = a0; q1 = a1;
-            const float b0 = cs * w0 - sn * w1 + j02 * w2;
-            const float b1 = sn * w0 + cs * w1 + j12 * w2;
-            w0 = b0; w1 = b1;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float r0 = cs * J[c] - sn * J[3 + c] + j02 * J[6 + c];
-                const float r1 = sn * J[c] + cs * J[3 + c] + j12 * J[6 + c];
-                J[c] = r0;
-                J[3 + c] = r1;
-            }
-            x0 = j12;                                         // x c - y s
-            x1 = -j02;                                        // x s + y c
-            det = cs * cs + sn * sn;
-        } else if (st.kind == kStageBend) {                   // EXTENSION (oracle/rro.c)
-            const float k = st.v[0], c = st.v[1];
-            float sn, cs;
-            __sincosf(k * x0, &sn, &cs);
-            const float yc = x1 - c;
-            const float j00 = -k * cs * yc, j10 = -k * sn * yc;   // j01 = -sn, j11 = cs
-            const float wxx = w0 * w0, wxy = 2.f * w0 * w1;
-            const float d0 = wxx * (k * k * sn * yc) - wxy * (k * cs);
-            const float d1 = -wxx * (k * k * cs * yc) - wxy * (k * sn);
-            const float a0 = d0 + j00 * q0 - sn * q1;
-            const float a1 = d1 + j10 * q0 + cs * q1;
-            q0 = a0; q1 = a1;
-            const float b0 = j00 * w0 - sn * w1;
-            const float b1 = j10 * w0 + cs * w1;
-            w0 = b0; w1 = b1;
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                const float r0 = j00 * J[cc] - sn * J[3 + cc];
-                const float r1 = j10 * J[cc] + cs * J[3 + cc];
-                J[cc] = r0;
-                J[3 + cc] = r1;
-            }
-            x0 = -sn * yc;
-            x1 = fmaf(cs, yc, c);
-            det = -k * yc;
-        } else {                                              // diffeo.hpp:175-193
-            const float* b = st.v;
-            const float ux = (x0 - b[0]) * b[3], uy = (x1 - b[1]) * b[4], uz = (x2 - b[2]) * b[5];
-            const float e = b[6] * __expf(-0.5f * (ux * ux + uy * uy + uz * uz));
-            const float gx = ux * b[3], gy = uy * b[4], gz = uz * b[5];   // grad f = -e g
-            const float wg = w0 * gx + w1 * gy + w2 * gz;
-            const float ws = w0 * w0 * b[3] * b[3] + w1 * w1 * b[4] * b[4] + w2 * w2 * b[5] * b[5];
-            const float whw = e * (wg * wg - ws);                           // w^T Hess f w
-            const float fq = -e * (gx * q0 + gy * q1 + gz * q2);          // grad f . q
-            const float fw = -e * wg;                                       // grad f . w
-            q0 = fmaf(b[7], whw + fq, q0);
-            q1 = fmaf(b[8], whw + fq, q1);
-            q2 = fmaf(b[9], whw + fq, q2);
-            w0 = fmaf(b[7], fw, w0);
-            w1 = fmaf(b[8], fw, w1);
-            w2 = fmaf(b[9], fw, w2);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float r = -e * (gx * J[c] + gy * J[3 + c] + gz * J[6 + c]);
-                J[c] = fmaf(b[7], r, J[c]);
-                J[3 + c] = fmaf(b[8], r, J[3 + c]);
-                J[6 + c] = fmaf(b[9], r, J[6 + c]);
-            }
-            x0 = fmaf(e, b[7], x0);
-            x1 = fmaf(e, b[8], x1);
-            x2 = fmaf(e, b[9], x2);
-            det = 1.f - e * (b[7] * gx + b[8] * gy + b[9] * gz);
-        }
-        vmin = fminf(vmin, fabsf(det));
-        dprod *= det;
-        vmin = fminf(vmin, fabsf(dprod));
-    }
-    // a = -J^-1 q via the adjugate (linalg.hpp:223-236)
-    const float c00 = J[4] * J[8] - J[5] * J[7];
-    const float c01 = J[2] * J[7] - J[1] * J[8];
-    const float c02 = J[1] * J[5] - J[2] * J[4];
-    const float c10 = J[5] * J[6] - J[3] * J[8];
-    const float c11 = J[0] * J[8] - J[2] * J[6];
-    const float c12 = J[2] * J[3] - J[0] * J[5];
-    const float c20 = J[3] * J[7] - J[4] * J[6];
-    const float c21 = J[1] * J[6] - J[0] * J[7];
-    const float c22 = J[0] * J[4] - J[1] * J[3];
-    const float d = J[0] * c00 + J[1] * c10 + J[2] * c20;
-    valid = fminf(valid, fminf(vmin, fabsf(d)));
-    const float id = -rcp_approx(d);
-    return f3(id * (c00 * q0 + c01 * q1 + c02 * q2), id * (c10 * q0 + c11 * q1 + c12 * q2),
-              id * (c20 * q0 + c21 * q1 + c22 * q2));
-}
-
-template <int KIND, int NB>
-__device__ __forceinline__ F3 accel(const DevParams& P, uint32_t um, F3 p, F3 y, float& valid) {
-    if constexpr (KIND == kEuclid) {
-        return f3(0.f, 0.f, 0.f);
-    } else if constexpr (KIND == kBumps) {
-        return accel_bumps<NB>(P, um, p, y);
-    } else if constexpr (KIND == kGraphGeneral) {
-        return accel_graph_general(P, p, y);
-    } else {
-        return accel_diffeo(P, p, y, valid);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Chord-vs-primitive intersection (scene.cpp:15-109), FP32.
-__device__ __forceinline__ bool slab(float a, float d, float lo, float hi, float& smin, float& smax) {
-    if (d == 0.f) return !(a < lo || a > hi);
-    float s1 = (lo - a) / d;
-    float s2 = (hi - a) / d;
-    if (s1 > s2) {
-        const float t = s1;
-        s1 = s2;
-        s2 = t;
-    }
-    smin = fmaxf(smin, s1);
-    smax = fminf(smax, s2);
-    return !(smin > smax);
-}
-
-// chord_box_entry (scene.cpp:15-34) for a box given per axis.
-__device__ __forceinline__ bool chord_box_entry(F3 a, F3 d, F3 lo, F3 hi, float& s_out) {
-    float smin = 0.f, smax = 1.f;
-    if (!slab(a.x, d.x, lo.x, hi.x, smin, smax)) return false;
-    if (!slab(a.y, d.y, lo.y, hi.y, smin, smax)) return false;
-    if (!slab(a.z, d.z, lo.z, hi.z, smin, smax)) return false;
-    s_out = smin;
-    return true;
-}
-
-__device__ __forceinline__ float comp(F3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
-__device__ __forceinline__ void set_comp(F3& v, int i, float x) {
-    if (i == 0) v.x = x;
-    else if (i == 1) v.y = x;
-    else v.z = x;
-}
-
-// hit_grid (scene.cpp:36-54): slabs around x_dim = k*spacing clipped to bounds.
-template <int DIM>
-__device__ __forceinline__ void hit_grid_dim(const DevGrid& g, F3 a, F3 b, F3 d, bool& have,
-                                             float& best) {
-    const float ad = comp(a, DIM), bd = comp(b, DIM);
-    const float clo = fminf(ad, bd), chi = fmaxf(ad, bd);
-    const int kmin = (int)ceilf((clo - g.hw) / g.spacing);
-    const int kmax = (int)floorf((chi + g.hw) / g.spacing);
-    for (int k = kmin; k <= kmax; ++k) {
-        F3 lo = f3(g.lo[0], g.lo[1], g.lo[2]), hi = f3(g.hi[0], g.hi[1], g.hi[2]);
-        const float plane = (float)k * g.spacing;
-        set_comp(lo, DIM, fmaxf(comp(lo, DIM), plane - g.hw));
-        set_comp(hi, DIM, fminf(comp(hi, DIM), plane + g.hw));
-        if (comp(lo, DIM) > comp(hi, DIM)) continue;
-        float s;
-        if (chord_box_entry(a, d, lo, hi, s) && (!have || s < best)) {
-            best = s;
-            have = true;
-        }
-    }
-}
-
-__device__ __forceinline__ bool hit_grid(const DevGrid& g, F3 a, F3 b, F3 d, float& s_out) {
-    bool have = false;
-    float best = 0.f;
-    hit_grid_dim<0>(g, a, b, d, have, best);
-    hit_grid_dim<1>(g, a, b, d, have, best);
-    hit_grid_dim<2>(g, a, b, d, have, best);
-    s_out = best;
-    return have;
-}
-
-// hit_sphere (scene.cpp:56-71) with a conservative early-out: a chord of
-// length L starting outside cannot reach the sphere when |oc| > r + L, i.e.
-// c = |oc|^2 - r^2 > (2r + L) L.
-__device__ __forceinline__ bool hit_sphere(const DevSphere& sp, F3 a, F3 d, float qa, float len,
-                                           float& s_out) {
-    const float ox = a.x - sp.c[0], oy = a.y - sp.c[1], oz = a.z - sp.c[2];
-    const float c = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -sp.r2)));
-    if (c <= 0.f) {
-        s_out = 0.f;
-        return true;
-    }
-    if (fmaf(-len, sp.two_r + len, c) > 0.f) return false;
-    const float qb = 2.f * (ox * d.x + oy * d.y + oz * d.z);
-    if (qb >= 0.f) return false;
-    const float disc = qb * qb - 4.f * qa * c;
-    if (disc < 0.f) return false;
-    const float q = 0.5f * (sqrtf(disc) - qb);
-    const float s = c / q;
-    if (s > 1.f) return false;
-    s_out = s;
-    return true;
-}
-
-__device__ __forceinline__ bool hit_half_space(const DevHalf& hs, F3 a, F3 d, float& s_out) {
-    const float e0 = hs.n[0] * a.x + hs.n[1] * a.y + hs.n[2] * a.z - hs.off;
-    if (e0 <= 0.f) {
-        s_out = 0.f;
-        return true;
-    }
-    const float de = hs.n[0] * d.x + hs.n[1] * d.y + hs.n[2] * d.z;
-    if (de >= 0.f) return false;
-    const float s = -e0 / de;
-    if (s > 1.f) return false;
-    s_out = s;
-    return true;
-}
-
-// ---------------------------------------------------------------------------
-// EXTENSION: triangle meshes.  The chord [a, b] of a step is tested against a
-// BVH (slab test per node, Moller-Trumbore per triangle, ties keep the lower
-// original triangle index: oracle/rro.c hit_mesh).  Each lane also keeps a
-// "free distance": the distance from a query point to the nearest leaf box;
-// while the marched path stays inside that ball (sum of chord lengths) no
-// mesh test is needed.  Both are __noinline__ so scenes without meshes keep
-// the march loop's register allocation.
-__device__ __noinline__ bool mesh_chord(const DevMesh& M, F3 a, F3 d, float& best_s, int& best_rec) {
-    const float ix = d.x != 0.f ? 1.f / d.x : 3.0e38f;
-    const float iy = d.y != 0.f ? 1.f / d.y : 3.0e38f;
-    const float iz = d.z != 0.f ? 1.f / d.z : 3.0e38f;
-    bool have = false;
-    float best = 1.f;
-    int best_t = 0x7fffffff;
-    int stack[64];
-    int sp = 0, node = 0;
-    for (;;) {
-        const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
-        float t0 = 0.f, t1 = best;
-        {
-            float u = (n0.x - a.x) * ix, w = (n1.x - a.x) * ix;
-            t0 = fmaxf(t0, fminf(u, w));
-            t1 = fminf(t1, fmaxf(u, w));
-            u = (n0.y - a.y) * iy;
-            w = (n1.y - a.y) * iy;
-            t0 = fmaxf(t0, fminf(u, w));
-            t1 = fminf(t1, fmaxf(u, w));
-            u = (n0.z - a.z) * iz;
-            w = (n1.z - a.z) * iz;
-            t0 = fmaxf(t0, fminf(u, w));
-            t1 = fminf(t1, fmaxf(u, w));
-        }
-        // a zero chord component makes u, w +-inf or NaN: fall back to the
-        // containment test on that axis
-        bool overlap = t0 <= t1;
-        if (d.x == 0.f) overlap = overlap && a.x >= n0.x && a.x <= n1.x;
-        if (d.y == 0.f) overlap = overlap && a.y >= n0.y && a.y <= n1.y;
-        if (d.z == 0.f) overlap = overlap && a.z >= n0.z && a.z <= n1.z;
-        if (overlap) {
-            const int first = __float_as_int(n0.w), cnt = __float_as_int(n1.w);
-            if (cnt > 0) {
-                for (int i = first; i < first + cnt; ++i) {
-                    const float4 r0 = __ldg(M.tris + 3 * i), r1 = __ldg(M.tris + 3 * i + 1),
-                                 r2 = __ldg(M.tris + 3 * i + 2);
-                    const F3 e1 = f3(r1.x, r1.y, r1.z), e2 = f3(r2.x, r2.y, r2.z);
-                    const F3 pv = f3(d.y * e2.z - d.z * e2.y, d.z * e2.x - d.x * e2.z, d.x * e2.y - d.y * e2.x);
-                    const float det = e1.x * pv.x + e1.y * pv.y + e1.z * pv.z;
-                    if (det == 0.f) continue;
-                    const float inv = 1.f / det;
-                    const F3 tv = f3(a.x - r0.x, a.y - r0.y, a.z - r0.z);
-                    const float u = (tv.x * pv.x + tv.y * pv.y + tv.z * pv.z) * inv;
-                    if (u < 0.f || u > 1.f) continue;
-                    const F3 qv = f3(tv.y * e1.z - tv.z * e1.y, tv.z * e1.x - tv.x * e1.z, tv.x * e1.y - tv.y * e1.x);
-                    const float v = (d.x * qv.x + d.y * qv.y + d.z * qv.z) * inv;
-                    if (v < 0.f || u + v > 1.f) continue;
-                    const float s = (e2.x * qv.x + e2.y * qv.y + e2.z * qv.z) * inv;
-                    if (s < 0.f || s > 1.f) continue;
-                    const int t = __float_as_int(r0.w);
-                    if (!have || s < best || (s == best && t < best_t)) {
-                        best = s;
-                        best_t = t;
-                        best_rec = i;
-                        have = true;
-                    }
-                }
-            } else if (sp < 63) {
-                stack[sp++] = first;      // right child
-                node = node + 1;          // left child
-                continue;
-            }
-        }
-        if (sp == 0) break;
-        node = stack[--sp];
-    }
-    if (have) best_s = best;
-    return have;
-}
-
-__device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
-    const float dx = fmaxf(fmaxf(n0.x - p.x, p.x - n1.x), 0.f);
-    const float dy = fmaxf(fmaxf(n0.y - p.y, p.y - n1.y), 0.f);
-    const float dz = fmaxf(fmaxf(n0.z - p.z, p.z - n1.z), 0.f);
-    return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-}
-
-// Distance from p to the nearest leaf box (capped): no triangle lies closer.
-// Nearest-child-first descent so the bound tightens early.
-#ifndef RR_DIFFEO_RK4_UNROLL
-#define RR_DIFFEO_RK4_UNROLL 0   // general diffeo chains: 1 = RK4 stages unrolled (4 copies of the fold);
-                                 // rolled is faster (I-cache: bend 58.0 -> 50.5 ms, profiles/r1k_unroll_ab.log)
-#endif
-#ifndef RR_TWIST_RK4
-#define RR_TWIST_RK4 1     // z-free RK4 for a single-twist metric (march_fixed)
-#endif
-#ifndef RR_MESH_FREE_CAP
-#define RR_MESH_FREE_CAP 0.5f   // re-measured with rolled diffeo stages + 6 CTAs/SM (profiles/r1k_freecap_ab.log):
-                                // caps 0.25 / 0.5 / 1 / 2: C4 twist 13.0 / 12.8 / 13.3 / 14.2 ms, twist+bend 50.7 / 50.5 / 51.1 / 51.5 ms
-#endif
-__device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
-    float best2 = cap * cap;
-    int stack[48];
-    float sd[48];
-    int sp = 0, node = 0;
-    float nd2 = box_dist2(__ldg(M.nodes), __ldg(M.nodes + 1), p);
-    for (;;) {
-        if (nd2 < best2) {
-            const float4 n0 = __ldg(M.nodes + 2 * node), n1 = __ldg(M.nodes + 2 * node + 1);
-            if (__float_as_int(n1.w) > 0) {
-                best2 = nd2;
-            } else {
-                const int l = node + 1, r = __float_as_int(n0.w);
-                const float dl = box_dist2(__ldg(M.nodes + 2 * l), __ldg(M.nodes + 2 * l + 1), p);
-                const float dr = box_dist2(__ldg(M.nodes + 2 * r), __ldg(M.nodes + 2 * r + 1), p);
-                const bool lf = dl <= dr;
-                if (sp < 48) {
-                    stack[sp] = lf ? r : l;
-                    sd[sp] = lf ? dr : dl;
-                    ++sp;
-                }
-                node = lf ? l : r;
-                nd2 = lf ? dl : dr;
-                continue;
-            }
-        }
-        // pop the next candidate that can still beat the bound
-        bool found = false;
-        while (sp > 0) {
-            --sp;
-            if (sd[sp] < best2) {
-                node = stack[sp];
-                nd2 = sd[sp];
-                found = true;
-                break;
-            }
-        }
-        if (!found) break;
-    }
-    return sqrtf(best2);
-}
-
-// Nearest hit over all primitives; ties keep the lower primitive index
-// (scene.cpp:99-109), i.e. the lexicographic minimum of (s, index).
-__device__ __forceinline__ bool consider(bool h, float s, int idx, int id, bool& have, float& best,
-                                         int& prim, int& hid) {
-    if (h && (!have || s < best || (s == best && idx < prim))) {
-        best = s;
-        prim = idx;
-        hid = id;   // (kind << 8) | slot, for the hit normal (EXT shading)
-        have = true;
-        return true;
-    }
-    return false;
-}
-
-// Free-distance budget of the analytic primitives (spheres, half-spaces):
-// `sfree` is a lower bound of the distance from the current chord start to
-// every sphere and half-space region.  A chord of length len < sfree cannot
-// reach any of them (so the exact tests could only report "no hit"); the
-// budget shrinks by len per skipped chord and is recomputed at the chord end
-// after every tested chord.  Inside-start chords have sfree <= 0 and are
-// always tested.  Results are identical to testing every chord.
-__device__ __forceinline__ float analytic_free(const DevParams& P, F3 b) {
-    float fr = 3.0e38f;
-#pragma unroll
-    for (int i = 0; i < kStaticSpheres; ++i)
-        if (i < P.n_spheres) {
-            const DevSphere& sp = P.spheres[i];
-            const float ox = b.x - sp.c[0], oy = b.y - sp.c[1], oz = b.z - sp.c[2];
-            fr = fminf(fr, sqrt_approx(fmaf(ox, ox, fmaf(oy, oy, oz * oz))) - sp.r);
-        }
-    for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
-        const DevSphere& sp = P.spheres[i];
-        const float ox = b.x - sp.c[0], oy = b.y - sp.c[1], oz = b.z - sp.c[2];
-        fr = fminf(fr, sqrt_approx(fmaf(ox, ox, fmaf(oy, oy, oz * oz))) - sp.r);
-    }
-#pragma unroll
-    for (int i = 0; i < kStaticHalves; ++i)
-        if (i < P.n_halves) {
-            const DevHalf& hs = P.halves[i];
-            fr = fminf(fr, (fmaf(hs.n[0], b.x, fmaf(hs.n[1], b.y, hs.n[2] * b.z)) - hs.off) * hs.inv_norm);
-        }
-    for (int i = kStaticHalves; i < P.n_halves; ++i) {
-        const DevHalf& hs = P.halves[i];
-        fr = fminf(fr, (fmaf(hs.n[0], b.x, fmaf(hs.n[1], b.y, hs.n[2] * b.z)) - hs.off) * hs.inv_norm);
-    }
-    // rounding margin of the FP32 distances (approximate sqrt, world units)
-    return fr - fmaf(2e-6f, fabsf(fr), 1e-5f) - 1e-6f * (fabsf(b.x) + fabsf(b.y) + fabsf(b.z));
-}
-
-template <bool MESH>
-__device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float& s_best,
-                                          int& prim, int& hid, float& mfree, int& mrec,
-                                          float& sfree) {
-    const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
-    const float qa = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
-    const float len = fmaf(sqrt_approx(qa), 1.0001f, 1e-30f);   // conservative chord length
-    bool have = false;
-    float s = 0.f;
-    if (len < sfree) {
-        sfree -= len;                     // no sphere / half-space within reach
-    } else {
-#pragma unroll
-        for (int i = 0; i < kStaticSpheres; ++i)
-            if (i < P.n_spheres) {
-                const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
-                consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
-            }
-        for (int i = kStaticSpheres; i < P.n_spheres; ++i) {
-            const bool h = hit_sphere(P.spheres[i], a, d, qa, len, s);
-            consider(h, s, P.spheres[i].index, (kPrimSphere << 8) | i, have, s_best, prim, hid);
-        }
-#pragma unroll
-        for (int i = 0; i < kStaticHalves; ++i)
-            if (i < P.n_halves) {
-                const bool h = hit_half_space(P.halves[i], a, d, s);
-                consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
-            }
-        for (int i = kStaticHalves; i < P.n_halves; ++i) {
-            const bool h = hit_half_space(P.halves[i], a, d, s);
-            consider(h, s, P.halves[i].index, (kPrimHalfSpace << 8) | i, have, s_best, prim, hid);
-        }
-        if (!have) sfree = analytic_free(P, b);
-    }
-    for (int i = 0; i < P.n_grids; ++i) {
-        const bool h = hit_grid(P.grids[i], a, b, d, s);
-        consider(h, s, P.grids[i].index, (kPrimGrid << 8) | i, have, s_best, prim, hid);
-    }
-    if (MESH) {
-        if (len < mfree) {
-            mfree -= len;                 // the chord stays inside the free ball
-        } else {
-            for (int i = 0; i < P.n_meshes; ++i) {
-                int rec = 0;
-                const bool h = mesh_chord(P.meshes[i], a, d, s, rec);
-                if (consider(h, s, P.meshes[i].index, (kPrimMesh << 8) | i, have, s_best, prim, hid))
-                    mrec = rec;
-            }
-            float fr = 3.0e38f;
-            for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, RR_MESH_FREE_CAP));
-            mfree = fr;
-        }
-    }
-    return have;
-}
-
-// Outward unit normal of a hit (EXTENSION shading; oracle/rro.c
-// intersect_segment_n): sphere radial, half-space n/|n|, grid entry face,
-// -chord direction for a chord that starts inside (s == 0).
-__device__ F3 hit_normal(const DevParams& P, int hid, float s, F3 a, F3 b, F3 point, int mrec) {
-    const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
-    if (hid >> 8 == kPrimMesh) {                // geometric normal facing the chord
-        const DevMesh& M = P.meshes[hid & 0xff];
-        const float4 r1 = __ldg(M.tris + 3 * mrec + 1), r2 = __ldg(M.tris + 3 * mrec + 2);
-        F3 n = f3(r1.y * r2.z - r1.z * r2.y, r1.z * r2.x - r1.x * r2.z, r1.x * r2.y - r1.y * r2.x);
-        const float sg = (n.x * d.x + n.y * d.y + n.z * d.z) > 0.f ? -1.f : 1.f;
-        const float il = sg * rsqrtf(n.x * n.x + n.y * n.y + n.z * n.z);
-        return f3(n.x * il, n.y * il, n.z * il);
-    }
-    const float kind = hid >> 8;
-    const int slot = hid & 0xff;
-    F3 n;
-    int grid_axis = -1;
-    if (s > 0.f && hid >> 8 == kPrimGrid) {
-        // re-run the winning slab entry with axis tracking
-        const DevGrid& g = P.grids[slot];
-        float best = 2.f;
-        const float av[3] = {a.x, a.y, a.z}, bv[3] = {b.x, b.y, b.z}, dv[3] = {d.x, d.y, d.z};
-        for (int dim = 0; dim < 3; ++dim) {
-            const float clo = fminf(av[dim], bv[dim]), chi = fmaxf(av[dim], bv[dim]);
-            const int kmin = (int)ceilf((clo - g.hw) / g.spacing);
-            const int kmax = (int)floorf((chi + g.hw) / g.spacing);
-            for (int k = kmin; k <= kmax; ++k) {
-                float lo[3] = {g.lo[0], g.lo[1], g.lo[2]}, hi[3] = {g.hi[0], g.hi[1], g.hi[2]};
-                const float plane = (float)k * g.spacing;
-                lo[dim] = fmaxf(lo[dim], plane - g.hw);
-                hi[dim] = fminf(hi[dim], plane + g.hw);
-                if (lo[dim] > hi[dim]) continue;
-                float smin = 0.f, smax = 1.f;
-                int ax = -1;
-                bool ok = true;
-                for (int e = 0; e < 3 && ok; ++e) {
-                    if (dv[e] == 0.f) {
-                        ok = !(av[e] < lo[e] || av[e] > hi[e]);
-                        continue;
-                    }
-                    float s1 = (lo[e] - av[e]) / dv[e], s2 = (hi[e] - av[e]) / dv[e];
-                    if (s1 > s2) {
-                        const float t = s1;
-                        s1 = s2;
-                        s2 = t;
-                    }
-                    if (s1 > smin) {
-                        smin = s1;
-                        ax = e;
-                    }
-                    smax = fminf(smax, s2);
-                    ok = !(smin > smax);
-                }
-                if (ok && smin < best) {
-                    best = smin;
-                    grid_axis = ax;
-                }
-            }
-        }
-    }
-    (void)kind;
-    if (s == 0.f || (hid >> 8 == kPrimGrid && grid_axis < 0)) {
-        const float il = rsqrtf(fmaxf(d.x * d.x + d.y * d.y + d.z * d.z, 1e-30f));
-        n = f3(-d.x * il, -d.y * il, -d.z * il);
-    } else if (hid >> 8 == kPrimSphere) {
-        const DevSphere& sp = P.spheres[slot];
-        const F3 r = f3(point.x - sp.c[0], point.y - sp.c[1], point.z - sp.c[2]);
-        const float il = rsqrtf(r.x * r.x + r.y * r.y + r.z * r.z);
-        n = f3(r.x * il, r.y * il, r.z * il);
-    } else if (hid >> 8 == kPrimHalfSpace) {
-        const DevHalf& hs = P.halves[slot];
-        const float il = rsqrtf(hs.n[0] * hs.n[0] + hs.n[1] * hs.n[1] + hs.n[2] * hs.n[2]);
-        n = f3(hs.n[0] * il, hs.n[1] * il, hs.n[2] * il);
-    } else {
-        const float dc = grid_axis == 0 ? d.x : (grid_axis == 1 ? d.y : d.z);
-        const float sg = dc > 0.f ? -1.f : 1.f;
-        n = f3(grid_axis == 0 ? sg : 0.f, grid_axis == 1 ? sg : 0.f, grid_axis == 2 ? sg : 0.f);
-    }
-    return n;
-}
-
-__device__ __forceinline__ bool inside_bounds(const DevParams& P, F3 p) {
-    return p.x >= P.lo[0] && p.x <= P.hi[0] && p.y >= P.lo[1] && p.y <= P.hi[1] &&
-           p.z >= P.lo[2] && p.z <= P.hi[2];
-}
-
-__device__ __forceinline__ unsigned cell_of(const DevParams& P, F3 p) {
-    const int g = P.grid;
-    const int ix = min(max((int)floorf((p.x - P.grid_lo[0]) * P.grid_inv[0]), 0), g - 1);
-    const int iy = min(max((int)floorf((p.y - P.grid_lo[1]) * P.grid_inv[1]), 0), g - 1);
-    const int iz = min(max((int)floorf((p.z - P.grid_lo[2]) * P.grid_inv[2]), 0), g - 1);
-    return ((unsigned)iz * g + iy) * g + ix;
-}
-
-struct RayResult {
-    int status;    // primary: 0 miss 1 hit 2 failed; shadow: 1 lit 0 blocked
-    int prim;
-    int steps;
-    float t;
-    F3 point;
-    F3 normal;     // NORMAL passes only
-};
-
-struct LaneCounters {
-    unsigned steps_integrated;
-    unsigned bump_evals;
-    unsigned lane_slots;       // loop iterations executed by this lane (active or not)
-};
-
-enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3 };
-
-// ---------------------------------------------------------------------------
-// March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
-// until every live lane has terminated; retired lanes keep computing (their
-// results are locked in), exactly as the reference's retired pack lanes.
-// PASS == kPassShadow marches a shadow geodesic (EXTENSION, oracle/rro.c
-// shadow_march): lit (1) when it crosses the sphere |x - q| = sqrt(dist2),
-// leaves the bounds or runs out of steps; blocked (0) on a nearer hit or a
-// metric failure.
-template <int KIND, int NB, int PASS, bool MESH>
-__device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool live, F3 p, F3 v,
-                                                     LaneCounters& cnt, F3 q, float dist2);
-
-template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, F3 p, F3 v,
-                                                LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
-                                                float dist2 = 0.f) {
-    RayResult res{PASS == kPassShadow ? 1 : 0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
-    bool active = live;
-    float cx = 0.f, cy = 0.f, cz = 0.f;       // Kahan compensation of the position sum
-    const float h = P.h;
-    const float half = 0.5f * h;
-    const float sixth = h / 6.f;
-    int step = 0;                             // this lane's reference step index
-    const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
-    float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
-    float sfree = 0.f;                        // sphere / half-space free distance budget
-    const bool twist1 = KIND == kDiffeo && P.n_stages == 1 && P.stages[0].kind == kStageTwist;
-    for (;;) {
-        if (!__any_sync(kFull, active)) break;
-        cnt.lane_slots += 1;
-        uint32_t um = 0;
-        int nj = 0;                           // >= 2: this lane jumps nj straight steps
-        if constexpr (KIND == kEuclid) {
-            // Gamma = 0 everywhere: every geodesic is the straight line x + j h y,
-            // so a lane jumps straight to its bounds exit (or its light's
-            // sphere); the chord test finds the hit and its reference step.
-            if (P.skip && active) {
-                const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
-                const float isp = rsqrtf(speed2);
-                float te = 3.0e38f;
-                if (v.x != 0.f) te = fminf(te, ((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x) / v.x);
-                if (v.y != 0.f) te = fminf(te, ((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y) / v.y);
-                if (v.z != 0.f) te = fminf(te, ((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z) / v.z);
-                float L = te * speed2 * isp;
-                if (PASS == kPassShadow) {
-                    const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
-                    L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
-                }
-                const float n = floorf(L * isp / h) - 1.f;
-                nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
-                if (nj < 2) nj = 0;
-            }
-        }
-        if constexpr (KIND == kBumps) {
-            uint32_t lm = 0;
-            unsigned cell = 0;
-            if (active) {
-                if (P.cull) {
-                    cell = cell_of(P, p);
-                    lm = __ldg(P.cull_masks + cell);
-                } else {
-                    lm = P.all_mask;
-                }
-            }
-            // Empty-space skipping: in a cell whose Chebyshev distance to the
-            // nearest non-empty cell is k, every point within (k-1) cells is
-            // bump-free (6 sigma, dilated by 1.5h), the culled metric is flat
-            // and the geodesic is the straight line x + j h y (Gamma = 0), so
-            // nj whole steps collapse into one chord.  A jump never crosses the
-            // bounds exit or (shadow rays) the light's sphere.
-            if (P.skip && active && lm == 0u) {
-                const int k = __ldg(P.skip_k + cell);
-                if (k >= 2) {
-                    const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
-                    const float isp = rsqrtf(speed2);
-                    float L = (float)(k - 1) * P.cell_min;
-                    float te = 3.0e38f;   // parameter distance to the bounds exit along v
-                    if (v.x != 0.f) te = fminf(te, ((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x) / v.x);
-                    if (v.y != 0.f) te = fminf(te, ((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y) / v.y);
-                    if (v.z != 0.f) te = fminf(te, ((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z) / v.z);
-                    L = fminf(L, te * speed2 * isp);
-                    if (PASS == kPassShadow) {
-                        const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
-                        L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
-                    }
-                    const float n = floorf(L * isp / h) - 1.f;
-                    nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
-                    if (nj < 2) nj = 0;
-                }
-            }
-            um = __reduce_or_sync(kFull, nj ? 0u : lm);
-            if (active && !nj) cnt.bump_evals += (SCHEME == 0 ? 1u : 4u) * __popc(um);
-        }
-        float valid = 3.0e38f;
-        F3 dp, vn;
-        if (__all_sync(kFull, nj != 0 || !active)) {         // whole warp jumps: no integration
-            dp = f3(0.f, 0.f, 0.f);
-            vn = v;
-        } else if (SCHEME == 0) {                            // Euler (integrate.hpp:55-61)
-            const F3 a = accel<KIND, NB>(P, um, p, v, valid);
-            dp = f3(h * v.x, h * v.y, h * v.z);
-            vn = f3(fmaf(h, a.x, v.x), fmaf(h, a.y, v.y), fmaf(h, a.z, v.z));
-        } else if (KIND == kDiffeo && RR_TWIST_RK4 && twist1) {
-            // RK4 of the single twist (integrate.hpp:63-93 with accel_diffeo's
-            // closed form): a_z = 0 and a does not depend on z, so z' stays
-            // constant, the stage points need no z and dz = h z'.
-            float sxx = 0.f, sxy = 0.f, svx = 0.f, svy = 0.f;
-            float px = p.x, py = p.y, vx = v.x, vy = v.y;
-            const float vz = v.z;
-#pragma unroll
-            for (int st = 0; st < 4; ++st) {
-                const float ax = vz * fmaf(vz, px, 2.f * vy), ay = vz * fmaf(vz, py, -2.f * vx);
-                const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
-                sxx = fmaf(wgt, vx, sxx); sxy = fmaf(wgt, vy, sxy);
-                svx = fmaf(wgt, ax, svx); svy = fmaf(wgt, ay, svy);
-                const float c = st < 2 ? half : h;
-                px = fmaf(c, vx, p.x); py = fmaf(c, vy, p.y);
-                vx = fmaf(c, ax, v.x); vy = fmaf(c, ay, v.y);
-            }
-            valid = 1.f;
-            dp = f3(sixth * sxx, sixth * sxy, h * vz);
-            vn = f3(fmaf(sixth, svx, v.x), fmaf(sixth, svy, v.y), vz);
-        } else {                                             // RK4 (integrate.hpp:63-93)
-            F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
-            F3 ps = p, vs = v;
-            auto stage = [&](int st) {
-                const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
-                const float wgt = (st == 0 || st == 3) ? 1.f : 2.f;
-                sx = f3(fmaf(wgt, vs.x, sx.x), fmaf(wgt, vs.y, sx.y), fmaf(wgt, vs.z, sx.z));
-                sv = f3(fmaf(wgt, a.x, sv.x), fmaf(wgt, a.y, sv.y), fmaf(wgt, a.z, sv.z));
-                const float c = st < 2 ? half : h;
-                ps = f3(fmaf(c, vs.x, p.x), fmaf(c, vs.y, p.y), fmaf(c, vs.z, p.z));
-                vs = f3(fmaf(c, a.x, v.x), fmaf(c, a.y, v.y), fmaf(c, a.z, v.z));
-            };
-            if constexpr (KIND == kDiffeo && RR_DIFFEO_RK4_UNROLL) {   // unrolled stages
-#pragma unroll
-                for (int st = 0; st < 4; ++st) stage(st);
-            } else {
-#pragma unroll 1
-                for (int st = 0; st < 4; ++st) stage(st);   // one call site: the bump block is inlined once
-            }
-            dp = f3(sixth * sx.x, sixth * sx.y, sixth * sx.z);
-            vn = f3(fmaf(sixth, sv.x, v.x), fmaf(sixth, sv.y, v.y), fmaf(sixth, sv.z, v.z));
-        }
-        if (nj) {                                            // straight jump of nj steps
-            const float hn = h * (float)nj;
-            dp = f3(hn * v.x, hn * v.y, hn * v.z);
-            vn = v;
-            valid = 3.0e38f;
-        }
-        // Compensated position update: pn = p + dp carrying the rounding error.
-        F3 pn;
-        {
-            const float yx = dp.x - cx, yy = dp.y - cy, yz = dp.z - cz;
-            pn = f3(p.x + yx, p.y + yy, p.z + yz);
-            cx = (pn.x - p.x) - yx;
-            cy = (pn.y - p.y) - yy;
-            cz = (pn.z - p.z) - yz;
-        }
-        if (active) {
-            const int nsub = nj ? nj : 1;
-            cnt.steps_integrated += 1;
-            float s = 0.f;
-            int prim = -1, hid = 0, mrec = 0;
-            if (KIND == kDiffeo && !(valid > 1e-14f)) {     // kernel_impl.hpp:54-61
-                res.status = PASS == kPassShadow ? 0 : 2;
-                res.steps = step;
-                active = false;
-            } else if (intersect<MESH>(P, p, pn, s, prim, hid, mfree, mrec, sfree)) { // kernel_impl.hpp:63-76
-                const F3 pt = f3(fmaf(s, pn.x - p.x, p.x), fmaf(s, pn.y - p.y, p.y),
-                                 fmaf(s, pn.z - p.z, p.z));
-                const float sj = s * (float)nsub;            // hit position in reference steps
-                const int sub = min((int)sj, nsub - 1);
-                if constexpr (PASS == kPassShadow) {
-                    const F3 r = f3(pt.x - q.x, pt.y - q.y, pt.z - q.z);
-                    res.status = (r.x * r.x + r.y * r.y + r.z * r.z) < dist2 ? 0 : 1;
-                } else {
-                    res.status = 1;
-                    res.prim = prim;
-                    res.point = pt;
-                    res.t = ((float)step + sj) * h;
-                    if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, pn, pt, mrec);
-                }
-                res.steps = step + sub + 1;
-                active = false;
-            } else if (PASS == kPassShadow &&
-                       (pn.x - q.x) * (pn.x - q.x) + (pn.y - q.y) * (pn.y - q.y) +
-                               (pn.z - q.z) * (pn.z - q.z) >= dist2) {
-                res.status = 1;                              // reached the light's sphere
-                res.steps = step + nsub;
-                active = false;
-            } else if (!inside_bounds(P, pn)) {             // kernel_impl.hpp:77-82
-                res.status = PASS == kPassShadow ? 1 : 0;
-                res.steps = step + nsub;
-                active = false;
-            }
-            step += nsub;
-            if (active && step >= P.max_steps) {             // kernel_impl.hpp:87-91
-                res.status = PASS == kPassShadow ? 1 : 0;
-                res.steps = P.max_steps;
-                active = false;
-            }
-        }
-        p = pn;
-        v = vn;
-    }
-    return res;
-}
-
-
-// ---------------------------------------------------------------------------
-// EXTENSION: adaptive Bogacki-Shampine 3(2) march (integrator.scheme "rk23";
-// FP64 definition: oracle/rro.c march_one_rk23).  Per-lane step size; FSAL
-// (k1 of the next step is k4 of the accepted one); the warp-uniform bump mask
-// is taken at the step start and covers every stage point because the
-// culling grid is dilated for h_max = 4 h0.  Rejected lanes keep their state.
-template <int KIND, int NB, int PASS, bool MESH>
-__device__ __forceinline__ RayResult march_unit_rk23(const DevParams& P, bool live, F3 p, F3 v,
-                                                     LaneCounters& cnt, F3 q, float dist2) {
-    RayResult res{PASS == kPassShadow ? 1 : 0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
-    bool active = live;
-    const float h0 = P.h, hmin = h0 / 64.f, hmax = 4.f * h0, tol = P.tol;
-    const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
-    float h = h0, t = 0.f;
-    int steps = 0, attempts = 0;
-    float mfree = 0.f, sfree = 0.f;
-    bool have_k1 = false;
-    F3 k1v = f3(0.f, 0.f, 0.f);
-    for (;;) {
-        if (!__any_sync(kFull, active)) break;
-        cnt.lane_slots += 1;
-        uint32_t um = 0;
-        int nj = 0;                   // >= 2: this lane jumps nj straight steps of h_max
-        // Straight jumps: where the (culled) metric is flat the error estimate
-        // is ~0, so h sits at h_max and the geodesic is x + j h_max y; a lane
-        // at h_max collapses nj such steps into one chord (same rules as the
-        // fixed-step march: never past the bounds exit or the light's sphere,
-        // bump scenes only inside empty cells of the culling grid).
-        float L = -1.f;
-        if (P.skip && active && h >= hmax) {
-            if constexpr (KIND == kEuclid) L = 3.0e38f;
-            if constexpr (KIND == kBumps) {
-                if (P.cull) {
-                    const unsigned cell = cell_of(P, p);
-                    if (__ldg(P.cull_masks + 2u * P.cull_cells + cell) == 0u) {
-                        const int k = __ldg(P.skip_k + cell);
-                        if (k >= 2) L = (float)(k - 1) * P.cell_min;
-                    }
-                }
-            }
-        }
-        if (L > 0.f) {
-            const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
-            const float isp = rsqrtf(speed2);
-            float te = 3.0e38f;
-            if (v.x != 0.f) te = fminf(te, ((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x) / v.x);
-            if (v.y != 0.f) te = fminf(te, ((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y) / v.y);
-            if (v.z != 0.f) te = fminf(te, ((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z) / v.z);
-            L = fminf(L, te * speed2 * isp);
-            if (PASS == kPassShadow) {
-                const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
-                L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
-            }
-            const float n = floorf(L * isp / hmax) - 1.f;
-            nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - steps));
-            if (nj < 2) nj = 0;
-        }
-        if constexpr (KIND == kBumps) {
-            uint32_t lm = 0;
-            if (active && !nj) {   // the mask level whose dilation covers this lane's h
-                const unsigned lvl = h <= h0 ? 0u : (h <= 2.f * h0 ? 1u : 2u);
-                lm = P.cull ? __ldg(P.cull_masks + lvl * P.cull_cells + cell_of(P, p)) : P.all_mask;
-            }
-            um = __reduce_or_sync(kFull, lm);
-        }
-        float valid = 3.0e38f;
-        const bool need_k1 = !__all_sync(kFull, have_k1 || !active);
-        if (need_k1) {                         // first step (warp-uniform branch)
-            const F3 a = accel<KIND, NB>(P, um, p, v, valid);
-            if (!have_k1) k1v = a;
-            have_k1 = true;
-        }
-        const F3 k1x = v;
-        F3 k2x, k2v, k3x, k3v, k4x, k4v, xn, vn;
-        float e = 0.f;
-        if (__all_sync(kFull, nj != 0 || !active)) {   // whole warp jumps: no integration
-            k2x = k3x = k4x = v;
-            k2v = k3v = k4v = f3(0.f, 0.f, 0.f);
-            xn = p;
-            vn = v;
-        } else {
-            // stages k2, k3, k4 through one call site
-            F3 ps = f3(fmaf(0.5f * h, k1x.x, p.x), fmaf(0.5f * h, k1x.y, p.y), fmaf(0.5f * h, k1x.z, p.z));
-            F3 vs = f3(fmaf(0.5f * h, k1v.x, v.x), fmaf(0.5f * h, k1v.y, v.y), fmaf(0.5f * h, k1v.z, v.z));
-#pragma unroll 1
-            for (int st = 0; st < 3; ++st) {
-                const F3 a = accel<KIND, NB>(P, um, ps, vs, valid);
-                if (st == 0) {
-                    k2x = vs; k2v = a;
-                    ps = f3(fmaf(0.75f * h, k2x.x, p.x), fmaf(0.75f * h, k2x.y, p.y), fmaf(0.75f * h, k2x.z, p.z));
-                    vs = f3(fmaf(0.75f * h, k2v.x, v.x), fmaf(0.75f * h, k2v.y, v.y), fmaf(0.75f * h, k2v.z, v.z));
-                } else if (st == 1) {
-                    k3x = vs; k3v = a;
-                    const float c1 = 2.f / 9.f * h, c2 = 1.f / 3.f * h, c3 = 4.f / 9.f * h;
-                    xn = f3(fmaf(c1, k1x.x, fmaf(c2, k2x.x, fmaf(c3, k3x.x, p.x))),
-                            fmaf(c1, k1x.y, fmaf(c2, k2x.y, fmaf(c3, k3x.y, p.y))),
-                            fmaf(c1, k1x.z, fmaf(c2, k2x.z, fmaf(c3, k3x.z, p.z))));
-                    vn = f3(fmaf(c1, k1v.x, fmaf(c2, k2v.x, fmaf(c3, k3v.x, v.x))),
-                            fmaf(c1, k1v.y, fmaf(c2, k2v.y, fmaf(c3, k3v.y, v.y))),
-                            fmaf(c1, k1v.z, fmaf(c2, k2v.z, fmaf(c3, k3v.z, v.z))));
-                    ps = xn;
-                    vs = vn;
-                } else {
-                    k4x = vs; k4v = a;
-                }
-            }
-            if constexpr (KIND == kBumps) {
-                if (active && !nj) cnt.bump_evals += 3u * __popc(um);
-            }
-            // embedded error, mixed abs/rel scale
-            const float e1 = -5.f / 72.f * h, e2 = 1.f / 12.f * h, e3 = 1.f / 9.f * h, e4 = -1.f / 8.f * h;
-            const float y0[6] = {p.x, p.y, p.z, v.x, v.y, v.z};
-            const float y1[6] = {xn.x, xn.y, xn.z, vn.x, vn.y, vn.z};
-            const float ka[6] = {k1x.x, k1x.y, k1x.z, k1v.x, k1v.y, k1v.z};
-            const float kb[6] = {k2x.x, k2x.y, k2x.z, k2v.x, k2v.y, k2v.z};
-            const float kc[6] = {k3x.x, k3x.y, k3x.z, k3v.x, k3v.y, k3v.z};
-            const float kd[6] = {k4x.x, k4x.y, k4x.z, k4v.x, k4v.y, k4v.z};
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                const float err = fmaf(e1, ka[i], fmaf(e2, kb[i], fmaf(e3, kc[i], e4 * kd[i])));
-                const float sc = tol * (1.f + fmaxf(fabsf(y0[i]), fabsf(y1[i])));
-                e = fmaxf(e, __fdividef(fabsf(err), sc));
-            }
-        }
-        if (nj) {                                            // straight jump of nj h_max steps
-            const float hn = hmax * (float)nj;
-            xn = f3(fmaf(hn, v.x, p.x), fmaf(hn, v.y, p.y), fmaf(hn, v.z, p.z));
-            vn = v;
-            k4v = f3(0.f, 0.f, 0.f);                         // flat (culled) metric at xn
-            e = 0.f;
-            valid = 3.0e38f;
-        }
-        const bool accept = e <= 1.f || h <= hmin;
-        if (active) {
-            const int nsub = nj ? nj : 1;
-            const float hstep = nj ? hmax * (float)nj : h;
-            cnt.steps_integrated += 1;
-            attempts += nsub;
-            float s = 0.f;
-            int prim = -1, hid = 0, mrec = 0;
-            if (KIND == kDiffeo && !(valid > 1e-14f)) {
-                res.status = PASS == kPassShadow ? 0 : 2;
-                res.steps = steps;
-                active = false;
-            } else if (accept) {
-                if (intersect<MESH>(P, p, xn, s, prim, hid, mfree, mrec, sfree)) {
-                    const F3 pt = f3(fmaf(s, xn.x - p.x, p.x), fmaf(s, xn.y - p.y, p.y),
-                                     fmaf(s, xn.z - p.z, p.z));
-                    const int sub = min((int)(s * (float)nsub), nsub - 1);
-                    if constexpr (PASS == kPassShadow) {
-                        const F3 r = f3(pt.x - q.x, pt.y - q.y, pt.z - q.z);
-                        res.status = (r.x * r.x + r.y * r.y + r.z * r.z) < dist2 ? 0 : 1;
-                    } else {
-                        res.status = 1;
-                        res.prim = prim;
-                        res.point = pt;
-                        res.t = fmaf(s, hstep, t);
-                        if constexpr (PASS == kPassHits) res.normal = hit_normal(P, hid, s, p, xn, pt, mrec);
-                    }
-                    res.steps = steps + sub + 1;
-                    active = false;
-                } else {
-                    steps += nsub;
-                    const bool crossed = PASS == kPassShadow &&
-                        (xn.x - q.x) * (xn.x - q.x) + (xn.y - q.y) * (xn.y - q.y) +
-                            (xn.z - q.z) * (xn.z - q.z) >= dist2;
-                    if (crossed || !inside_bounds(P, xn)) {
-                        res.status = PASS == kPassShadow ? 1 : 0;
-                        res.steps = steps;
-                        active = false;
-                    } else {
-                        t += hstep;
-                        p = xn;
-                        v = vn;
-                        k1v = k4v;
-                    }
-                }
-            }
-            if (active) {
-                const float fac = e > 0.f ? fminf(5.f, fmaxf(0.2f, 0.9f * ex2(-__log2f(e) / 3.f))) : 5.f;
-                h = fminf(hmax, fmaxf(hmin, h * fac));
-                if (steps >= P.max_steps || attempts >= 16 * P.max_steps) {
-                    res.status = PASS == kPassShadow ? 1 : 0;
-                    res.steps = steps;
-                    active = false;
-                }
-            }
-        }
-    }
-    return res;
-}
-
-template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__device__ __forceinline__ RayResult march_unit(const DevParams& P, bool live, F3 p, F3 v,
-                                                LaneCounters& cnt, F3 q = F3{0.f, 0.f, 0.f},
-                                                float dist2 = 0.f) {
-    if constexpr (SCHEME == 2) return march_unit_rk23<KIND, NB, PASS, MESH>(P, live, p, v, cnt, q, dist2);
-    else return march_fixed<KIND, NB, SCHEME, PASS, MESH>(P, live, p, v, cnt, q, dist2);
-}
-
-// g at x (metric.cpp:12-15 / :40-42), for the shadow ray's unit g-speed.
-__device__ void metric_at(const DevParams& P, F3 x, float g[6], bool& ok) {
-    float gx = 0.f, gy = 0.f, gz = 0.f;   // grad f (graph) ; J (diffeo) below
-    ok = true;
-    g[0] = g[3] = g[5] = 1.f;
-    g[1] = g[2] = g[4] = 0.f;
-    if (P.kind == kBumps || P.kind == kGraphGeneral) {
-        for (int j = 0; j < (P.kind == kBumps ? P.nb_slot : P.n_bumps); ++j) {
-            const DevBump& b = P.bumps[j];
-            const float dx = x.x - b.cx, dy = x.y - b.cy, dz = x.z - b.cz;
-            const float v = ex2(fmaf(dx * b.kx, dx, fmaf(dy * b.ky, dy, fmaf(dz * b.kz, dz, b.la)))) * b.sgn;
-            gx = fmaf(-v * kBeta, dx * b.kx, gx);
-            gy = fmaf(-v * kBeta, dy * b.ky, gy);
-            gz = fmaf(-v * kBeta, dz * b.kz, gz);
-        }
-        float xp[5], yp[5], zp[5];
-        xp[0] = yp[0] = zp[0] = 1.f;
-        for (int k = 1; k < 5; ++k) {
-            xp[k] = xp[k - 1] * x.x;
-            yp[k] = yp[k - 1] * x.y;
-            zp[k] = zp[k - 1] * x.z;
-        }
-        for (int i = 0; i < P.n_poly; ++i) {
-            const DevPoly& t = P.poly[i];
-            if (t.a > 0) gx = fmaf(t.coef * t.a, xp[t.a - 1] * yp[t.b] * zp[t.c], gx);
-            if (t.b > 0) gy = fmaf(t.coef * t.b, xp[t.a] * yp[t.b - 1] * zp[t.c], gy);
-            if (t.c > 0) gz = fmaf(t.coef * t.c, xp[t.a] * yp[t.b] * zp[t.c - 1], gz);
-        }
-        g[0] += gx * gx; g[1] = gx * gy; g[2] = gx * gz;
-        g[3] += gy * gy; g[4] = gy * gz; g[5] += gz * gz;
-    } else if (P.kind == kDiffeo) {
-        float J[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
-        float x0 = x.x, x1 = x.y, x2 = x.z;
-        for (int s = 0; s < P.n_stages; ++s) {
-            const DevStage& st = P.stages[s];
-            float Js[9], n0, n1, n2;
-            if (st.kind == kStageAffine) {
-                for (int k = 0; k < 9; ++k) Js[k] = st.v[k];
-                n0 = st.v[0] * x0 + st.v[1] * x1 + st.v[2] * x2 + st.v[9];
-                n1 = st.v[3] * x0 + st.v[4] * x1 + st.v[5] * x2 + st.v[10];
-                n2 = st.v[6] * x0 + st.v[7] * x1 + st.v[8] * x2 + st.v[11];
-            } else if (st.kind == kStageTwist) {
-                float sn, cs;
-                sincosf(x2, &sn, &cs);
-                Js[0] = cs; Js[1] = -sn; Js[2] = -(x0 * sn) - x1 * cs;
-                Js[3] = sn; Js[4] = cs; Js[5] = x0 * cs - x1 * sn;
-                Js[6] = 0.f; Js[7] = 0.f; Js[8] = 1.f;
-                n0 = x0 * cs - x1 * sn;
-                n1 = x0 * sn + x1 * cs;
-                n2 = x2;
-            } else if (st.kind == kStageBend) {
-                const float k = st.v[0], c = st.v[1];
-                float sn, cs;
-                __sincosf(k * x0, &sn, &cs);
-                const float yc = x1 - c;
-                Js[0] = -k * cs * yc; Js[1] = -sn; Js[2] = 0.f;
-                Js[3] = -k * sn * yc; Js[4] = cs; Js[5] = 0.f;
-                Js[6] = 0.f; Js[7] = 0.f; Js[8] = 1.f;
-                n0 = -sn * yc;
-                n1 = fmaf(cs, yc, c);
-                n2 = x2;
-            } else {
-                const float* b = st.v;
-                const float ux = (x0 - b[0]) * b[3], uy = (x1 - b[1]) * b[4], uz = (x2 - b[2]) * b[5];
-                const float e = b[6] * __expf(-0.5f * (ux * ux + uy * uy + uz * uz));
-                const float fg[3] = {-e * ux * b[3], -e * uy * b[4], -e * uz * b[5]};
-                for (int i = 0; i < 3; ++i)
-                    for (int j = 0; j < 3; ++j) Js[3 * i + j] = (i == j ? 1.f : 0.f) + b[7 + i] * fg[j];
-                n0 = fmaf(e, b[7], x0);
-                n1 = fmaf(e, b[8], x1);
-                n2 = fmaf(e, b[9], x2);
-            }
-            float R[9];
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j)
-                    R[3 * i + j] = Js[3 * i] * J[j] + Js[3 * i + 1] * J[3 + j] + Js[3 * i + 2] * J[6 + j];
-            for (int k = 0; k < 9; ++k) J[k] = R[k];
-            x0 = n0; x1 = n1; x2 = n2;
-        }
-        const float d = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
-                        J[2] * (J[3] * J[7] - J[4] * J[6]);
-        ok = fabsf(d) > 1e-14f;
-        g[0] = J[0] * J[0] + J[3] * J[3] + J[6] * J[6];
-        g[1] = J[0] * J[1] + J[3] * J[4] + J[6] * J[7];
-        g[2] = J[0] * J[2] + J[3] * J[5] + J[6] * J[8];
-        g[3] = J[1] * J[1] + J[4] * J[4] + J[7] * J[7];
-        g[4] = J[1] * J[2] + J[4] * J[5] + J[7] * J[8];
-        g[5] = J[2] * J[2] + J[5] * J[5] + J[8] * J[8];
-    }
-}
-
-// Pseudo-colour + fog (render.cpp:14-25); failures magenta (render.cpp:39).
-// `light` scales the colour (EXTENSION lit shading; 1 = reference shading).
-__device__ __forceinline__ void shade(const DevParams& P, const RayResult& r, uint8_t* rgb,
-                                      float light = 1.f) {
-    if (r.status == 2) {
-        rgb[0] = 255; rgb[1] = 0; rgb[2] = 255;
-        return;
-    }
-    if (r.status != 1) {
-        rgb[0] = rgb[1] = rgb[2] = 0;
-        return;
-    }
-    const float atten = expf(-P.fog * r.t);
-    const float pv[3] = {r.point.x, r.point.y, r.point.z};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const float frac = pv[k] - floorf(pv[k]);
-        // lround (half away from zero) for the non-negative argument, without
-        // the 64-bit conversion code of lroundf: trunc + exact fraction test
-        const float x = 255.f * (frac * atten * light);
-        const float tr = truncf(x);
-        int v = (int)tr + ((x - tr) >= 0.5f ? 1 : 0);
-        v = v < 0 ? 0 : (v > 255 ? 255 : v);
-        rgb[k] = (uint8_t)v;
-    }
-}
-
-// Primary ray of pixel (px, py) (camera.cpp:22-29), computed in FP64.
-__device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w, int h, F3& pos,
-                                       F3& dir) {
-    const double sx = (2.0 * (px + 0.5) / w - 1.0) * c.tan_half * c.aspect;
-    const double sy = (1.0 - 2.0 * (py + 0.5) / h) * c.tan_half;
-    const double dx = c.f0[0] + sx * c.f2[0] + sy * c.f1[0];
-    const double dy = c.f0[1] + sx * c.f2[1] + sy * c.f1[1];
-    const double dz = c.f0[2] + sx * c.f2[2] + sy * c.f1[2];
-    const double n2 = c.g[0] * dx * dx + c.g[3] * dy * dy + c.g[5] * dz * dz +
-                      2.0 * (c.g[1] * dx * dy + c.g[2] * dx * dz + c.g[4] * dy * dz);
-    const double inv = 1.0 / sqrt(n2);
-    pos = f3((float)c.pos[0], (float)c.pos[1], (float)c.pos[2]);
-    dir = f3((float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
-}
-
-// ---------------------------------------------------------------------------
-// Ray-pair march (Gaussian-bump metric, fixed-step RK4, mesh-free scenes):
-// march_fixed for two rays per thread.  The integrator and the metric run
-// packed (F2 / P3); the culling lookup, the chord test and the termination
-// bookkeeping run per ray on the unpacked halves with exactly march_fixed's
-// rules (kernel_impl.hpp:22-94).  The warp-uniform bump mask is the OR over
-// the 64 rays of the unit.
-template <int PASS>
-__device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
-                                          float light_d) {
-    const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
-    const float isp = rsqrtf(speed2);
-    float L = (float)(k - 1) * P.cell_min;
-    float te = 3.0e38f;   // parameter distance to the bounds exit along v
-    if (v.x != 0.f) te = fminf(te, __fdividef((v.x > 0.f ? P.hi[0] : P.lo[0]) - p.x, v.x));
-    if (v.y != 0.f) te = fminf(te, __fdividef((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y, v.y));
-    if (v.z != 0.f) te = fminf(te, __fdividef((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z, v.z));
-    L = fminf(L, te * speed2 * isp);
-    if (PASS == kPassShadow) {
-        const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
-        L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
-    }
-    const float n = floorf(L * isp * P.inv_h) - 1.f;   // fast division: the -1 step margin covers it
-    const int nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
-    return nj < 2 ? 0 : nj;
-}
-
-template <int PASS>
-__device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
-                                             int r, const RayResult& res);
-
-// Marches a ray pair.  Primary passes write each ray's output when it
-// terminates (emit_primary); every pass returns per-ray status and
-// reference-equivalent step counts.
-template <int NB, int PASS>
-__device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool live1, P3 p, P3 v,
-                                           LaneCounters& cnt, const DevLaunch& L, unsigned unit,
-                                           int (&status)[2], int (&steps)[2], float (&tout)[2],
-                                           F3 (&pout)[2], F3 q0 = F3{0.f, 0.f, 0.f},
-                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f) {
-    status[0] = status[1] = PASS == kPassShadow ? 1 : 0;
-    steps[0] = steps[1] = 0;
-    bool act[2] = {live0, live1};
-    int step[2] = {0, 0};
-    const F3 qq[2] = {q0, q1};
-    const float dd[2] = {d20, d21};
-    float light_d[2] = {0.f, 0.f};
-    if (PASS == kPassShadow) {
-        light_d[0] = sqrtf(d20);
-        light_d[1] = sqrtf(d21);
-    }
-    const float h = P.h;
-    const F2 half = bc2(0.5f * h), full = bc2(h), sixth = bc2(h / 6.f);
-    P3 c{bc2(0.f), bc2(0.f), bc2(0.f)};    // Kahan compensation of the position sums
-    float sfree[2] = {0.f, 0.f};           // sphere / half-space free distance budgets
-    for (;;) {
-        if (!__any_sync(kFull, act[0] || act[1])) break;
-        cnt.lane_slots += 2;
-        int nj[2] = {0, 0};
-        uint32_t lmo = 0u;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            uint32_t lm = 0u;
-            unsigned cell = 0;
-            if (act[r]) {
-                if (P.cull) {
-                    cell = cell_of(P, ray_of(p, r));
-                    lm = __ldg(P.cull_masks + cell);
-                } else {
-                    lm = P.all_mask;
-                }
-                if (P.skip && lm == 0u) {
-                    const int k = __ldg(P.skip_k + cell);
-                    if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r]);
-                }
-            }
-            lmo |= nj[r] ? 0u : lm;
-        }
-        const uint32_t um = __reduce_or_sync(kFull, lmo);
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(um);
-        P3 dp, vn;
-        const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
-        if (__all_sync(kFull, jw0 && jw1)) {                // whole warp jumps: no integration
-            dp = P3{bc2(0.f), bc2(0.f), bc2(0.f)};
-            vn = v;
-        } else {                                             // RK4 (integrate.hpp:63-93)
-            P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
-            P3 ps = p, vs = v;
-#if RR_X2_RK4_UNROLL
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
-            for (int st = 0; st < 4; ++st) {   // one call site: the bump block is inlined once
-                const P3 a = accel_bumps_x2<NB>(P, um, ps, vs);
-                const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
-                sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
-                sv = P3{fma2(wgt, a.x, sv.x), fma2(wgt, a.y, sv.y), fma2(wgt, a.z, sv.z)};
-                const F2 cc = st < 2 ? half : full;
-                ps = P3{fma2(cc, vs.x, p.x), fma2(cc, vs.y, p.y), fma2(cc, vs.z, p.z)};
-                vs = P3{fma2(cc, a.x, v.x), fma2(cc, a.y, v.y), fma2(cc, a.z, v.z)};
-            }
-            dp = P3{mul2(sixth, sx.x), mul2(sixth, sx.y), mul2(sixth, sx.z)};
-            vn = P3{fma2(sixth, sv.x, v.x), fma2(sixth, sv.y, v.y), fma2(sixth, sv.z, v.z)};
-        }
-        if (nj[0] | nj[1]) {                                 // straight jumps of nj steps
-            const F2 hn = mk2(h * (float)nj[0], h * (float)nj[1]);
-            const P3 dj{mul2(hn, v.x), mul2(hn, v.y), mul2(hn, v.z)};
-            const bool j0 = nj[0] != 0, j1 = nj[1] != 0;
-            dp = P3{sel2(j0, j1, dj.x, dp.x), sel2(j0, j1, dj.y, dp.y), sel2(j0, j1, dj.z, dp.z)};
-            vn = P3{sel2(j0, j1, v.x, vn.x), sel2(j0, j1, v.y, vn.y), sel2(j0, j1, v.z, vn.z)};
-        }
-        // compensated position update: pn = p + dp carrying the rounding error
-        const P3 yv{sub2(dp.x, c.x), sub2(dp.y, c.y), sub2(dp.z, c.z)};
-        const P3 pn{add2(p.x, yv.x), add2(p.y, yv.y), add2(p.z, yv.z)};
-        c = P3{sub2(sub2(pn.x, p.x), yv.x), sub2(sub2(pn.y, p.y), yv.y), sub2(sub2(pn.z, p.z), yv.z)};
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            if (!act[r]) continue;
-            const F3 a = ray_of(p, r), b = ray_of(pn, r);
-            const int nsub = nj[r] ? nj[r] : 1;
-            cnt.steps_integrated += 1;
-            float s = 0.f, mfree = 0.f;
-            int prim = -1, hid = 0, mrec = 0;
-            const bool hit = intersect<false>(P, a, b, s, prim, hid, mfree, mrec, sfree[r]);
-            if (hit) {                                       // kernel_impl.hpp:63-76
-                const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
-                const float sj = s * (float)nsub;            // hit position in reference steps
-                const int sub = min((int)sj, nsub - 1);
-                if constexpr (PASS == kPassShadow) {
-                    const F3 rr = f3(pt.x - qq[r].x, pt.y - qq[r].y, pt.z - qq[r].z);
-                    status[r] = (rr.x * rr.x + rr.y * rr.y + rr.z * rr.z) < dd[r] ? 0 : 1;
-                } else {
-                    if constexpr (PASS == kPassHits) {
-                        RayResult res{1, prim, 0, ((float)step[r] + sj) * h, pt, f3(0.f, 0.f, 0.f)};
-                        res.normal = hit_normal(P, hid, s, a, b, pt, mrec);
-                        emit_primary<PASS>(P, L, unit, r, res);
-                    } else {
-                        tout[r] = ((float)step[r] + sj) * h;
-                        pout[r] = pt;
-                    }
-                    status[r] = 1;
-                }
-                steps[r] = step[r] + sub + 1;
-                act[r] = false;
-            } else if (PASS == kPassShadow &&
-                       (b.x - qq[r].x) * (b.x - qq[r].x) + (b.y - qq[r].y) * (b.y - qq[r].y) +
-                               (b.z - qq[r].z) * (b.z - qq[r].z) >= dd[r]) {
-                status[r] = 1;                               // reached the light's sphere
-                steps[r] = step[r] + nsub;
-                act[r] = false;
-            } else {
-                step[r] += nsub;
-                const bool out = !inside_bounds(P, b);      // kernel_impl.hpp:77-82
-                if (out || step[r] >= P.max_steps) {         // kernel_impl.hpp:87-91
-                    status[r] = PASS == kPassShadow ? 1 : 0;
-                    steps[r] = out ? step[r] : P.max_steps;
-                    act[r] = false;
-                    if constexpr (PASS == kPassHits) {
-                        RayResult res{0, -1, 0, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
-                        emit_primary<PASS>(P, L, unit, r, res);
-                    }
-                }
-                continue;
-            }
-            step[r] += nsub;
-        }
-        p = pn;
-        v = vn;
-    }
-}
-
-template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-__global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23
-                                         : (MESH ? RR_MIN_BLOCKS_MESH : RR_MIN_BLOCKS))
-march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned unit = 0;
-        if (lane == 0) unit = atomicAdd(L.counter, 1u);
-        unit = __shfl_sync(kFull, unit, 0);
-        if (unit >= L.n_units) break;
-
-        bool live;
-        F3 pos, dir;
-        int px = 0, py = 0, lx = 0, ly = 0;
-        unsigned long long ray_index = 0, tile_k = 0, pix = 0;
-        if (L.mode == kModeRays) {
-            ray_index = (unsigned long long)unit * kUnit + lane;
-            live = ray_index < L.n_rays;
-            if (live) {
-                const double* r = L.rays + 6 * ray_index;
-                pos = f3((float)r[0], (float)r[1], (float)r[2]);
-                dir = f3((float)r[3], (float)r[4], (float)r[5]);
-            } else {
-                pos = dir = f3(0.f, 0.f, 0.f);
-            }
-        } else {
-            // shadow pass: a unit is 32/lpp pixels of a micro-tile x lpp lights
-            const unsigned mt = PASS == kPassShadow ? unit / L.lpp : unit;
-            const int sub = PASS == kPassShadow ? (int)(unit % L.lpp) : 0;
-            const int ppu = PASS == kPassShadow ? kUnit / L.lpp : kUnit;
-            const int idx = sub * ppu + lane % ppu;          // pixel within the micro-tile
-            tile_k = mt / L.micro_per_tile;
-            const unsigned micro = mt % L.micro_per_tile;
-            const unsigned tile = L.shard + (unsigned)tile_k * L.n_shards;
-            const int tx = tile % L.tiles_x, ty = tile / L.tiles_x;
-            const int mpr = L.tile_w / kMicroW;
-            lx = (micro % mpr) * kMicroW + (idx & 7);
-            ly = (micro / mpr) * kMicroH + (idx >> 3);
-            px = tx * L.tile_w + lx;
-            py = ty * L.tile_h + ly;
-            live = px < L.width && py < L.height;
-            // output index: row-major frame, or tile-major shard buffer
-            pix = L.mode == kModeFrame ? (unsigned long long)py * L.width + px
-                                       : tile_k * L.tile_w * L.tile_h + (unsigned long long)ly * L.tile_w + lx;
-            if (PASS != kPassShadow) {
-                if (live) raygen(L.cam, px, py, L.width, L.height, pos, dir);
-                else pos = dir = f3(0.f, 0.f, 0.f);
-            }
-        }
-
-        LaneCounters cnt{0u, 0u, 0u};
-        unsigned ref_steps = 0, errs = 0, shadow_steps = 0;
-        bool pad_writer = true;
-        if constexpr (PASS == kPassShadow) {
-            // ---- EXTENSION: shadow geodesics.  Lane = (pixel, light): lpp lights
-            // of 32/lpp pixels march together; contributions are summed across
-            // the lanes of a pixel; light groups beyond lpp loop.
-            const int ppu = kUnit / L.lpp;
-            const int li = lane / ppu;
-            HitRec hr{};
-            if (live) hr = L.hits[pix];
-            const bool hit = live && (hr.status == 1);
-            const F3 q = f3(hr.p[0], hr.p[1], hr.p[2]);
-            const F3 n = f3(hr.n[0], hr.n[1], hr.n[2]);
-            float contrib = 0.f;
-            for (int lg = 0; lg < P.n_lights; lg += L.lpp) {
-                const int l = lg + li;
-                const DevLight& Lt = P.lights[l < P.n_lights ? l : 0];
-                const F3 D = f3(Lt.pos[0] - q.x, Lt.pos[1] - q.y, Lt.pos[2] - q.z);
-                const float dist2 = D.x * D.x + D.y * D.y + D.z * D.z;
-                const float lam = (n.x * D.x + n.y * D.y + n.z * D.z) * rsqrtf(dist2);
-                bool want = hit && l < P.n_lights && lam > 0.f;
-                F3 x0 = f3(0.f, 0.f, 0.f), v0 = f3(0.f, 0.f, 0.f);
-                if (want) {
-                    x0 = f3(fmaf(kShadowEps, n.x, q.x), fmaf(kShadowEps, n.y, q.y),
-                            fmaf(kShadowEps, n.z, q.z));
-                    float g[6];
-                    bool ok;
-                    metric_at(P, x0, g, ok);
-                    const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
-                                     2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
-                    const float inv = rsqrtf(n2);
-                    v0 = f3(D.x * inv, D.y * inv, D.z * inv);
-                    want = ok;
-                }
-                const RayResult sr = march_unit<KIND, NB, SCHEME, kPassShadow, MESH>(P, want, x0, v0, cnt, q, dist2);
-                if (want) shadow_steps += (unsigned)sr.steps;   // reference-equivalent steps
-                if (want && sr.status == 1) contrib = fmaf(Lt.intensity, lam, contrib);
-            }
-            // sum over the lanes of a pixel (same lane % ppu), in light order
-            for (int o = ppu; o < kUnit; o <<= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
-            if (live && li == 0) {
-                RayResult r{hr.status, 0, 0, hr.t, q, n};
-                shade(P, r, L.rgb + 3 * pix, P.ambient + contrib);
-            }
-            pad_writer = li == 0;     // one writer per pixel for the tile padding
-        } else {
-            const RayResult r = march_unit<KIND, NB, SCHEME, PASS, MESH>(P, live, pos, dir, cnt);
-            ref_steps = live ? (unsigned)r.steps : 0u;
-            errs = (live && r.status == 2) ? 1u : 0u;
-            if (live) {
-                if (L.mode == kModeRays) {
-                    uint8_t* o = L.outcomes + 48 * ray_index;      // render::PixelOutcome
-                    o[0] = (uint8_t)r.status;
-                    *reinterpret_cast<int*>(o + 4) = r.status == 1 ? r.prim : -1;
-                    double* pt = reinterpret_cast<double*>(o + 8);
-                    pt[0] = r.status == 1 ? (double)r.point.x : 0.0;
-                    pt[1] = r.status == 1 ? (double)r.point.y : 0.0;
-                    pt[2] = r.status == 1 ? (double)r.point.z : 0.0;
-                    *reinterpret_cast<double*>(o + 32) = r.status == 1 ? (double)r.t : 0.0;
-                    *reinterpret_cast<int*>(o + 40) = r.steps;
-                } else if constexpr (PASS == kPassHits) {
-                    HitRec hr;
-                    hr.p[0] = r.point.x;
-                    hr.p[1] = r.point.y;
-                    hr.p[2] = r.point.z;
-                    hr.t = r.t;
-                    hr.n[0] = r.normal.x;
-                    hr.n[1] = r.normal.y;
-                    hr.n[2] = r.normal.z;
-                    hr.status = r.status;
-                    L.hits[pix] = hr;
-                } else {
-                    shade(P, r, L.rgb + 3 * pix);
-                }
-            } else if (L.mode == kModeTiles && PASS == kPassShade) {
-                uint8_t* dst = L.rgb + 3 * pix;                    // zero partial-tile padding
-                dst[0] = dst[1] = dst[2] = 0;
-            }
-        }
-        if (PASS == kPassShadow && !live && pad_writer && L.mode == kModeTiles) {
-            uint8_t* dst = L.rgb + 3 * pix;
-            dst[0] = dst[1] = dst[2] = 0;
-        }
-        // per-unit counters: one REDUX per counter, one 64-bit atomic per warp
-        const unsigned steps = __reduce_add_sync(kFull, ref_steps);
-        const unsigned nerr = __reduce_add_sync(kFull, errs);
-        const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
-        const unsigned evals = __reduce_add_sync(kFull, cnt.bump_evals);
-        const unsigned nr = __reduce_add_sync(kFull, (live && PASS != kPassShadow) ? 1u : 0u);
-        const unsigned shs = __reduce_add_sync(kFull, shadow_steps);
-        const unsigned slots = __reduce_add_sync(kFull, cnt.lane_slots);
-        if (lane == 0) {
-            if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
-            if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
-            if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
-            if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
-            if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
-            if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
-            if (slots) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), (unsigned long long)slots);
-        }
-    }
-    // Sharded frame mode may write into another GPU's frame (peer/IPC mapping):
-    // make the stores visible system-wide before the kernel retires, ahead of
-    // the cross-rank synchronisation that hands the frame to its owner.
-    if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
-}
-
-
-// ---------------------------------------------------------------------------
-// Ray-pair frame kernel (Gaussian bumps, RK4, no meshes; frame and tile
-// modes).  A unit is two consecutive micro-tiles of march_kernel's order
-// (ray 0 of a thread in micro-tile 2u, ray 1 in 2u+1, same lane position),
-// so tiles remain unions of units (byte-identical frames across shard
-// counts).  L.n_units counts micro-tiles; the kernel serves (n+1)/2 units.
-// With lights the shadow pass marches light by light (lpp = 1).
-__device__ __forceinline__ void pixel_of(const DevLaunch& L, unsigned mt, int lane, bool& inrange,
-                                         bool& live, int& px, int& py, unsigned long long& pix) {
-    inrange = mt < L.n_units;
-    const unsigned m = inrange ? mt : 0u;
-    const unsigned long long tile_k = m / L.micro_per_tile;
-    const unsigned micro = m % L.micro_per_tile;
-    const unsigned tile = L.shard + (unsigned)tile_k * L.n_shards;
-    const int tx = tile % L.tiles_x, ty = tile / L.tiles_x;
-    const int mpr = L.tile_w / kMicroW;
-    const int lx = (micro % mpr) * kMicroW + (lane & 7);
-    const int ly = (micro / mpr) * kMicroH + (lane >> 3);
-    px = tx * L.tile_w + lx;
-    py = ty * L.tile_h + ly;
-    live = inrange && px < L.width && py < L.height;
-    pix = L.mode == kModeFrame ? (unsigned long long)py * L.width + px
-                               : tile_k * L.tile_w * L.tile_h + (unsigned long long)ly * L.tile_w + lx;
-}
-
-// Output of a terminated primary ray of a pair unit (pixel recomputed from
-// the unit, so no output addresses stay live through the march).
-template <int PASS>
-__device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
-                                             int r, const RayResult& res) {
-    bool inr, live;
-    int px, py;
-    unsigned long long pix;
-    pixel_of(L, 2 * unit + r, threadIdx.x & 31, inr, live, px, py, pix);
-    if constexpr (PASS == kPassHits) {
-        HitRec h;
-        h.p[0] = res.point.x;
-        h.p[1] = res.point.y;
-        h.p[2] = res.point.z;
-        h.t = res.t;
-        h.n[0] = res.normal.x;
-        h.n[1] = res.normal.y;
-        h.n[2] = res.normal.z;
-        h.status = res.status;
-        L.hits[pix] = h;
-    } else if constexpr (PASS == kPassShade) {
-        shade(P, res, L.rgb + 3 * pix);
-    }
-}
-
-// Per-warp accounting of one work unit, flushed with one atomic per field.
-struct UnitStats {
-    LaneCounters cnt;
-    unsigned ref_steps, errs, shadow_steps, nrays;
-};
-
-__device__ __forceinline__ void flush_unit_stats(const DevLaunch& L, const UnitStats& us, int lane,
-                                                 bool shadow) {
-    const unsigned steps = __reduce_add_sync(kFull, us.ref_steps);
-    const unsigned nerr = __reduce_add_sync(kFull, us.errs);
-    const unsigned integ = __reduce_add_sync(kFull, us.cnt.steps_integrated);
-    const unsigned evals = __reduce_add_sync(kFull, us.cnt.bump_evals);
-    const unsigned nr = __reduce_add_sync(kFull, us.nrays);
-    const unsigned shs = __reduce_add_sync(kFull, us.shadow_steps);
-    const unsigned slots = __reduce_add_sync(kFull, us.cnt.lane_slots);
-    if (lane == 0) {
-        if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
-        if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
-        if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
-        if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
-        if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
-        if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
-        if (slots) atomicAdd(L.stats + (shadow ? 7 : 6), (unsigned long long)slots);
-    }
-}
-
-// Primary rays of ray-pair unit `unit` (64 pixels: micro-tiles 2 unit, 2 unit
-// + 1): raygen, march, and either the fused shading (kPassShade) or hit
-// records for the shadow work (kPassHits).
-template <int NB, int PASS>
-__device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
-                                             int lane, UnitStats& us) {
-    bool inr[2], live[2];
-    int px[2], py[2];
-    unsigned long long pix[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
-    F3 pos[2], dir[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (live[r]) raygen(L.cam, px[r], py[r], L.width, L.height, pos[r], dir[r]);
-        else pos[r] = dir[r] = f3(0.f, 0.f, 0.f);
-    }
-    int st[2], stp[2];
-    float tt[2];
-    F3 pt[2];
-    march_pair<NB, PASS>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
-                         us.cnt, L, unit, st, stp, tt, pt);
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (live[r]) {
-            us.ref_steps += (unsigned)stp[r];
-            us.errs += st[r] == 2 ? 1u : 0u;
-            us.nrays += 1;
-            if constexpr (PASS == kPassShade) {
-                RayResult res{st[r], 0, 0, tt[r], pt[r], f3(0.f, 0.f, 0.f)};
-                shade(P, res, L.rgb + 3 * pix[r]);
-            }
-        } else if (inr[r] && L.mode == kModeTiles && PASS == kPassShade) {
-            uint8_t* dst = L.rgb + 3 * pix[r];                // zero partial-tile padding
-            dst[0] = dst[1] = dst[2] = 0;
-        }
-    }
-}
-
-// ---- EXTENSION: shadow geodesics (oracle/rro.c shadow_march) of ray-pair
-// unit `unit` toward light `l`.  Each (unit, light) is its own work item, so
-// the expensive shadow work is split finely across warps; the visibility
-// byte of every (pixel, light) is published and the unit's LAST light to
-// finish (per-unit counter L.done) shades its 64 pixels, summing the lit
-// contributions in light order (shade_lit in oracle/rro.c).
-template <int NB>
-__device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch& L, unsigned unit,
-                                            int l, int nl, int lane, UnitStats& us) {
-    bool inr[2], live[2];
-    int px[2], py[2];
-    unsigned long long pix[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) pixel_of(L, 2 * unit + r, lane, inr[r], live[r], px[r], py[r], pix[r]);
-    int status[2] = {0, 0};
-    float thit[2] = {0.f, 0.f};
-    F3 q[2], n[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (live[r]) {   // L2 loads: in the fused kernel the records were written by other SMs
-            const float4* hp = reinterpret_cast<const float4*>(L.hits + pix[r]);
-            a = __ldcg(hp);
-            b = __ldcg(hp + 1);
-        }
-        q[r] = f3(a.x, a.y, a.z);
-        thit[r] = a.w;
-        n[r] = f3(b.x, b.y, b.z);
-        status[r] = __float_as_int(b.w);
-    }
-    const DevLight& Lt = P.lights[l];
-    bool want[2];
-    float dist2[2];
-    F3 x0[2], v0[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const F3 D = f3(Lt.pos[0] - q[r].x, Lt.pos[1] - q[r].y, Lt.pos[2] - q[r].z);
-        dist2[r] = D.x * D.x + D.y * D.y + D.z * D.z;
-        const float lam = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(dist2[r]);
-        want[r] = live[r] && status[r] == 1 && lam > 0.f;
-        x0[r] = v0[r] = f3(0.f, 0.f, 0.f);
-        if (want[r]) {
-            x0[r] = f3(fmaf(kShadowEps, n[r].x, q[r].x), fmaf(kShadowEps, n[r].y, q[r].y),
-                       fmaf(kShadowEps, n[r].z, q[r].z));
-            float g[6];
-            bool ok;
-            metric_at(P, x0[r], g, ok);
-            const float n2 = g[0] * D.x * D.x + g[3] * D.y * D.y + g[5] * D.z * D.z +
-                             2.f * (g[1] * D.x * D.y + g[2] * D.x * D.z + g[4] * D.y * D.z);
-            const float inv = rsqrtf(n2);
-            v0[r] = f3(D.x * inv, D.y * inv, D.z * inv);
-            want[r] = ok;
-        }
-    }
-    int sst[2], sstp[2];
-    float tdum[2];
-    F3 pdum[2];
-    march_pair<NB, kPassShadow>(P, want[0], want[1], pair_of(x0[0], x0[1]), pair_of(v0[0], v0[1]),
-                                us.cnt, L, unit, sst, sstp, tdum, pdum, q[0], q[1], dist2[0], dist2[1]);
-    bool vis[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (want[r]) us.shadow_steps += (unsigned)sstp[r];   // reference-equivalent steps
-        vis[r] = want[r] && sst[r] == 1;
-    }
-    bool last = true;
-    if (nl > 1) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (live[r]) L.vis[pix[r] * (unsigned)nl + l] = vis[r] ? 1 : 0;
-        __threadfence();
-        __syncwarp();
-        unsigned before = 0;
-        if (lane == 0) before = atomicAdd(L.done + unit, 1u);
-        before = __shfl_sync(kFull, before, 0);
-        last = before == (unsigned)nl - 1u;
-        if (last) __threadfence();
-    }
-    if (!last) return;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (live[r]) {
-            float contrib = 0.f;
-            if (status[r] == 1) {
-                for (int k = 0; k < nl; ++k) {
-                    const bool lit = k == l ? vis[r] : __ldcg(L.vis + pix[r] * (unsigned)nl + k) != 0;
-                    if (!lit) continue;
-                    const DevLight& Lk = P.lights[k];
-                    const F3 D = f3(Lk.pos[0] - q[r].x, Lk.pos[1] - q[r].y, Lk.pos[2] - q[r].z);
-                    const float d2 = D.x * D.x + D.y * D.y + D.z * D.z;
-                    const float lam = (n[r].x * D.x + n[r].y * D.y + n[r].z * D.z) * rsqrtf(d2);
-                    contrib = fmaf(Lk.intensity, lam, contrib);
-                }
-            }
-            RayResult rr{status[r], 0, 0, thit[r], q[r], n[r]};
-            shade(P, rr, L.rgb + 3 * pix[r], P.ambient + contrib);
-        } else if (inr[r] && L.mode == kModeTiles) {
-            uint8_t* dst = L.rgb + 3 * pix[r];
-            dst[0] = dst[1] = dst[2] = 0;
-        }
-    }
-}
-
-// Ray-pair persistent kernel.  Work items are dispensed by one atomic
-// counter:
-//   kPassShade  : n_pairs primary units with fused shading (no lights);
-//   kPassHits   : n_pairs primary units writing hit records;
-//   kPassShadow : n_pairs x n_lights shadow units (after a kPassHits launch);
-//   kPassFused  : the two above in ONE launch — primary units first, then the
-//                 shadow units; a shadow unit waits (rarely: it was dispensed
-//                 n_pairs items later) for its primary unit's ready flag, so
-//                 the frame has one tail instead of two and no launch gap.
-//                 No deadlock: a flag's producer already holds a running warp
-//                 and waits on nothing.
-template <int NB, int PASS>
-__global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
-                                               : (PASS == kPassFused ? RR_MIN_BLOCKS_X2_FUSED
-                                                                     : RR_MIN_BLOCKS_X2))
-march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
-    const int lane = threadIdx.x & 31;
-    const unsigned n_pairs = (L.n_units + 1) / 2;
-    constexpr bool kShadowWork = PASS == kPassShadow || PASS == kPassFused;
-    const int nl = kShadowWork ? P.n_lights : 1;
-    const unsigned n_primary = PASS == kPassShadow ? 0u : n_pairs;
-    const unsigned n_work = n_primary + (kShadowWork ? n_pairs * (unsigned)nl : 0u);
-    auto fetch = [&]() {
-        unsigned w = 0;
-        if (lane == 0) w = atomicAdd(L.counter, 1u);
-        return __shfl_sync(kFull, w, 0);
-    };
-    // Two sequential loops (no if/else between the unit kinds inside one
-    // loop body: that made ptxas treat the bump loops as divergent and drop
-    // their uniform-datapath constant loads).  The warp whose fetch crosses
-    // n_primary carries that item into the shadow loop.
-    unsigned work = fetch();
-    if constexpr (PASS != kPassShadow) {
-        constexpr int kPrim = PASS == kPassFused ? kPassHits : PASS;
-        while (work < n_primary) {
-            UnitStats us{};
-            pair_primary<NB, kPrim>(P, L, work, lane, us);
-            if constexpr (PASS == kPassFused) {                 // publish the hit records
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) atomicExch(L.ready + work, 1u);
-            }
-            flush_unit_stats(L, us, lane, false);
-            work = fetch();
-        }
-    }
-    if constexpr (kShadowWork) {
-        while (work < n_work) {
-            const unsigned w = work - n_primary;
-            const unsigned unit = w / (unsigned)nl;
-            if constexpr (PASS == kPassFused) {
-                // whole-warp polling of the unit's ready flag (dispensed
-                // n_pairs items after its primary unit: normally already set)
-                for (;;) {
-                    unsigned f = 0;
-                    if (lane == 0) f = atomicAdd(L.ready + unit, 0u);
-                    if (__shfl_sync(kFull, f, 0)) break;
-                    __nanosleep(256);
-                }
-                __threadfence();
-            }
-            UnitStats us{};
-            pair_shadow<NB>(P, L, unit, (int)(w % (unsigned)nl), nl, lane, us);
-            flush_unit_stats(L, us, lane, true);
-            work = fetch();
-        }
-    }
-    if (L.mode == kModeFrame && L.n_shards > 1) __threadfence_system();
-}
 
 // ---------------------------------------------------------------------------
 // Culling grid build on the device (per scene upload, e.g. every animation
@@ -2281,144 +188,6 @@ __global__ void __launch_bounds__(128) accel_points_kernel(const __grid_constant
     validity[r] = KIND == kDiffeo ? (double)valid : 1.0;
 }
 
-template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-int occupancy_of() {
-    static int occ = [] {
-        int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<KIND, NB, SCHEME, PASS, MESH>,
-                                                      kThreads, 0);
-        return n > 0 ? n : 1;
-    }();
-    return occ;
-}
-
-template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
-cudaError_t launch_pass(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    const unsigned warps_needed = L.n_units;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of<KIND, NB, SCHEME, PASS, MESH>());
-    const unsigned max_useful = (warps_needed + 3) / 4;
-    if (blocks > max_useful) blocks = max_useful;
-    if (blocks == 0) blocks = 1;
-    march_kernel<KIND, NB, SCHEME, PASS, MESH><<<blocks, kThreads, 0, s>>>(P, L);
-    return cudaGetLastError();
-}
-
-template <int NB, int PASS>
-int occupancy_of2() {
-    static int occ = [] {
-        int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march2_kernel<NB, PASS>, kThreads, 0);
-        return n > 0 ? n : 1;
-    }();
-    return occ;
-}
-
-template <int NB, int PASS>
-cudaError_t launch_pass2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    const unsigned warps_needed = (L.n_units + 1) / 2;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of2<NB, PASS>());
-    const unsigned max_useful = (warps_needed + 3) / 4;
-    if (blocks > max_useful) blocks = max_useful;
-    if (blocks == 0) blocks = 1;
-    march2_kernel<NB, PASS><<<blocks, kThreads, 0, s>>>(P, L);
-    return cudaGetLastError();
-}
-
-template <int NB>
-cudaError_t launch_variant2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    if (P.n_lights == 0) return launch_pass2<NB, kPassShade>(P, L, s, num_sms);
-#if RR_X2_FUSED
-    return launch_pass2<NB, kPassFused>(P, L, s, num_sms);
-#endif
-    cudaError_t e = launch_pass2<NB, kPassHits>(P, L, s, num_sms);
-    if (e != cudaSuccess) return e;
-    DevLaunch L2 = L;
-    L2.counter = L.counter + 1;
-    L2.lpp = 1;
-    return launch_pass2<NB, kPassShadow>(P, L2, s, num_sms);
-}
-
-// Without lights: one fused launch.  With lights (EXTENSION): a hit-record
-// pass and a shadow+shade pass over the same units (each with its own unit
-// counter: L.counter[0] and L.counter[1]).  Scenes with meshes use the MESH
-// variants (BVH traversal compiled in; kept out of the mesh-free kernels).
-template <int KIND, int NB, int SCHEME, bool MESH>
-cudaError_t launch_variant(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    if (P.n_lights == 0 || L.mode == kModeRays)
-        return launch_pass<KIND, NB, SCHEME, kPassShade, MESH>(P, L, s, num_sms);
-    cudaError_t e = launch_pass<KIND, NB, SCHEME, kPassHits, MESH>(P, L, s, num_sms);
-    if (e != cudaSuccess) return e;
-    DevLaunch L2 = L;
-    L2.counter = L.counter + 1;
-    // lights per pixel marched in one unit: 1.  Pairing 2 lights x 16 pixels per
-    // warp was measured slower on C3 (27.2 vs 23.7 ms/frame): two light
-    // directions in one warp widen the culling union and split coherence.
-    L2.lpp = 1;
-    L2.n_units = L.n_units * L2.lpp;
-    return launch_pass<KIND, NB, SCHEME, kPassShadow, MESH>(P, L2, s, num_sms);
-}
-
-template <int SCHEME, bool MESH>
-cudaError_t dispatch_kind(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
-                          const char** name) {
-    switch (P.kind) {
-        case kEuclid:
-            *name = MESH ? "march_kernel<euclid,mesh>" : "march_kernel<euclid>";
-            return launch_variant<kEuclid, 0, SCHEME, MESH>(P, L, s, sms);
-        case kBumps:
-#if RR_RAY_PAIRS
-            if constexpr (!MESH && SCHEME == 1) {   // ray-pair frames (RK4, mesh-free)
-                if (L.mode != kModeRays) {
-                    if (P.nb_slot <= 4) {
-                        *name = "march2_kernel<bumps4>";
-                        return launch_variant2<4>(P, L, s, sms);
-                    }
-                    if (P.nb_slot <= 8) {
-                        *name = "march2_kernel<bumps8>";
-                        return launch_variant2<8>(P, L, s, sms);
-                    }
-                    if (P.nb_slot <= 16) {
-                        *name = "march2_kernel<bumps16>";
-                        return launch_variant2<16>(P, L, s, sms);
-                    }
-                    *name = "march2_kernel<bumps32>";
-                    return launch_variant2<32>(P, L, s, sms);
-                }
-            }
-#endif
-            if constexpr (!MESH && SCHEME != 2) {   // mesh / rk23 scenes use 16/32 slots only
-                if (P.nb_slot <= 4) {
-                    *name = "march_kernel<bumps4>";
-                    return launch_variant<kBumps, 4, SCHEME, MESH>(P, L, s, sms);
-                }
-                if (P.nb_slot <= 8) {
-                    *name = "march_kernel<bumps8>";
-                    return launch_variant<kBumps, 8, SCHEME, MESH>(P, L, s, sms);
-                }
-            }
-            if (P.nb_slot <= 16) {
-                *name = MESH ? "march_kernel<bumps16,mesh>" : "march_kernel<bumps16>";
-                return launch_variant<kBumps, 16, SCHEME, MESH>(P, L, s, sms);
-            }
-            *name = MESH ? "march_kernel<bumps32,mesh>" : "march_kernel<bumps32>";
-            return launch_variant<kBumps, 32, SCHEME, MESH>(P, L, s, sms);
-        case kGraphGeneral:
-            *name = MESH ? "march_kernel<graph,mesh>" : "march_kernel<graph>";
-            return launch_variant<kGraphGeneral, 0, SCHEME, MESH>(P, L, s, sms);
-        default:
-            *name = MESH ? "march_kernel<diffeo,mesh>" : "march_kernel<diffeo>";
-            return launch_variant<kDiffeo, 0, SCHEME, MESH>(P, L, s, sms);
-    }
-}
-
-template <int SCHEME>
-cudaError_t dispatch_scheme(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
-                            const char** name) {
-    return P.n_meshes > 0 ? dispatch_kind<SCHEME, true>(P, L, s, sms, name)
-                          : dispatch_kind<SCHEME, false>(P, L, s, sms, name);
-}
-
-
 template <int KIND, int NB>
 cudaError_t trace_kind(const DevParams& P, const double* starts, int n, float h, int max_steps,
                        int scheme, int use_bounds, double* states, int* counts, int* fail,
@@ -2434,6 +203,7 @@ cudaError_t trace_kind(const DevParams& P, const double* starts, int n, float h,
 }
 
 } // namespace
+
 
 cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float h, int max_steps,
                          int scheme, int use_bounds, double* states, int* counts, int* fail,
@@ -2484,9 +254,20 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
                            P.n_meshes == 0;
         *launches = lit && !fused ? 2 : 1;
     }
-    if (P.scheme == 2) return dispatch_scheme<2>(P, L, stream, num_sms, kernel_name);
-    return P.scheme == 0 ? dispatch_scheme<0>(P, L, stream, num_sms, kernel_name)
-                         : dispatch_scheme<1>(P, L, stream, num_sms, kernel_name);
+    switch (P.kind) {
+        case kEuclid:
+            return launch_family_euclid(P, L, stream, num_sms, kernel_name);
+        case kBumps:
+#if RR_RAY_PAIRS
+            if (P.scheme == 1 && P.n_meshes == 0)   // ray-pair frames and batches (RK4, mesh-free)
+                return launch_family_pair(P, L, stream, num_sms, kernel_name);
+#endif
+            return launch_family_bumps(P, L, stream, num_sms, kernel_name);
+        case kGraphGeneral:
+            return launch_family_graph(P, L, stream, num_sms, kernel_name);
+        default:
+            return launch_family_diffeo(P, L, stream, num_sms, kernel_name);
+    }
 }
 
 cudaError_t launch_cull_build(const double* d_gauss, int n, int G, const double lo[3],

@@ -41,10 +41,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         if _lib is None:
             if not os.path.exists(path):
                 raise DeviceError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-            lib = abi.bind(C.CDLL(path))
-            lib.rr_last_kernel.restype = C.c_char_p
-            lib.rr_last_kernel.argtypes = [C.c_void_p]
-            _lib = lib
+            _lib = abi.bind(C.CDLL(path))
         return _lib
 
 
@@ -151,6 +148,18 @@ class Renderer:
         self._check(self.lib.rr_render(self.ctx, C.byref(cam), C.byref(it), width, height,
                                        _addr(out), C.byref(st)))
         return out, st.as_dict()
+
+    def render_outcomes(self, cam: abi.rr_camera, integ: IntegratorConfig, width: int,
+                        height: int, rgb=True):
+        """The frame kernel with its PixelOutcome sink -> (rgb or None,
+        outcomes[h*w] row-major, stats): per-pixel parity of the frame path."""
+        out = np.zeros(width * height, abi.OUTCOME_DTYPE)
+        img = np.zeros((height, width, 3), np.uint8) if rgb else None
+        st = abi.rr_stats()
+        it = integ.to_abi()
+        self._check(self.lib.rr_render_outcomes(self.ctx, C.byref(cam), C.byref(it), width, height,
+                                                _addr(img), _addr(out), C.byref(st)))
+        return img, out, st.as_dict()
 
     def render_device(self, cam, integ: IntegratorConfig, width: int, height: int, d_rgb,
                       stream=None, with_stats: bool = False):

@@ -43,7 +43,7 @@ def test_march_matches_reference_golden(renderer, name):
     out = renderer.march(cfg.integrator, z["rays"])
     rep = compare_outcomes(out, z["outcomes"], z["flags"])
     assert rep.ok, rep.summary() + " " + "; ".join(rep.details)
-    assert renderer.last_kernel.startswith("march_kernel")
+    assert renderer.last_kernel.startswith("march")
 
 
 @pytest.mark.parametrize("name", golden_cases())

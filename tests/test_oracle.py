@@ -144,3 +144,62 @@ def test_oracle_against_live_reference(oracle_lib, reference_lib):
         rays = reference_lib.primary_rays(reference_json(cfg), 24, 16)
         ref = reference_lib.march(reference_json(cfg), rays, "scalar")
         assert outcomes_identical(oracle_lib.march(cfg, rays), ref)
+
+
+def test_oracle_row_subsample_and_pixel_flags_match_full_frame(oracle_lib):
+    """rro_render_rows / rro_flags_pixels (the full-size parity machinery)
+    reproduce the whole-frame rro_render / rro_flags bytes, lights included."""
+    import os
+    from conftest import ROOT
+    from paper_2005_05386_b200.config import load_config
+    cfg = load_config(os.path.join(ROOT, "configs", "c3_bumps16_shadows_1080p.json"))
+    w, h = 64, 36
+    rgb, out, st, flags = oracle_lib.render(cfg, w, h, with_flags=True)
+    r_rgb, r_out, r_st = oracle_lib.render_rows(cfg, w, h, 1, 3)
+    rows = list(range(1, h, 3))
+    assert np.array_equal(r_rgb, rgb[rows])
+    assert outcomes_identical(r_out, out.reshape(h, w)[rows].reshape(-1))
+    assert r_st["rays"] == len(rows) * w and r_st["wall_seconds"] > 0
+    pix = np.arange(0, w * h, 7, dtype=np.int64)
+    f = oracle_lib.flags_pixels(cfg, w, h, pix, out[pix])
+    assert np.array_equal(f, flags[pix])
+
+
+def test_check_frame_flags_only_failing_pixels(oracle_lib):
+    """oracle.parity.check_frame: identical outcomes need no flags; a broken
+    pixel is reported unless the oracle flags it."""
+    import os
+    from conftest import ROOT
+    from oracle.parity import check_frame
+    from paper_2005_05386_b200.config import load_config
+    cfg = load_config(os.path.join(ROOT, "configs", "c1_gauss1_512.json"))
+    w, h = 48, 32
+    rgb, out, _, _ = oracle_lib.render(cfg, w, h)
+    calls = []
+
+    def flag_fn(idx):
+        calls.append(len(idx))
+        return oracle_lib.flags_pixels(cfg, w, h, idx, out[idx])
+
+    rep, _, cand = check_frame(out, out, rgb, rgb, flag_fn)
+    assert rep.ok and cand == 0 and not calls
+    bad = out.copy()
+    i = int(np.nonzero(out["status"] == 1)[0][0])
+    bad["point"][i] += 1.0
+    rep, _, cand = check_frame(bad, out, rgb, rgb, flag_fn)
+    assert cand == 1 and calls == [1] and rep.endpoint_fail == 1 and not rep.ok
+
+
+def test_reference_row_outcomes_match_oracle(reference_lib, oracle_lib):
+    """refc_render_rows' outcome records (the reference's own MarchFn per row)
+    are bit-identical to the oracle's row subsample."""
+    import os
+    from conftest import ROOT
+    from paper_2005_05386_b200.config import load_config
+    cfg = load_config(os.path.join(ROOT, "configs", "c3_bumps16_1080p.json"))
+    w, h = 96, 54
+    rgb, out, st = reference_lib.render_rows(cfg, w, h, 2, 5, kernel="avx2", workers=4,
+                                             with_outcomes=True)
+    o_rgb, o_out, _ = oracle_lib.render_rows(cfg, w, h, 2, 5)
+    assert outcomes_identical(out, o_out)
+    assert np.array_equal(rgb, o_rgb)
