@@ -290,6 +290,10 @@ def cpu_sample(kind, cfg, w, h, target_s=4.0, kernel="avx2", workers=0):
         wall, _, _ = run(step0)
         per_row = wall / len(range(0, h, step0))
         step = max(1, min(h, math.ceil(h * per_row / target_s)))
+        # at least 4 rows per thread: the row is the work item, and a sample
+        # of fewer rows than threads would under-report the CPU's throughput
+        threads = workers or os.cpu_count() or 1
+        step = max(1, min(step, h // (4 * threads)))
         wall, steps, cores = run(step)
         rows = len(range(0, h, step))
         label = (f"reference render() row work items, KernelKind::{kernel.capitalize()}"
@@ -413,20 +417,27 @@ def run_b200(args, cfg):
         # the completion barrier.  Fallback: tile buffers + one NCCL gather +
         # detile on rank 0.
         exchange = "p2p-epilogue"
-        target = frame
+        target = frame.data_ptr()
+        ok = 1
         try:
-            from torch.multiprocessing.reductions import reduce_tensor
-            payload = [reduce_tensor(frame)] if rank == 0 else [None]
+            # library-owned mapping (rr_frame_export / rr_frame_import on this
+            # rank's own device, peer access enabled where supported)
+            payload = [r.frame_export(frame) if rank == 0 else None]
             dist.broadcast_object_list(payload, src=0)
             if rank != 0:
-                fn, fargs = payload[0]
-                target = fn(*fargs)
-            ok = torch.tensor([1], device=cdev)
+                target = r.frame_import(payload[0])
+            torch.cuda.synchronize()
+            dist.barrier()
+            r.frame_probe(target, rank, rank + 1)     # device-side store through the mapping
         except Exception:
-            ok = torch.tensor([0], device=cdev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0 or gloo:
-            exchange = "p2p-epilogue" if int(ok.item()) else "nccl-gather"
+            ok = 0
+        dist.barrier()
+        if rank == 0 and ok:
+            ok = int(frame.view(-1)[:world].cpu().tolist() == list(range(1, world + 1)))
+        okt = torch.tensor([ok], device=cdev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if int(okt.item()) == 0:
+            exchange = "nccl-gather"
         done = torch.zeros(1, device=cdev)
         max_k = r.shard_tile_count(w, h, TILE, TILE, 0, world)
         tiles = torch.zeros(max_k * TILE * TILE * 3, dtype=torch.uint8, device="cuda")
@@ -565,7 +576,8 @@ def run_b200(args, cfg):
                    "avg_steps_per_ray": est["total_steps"] / (ew * eh),
                    "simt_efficiency": simt(est),
                    "kernel": r.last_kernel}
-            if ecfg.metric.kind == "euclidean":
+            mkind = type(ecfg.metric).__name__          # EuclideanMetric / GraphMetric / DiffeoMetric
+            if mkind == "EuclideanMetric":
                 # Euclidean rays jump straight to their exit/hit: the reference-
                 # equivalent steps/s is mostly skipped work, not throughput
                 ent["note"] = ("steps_per_s counts reference-equivalent steps; Gamma = 0 rays "
@@ -574,7 +586,7 @@ def run_b200(args, cfg):
             else:
                 ent["rk4_steps_per_s"] = rk4_steps(est) / (ems * 1e-3)
                 eflop = algorithmic_flops(est, ecfg.integrator.scheme)
-                if ecfg.metric.kind == "graph":
+                if mkind == "GraphMetric":
                     ent["achieved_tflops"] = eflop / (ems * 1e-3) / 1e12
                     ent["frac"] = ent["achieved_tflops"] / peak
             if not args.no_cpu_baseline:
@@ -669,9 +681,9 @@ def run_b200(args, cfg):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
-        if rank != 0:
-            target = None             # drop the IPC mapping before rank 0 frees its frame
-            torch.cuda.synchronize()
+        if rank != 0 and exchange == "p2p-epilogue":
+            r.frame_close(target)     # drop the IPC mapping before rank 0 frees its frame
+        torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
     r.close()

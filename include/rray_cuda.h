@@ -320,6 +320,37 @@ int rr_render_shard(rr_ctx* ctx, const rr_camera* cam, const rr_integrator* inte
                     int height, int tile_w, int tile_h, int shard, int n_shards,
                     uint8_t* d_frame, rr_stats* stats, void* stream);
 
+/* ---- cross-process / cross-device frame exchange ----------
+ * The reference renders in one process (render.cpp:96-104); on a multi-GPU
+ * node one process drives each GPU and rr_render_shard's epilogue stores its
+ * pixels straight into rank 0's frame.  These calls make that mapping the
+ * library's business: the frame's owner exports its device buffer, every
+ * other process imports it ON ITS OWN CONTEXT'S DEVICE (cudaIpcOpenMemHandle
+ * with lazy peer access, after enabling peer access where the devices
+ * support it), proves the mapping with a device-side store, and closes it
+ * before the owner frees the frame. */
+typedef struct rr_frame_handle {
+    unsigned char ipc[64];            /* cudaIpcMemHandle_t of the allocation holding the frame */
+    uint64_t offset;                  /* byte offset of the frame inside that allocation */
+    uint64_t bytes;                   /* frame size in bytes */
+    uint64_t ptr;                     /* exporter's device address (same-process imports) */
+    int32_t device;                   /* exporter's CUDA ordinal */
+    int32_t pid;                      /* exporter's process id */
+} rr_frame_handle;
+
+/* Handle for `bytes` of device memory at d_frame (on ctx's device; any
+ * cudaMalloc'd or caching-allocator sub-allocation). */
+int rr_frame_export(rr_ctx* ctx, const void* d_frame, size_t bytes, rr_frame_handle* out);
+/* Maps an exported frame into this context's device; *d_frame is a device
+ * address usable as rr_render_shard's d_frame on ctx's device. */
+int rr_frame_import(rr_ctx* ctx, const rr_frame_handle* h, void** d_frame);
+/* Unmaps an imported frame (no-op for same-process imports). */
+int rr_frame_close(rr_ctx* ctx, void* d_frame);
+/* One device-side store of `value` at d_frame + offset from ctx's device,
+ * fenced system-wide and synchronised: a failing mapping returns status 4
+ * instead of faulting the first frame. */
+int rr_frame_probe(rr_ctx* ctx, void* d_frame, size_t offset, uint8_t value);
+
 /* Reassembles a frame from the concatenation of every shard's tile buffer
  * (shard 0 first, each padded to the largest shard's tile count). */
 int rr_detile(rr_ctx* ctx, const uint8_t* d_gathered, int width, int height, int tile_w,

@@ -123,6 +123,11 @@ class rr_options(C.Structure):
                 ("block_y", C.c_int32), ("persistent", C.c_int32), ("skip", C.c_int32)]
 
 
+class rr_frame_handle(C.Structure):
+    _fields_ = [("ipc", C.c_ubyte * 64), ("offset", C.c_uint64), ("bytes", C.c_uint64),
+                ("ptr", C.c_uint64), ("device", C.c_int32), ("pid", C.c_int32)]
+
+
 RAY_DTYPE = np.dtype([("position", "<f8", (3,)), ("direction", "<f8", (3,))])
 OUTCOME_DTYPE = np.dtype({
     "names": ["status", "prim", "point", "t", "steps"],
@@ -137,7 +142,7 @@ EXPECTED_SIZES = {
     "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
     "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 24,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 112,
-    "rr_options": 32,
+    "rr_options": 32, "rr_frame_handle": 96,
 }
 
 STRUCTS = {
@@ -147,7 +152,7 @@ STRUCTS = {
     "rr_primitive": rr_primitive, "rr_light": rr_light, "rr_scene_desc": rr_scene_desc,
     "rr_integrator": rr_integrator, "rr_ray_start": rr_ray_start,
     "rr_pixel_outcome": rr_pixel_outcome, "rr_camera": rr_camera, "rr_stats": rr_stats,
-    "rr_options": rr_options,
+    "rr_options": rr_options, "rr_frame_handle": rr_frame_handle,
 }
 
 # Every symbol include/rray_cuda.h declares, with its ctypes signature.
@@ -182,6 +187,10 @@ SIGNATURES = {
                                   C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P,
                                   C.POINTER(rr_stats), _P]),
     "rr_detile": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
+    "rr_frame_export": (C.c_int, [_P, _P, C.c_size_t, C.POINTER(rr_frame_handle)]),
+    "rr_frame_import": (C.c_int, [_P, C.POINTER(rr_frame_handle), C.POINTER(_P)]),
+    "rr_frame_close": (C.c_int, [_P, _P]),
+    "rr_frame_probe": (C.c_int, [_P, _P, C.c_size_t, C.c_uint8]),
     "rr_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "rr_trace": (C.c_int, [_P, C.POINTER(rr_integrator), _P, C.c_size_t, C.c_int, _P, _P, _P]),
     "rr_accel": (C.c_int, [_P, _P, _P, C.c_size_t, _P, _P]),

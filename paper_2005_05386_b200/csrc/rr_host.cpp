@@ -15,9 +15,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <unistd.h>
 
 #include "rr_bvh.h"
 #include "rr_device.cuh"
@@ -112,6 +115,7 @@ struct rr_ctx {
     // the previous launch (ev1, recorded after it).
     bool launched = false;
     cudaStream_t last_stream = nullptr;
+    std::map<void*, void*> imports;          // imported frame address -> IPC mapping base
 };
 
 namespace {
@@ -790,6 +794,7 @@ void rr_destroy(rr_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->imports) cudaIpcCloseMemHandle(kv.second);
     if (c->d_masks) cudaFree(c->d_masks);
     if (c->d_skip) cudaFree(c->d_skip);
     if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
@@ -1176,6 +1181,89 @@ int rr_render_shard(rr_ctx* c, const rr_camera* cam, const rr_integrator* integ,
     cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
     if ((rc = run_launch(c, L, s))) return rc;
     if (stats) return collect_stats(c, s, stats, t0);
+    return RR_OK;
+}
+
+int rr_frame_export(rr_ctx* c, const void* d_frame, size_t bytes, rr_frame_handle* out) {
+    if (!c || !d_frame || !out) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    RR_CUDA(c, cudaSetDevice(c->device));
+    std::memset(out, 0, sizeof *out);
+    // the IPC handle names the whole allocation: find its base (driver
+    // cuMemGetAddressRange, fetched at run time so the library does not link
+    // libcuda) so that sub-allocations (torch's caching allocator) work
+    using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static RangeFn range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<RangeFn>(fn);
+    }();
+    const unsigned long long addr = reinterpret_cast<uintptr_t>(d_frame);
+    unsigned long long base = addr;
+    size_t size = bytes;
+    if (range && range(&base, &size, addr) != 0) return set_err(c, RR_ERR_CONFIG, "rr_frame_export: not device memory");
+    if (addr + bytes > base + size) return set_err(c, RR_ERR_CONFIG, "rr_frame_export: frame exceeds its allocation");
+    cudaIpcMemHandle_t h;
+    RR_CUDA(c, cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof h == sizeof out->ipc, "cudaIpcMemHandle_t size");
+    std::memcpy(out->ipc, &h, sizeof h);
+    out->offset = addr - base;
+    out->bytes = bytes;
+    out->ptr = addr;
+    out->device = c->device;
+    out->pid = (int32_t)getpid();
+    return RR_OK;
+}
+
+int rr_frame_import(rr_ctx* c, const rr_frame_handle* h, void** d_frame) {
+    if (!c || !h || !d_frame) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    RR_CUDA(c, cudaSetDevice(c->device));
+    *d_frame = nullptr;
+    if (h->device != c->device) {   // direct peer access where the pair supports it
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, c->device, h->device) == cudaSuccess && can) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(h->device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return cuda_err(c, e, "cudaDeviceEnablePeerAccess");
+        }
+        cudaGetLastError();
+    }
+    if (h->pid == (int32_t)getpid()) {   // same process: the UVA address is valid as is
+        *d_frame = reinterpret_cast<void*>(h->ptr);
+        return RR_OK;
+    }
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, h->ipc, sizeof ih);
+    void* base = nullptr;
+    RR_CUDA(c, cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess));
+    *d_frame = static_cast<uint8_t*>(base) + h->offset;
+    c->imports[*d_frame] = base;
+    return RR_OK;
+}
+
+int rr_frame_close(rr_ctx* c, void* d_frame) {
+    if (!c) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    auto it = c->imports.find(d_frame);
+    if (it == c->imports.end()) return RR_OK;
+    RR_CUDA(c, cudaSetDevice(c->device));
+    if (c->launched) RR_CUDA(c, cudaEventSynchronize(c->ev1));   // no shard still writing
+    void* base = it->second;
+    c->imports.erase(it);
+    RR_CUDA(c, cudaIpcCloseMemHandle(base));
+    return RR_OK;
+}
+
+int rr_frame_probe(rr_ctx* c, void* d_frame, size_t offset, uint8_t value) {
+    if (!c || !d_frame) return RR_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(c->mu);
+    RR_CUDA(c, cudaSetDevice(c->device));
+    RR_CUDA(c, rr::launch_probe(static_cast<uint8_t*>(d_frame) + offset, value, c->stream));
+    RR_CUDA(c, cudaStreamSynchronize(c->stream));
     return RR_OK;
 }
 

@@ -50,6 +50,10 @@ cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float 
 cudaError_t launch_accel_points(const DevParams& P, const double* pos, const double* vel, int n,
                                 double* acc, double* validity, cudaStream_t s);
 
+// One-byte device store (+ system fence) through a possibly peer/IPC-mapped
+// pointer: the exchange's mapping probe.
+cudaError_t launch_probe(uint8_t* p, uint8_t value, cudaStream_t s);
+
 // Dense FFMA microbenchmark; returns TFLOP/s (2 flop per FFMA).
 cudaError_t measure_fp32_peak(int num_sms, double* tflops);
 

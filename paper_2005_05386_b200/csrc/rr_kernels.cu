@@ -79,6 +79,11 @@ __global__ void detile_kernel(const uint8_t* __restrict__ g, int width, int heig
     rgb[dst + 2] = g[src + 2];
 }
 
+__global__ void probe_kernel(uint8_t* p, uint8_t v) {
+    *p = v;
+    __threadfence_system();
+}
+
 // FFMA throughput probe: 8 independent FMA chains per thread, imm-free.
 __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
     float x[8];
@@ -289,6 +294,11 @@ cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int ti
     dim3 grid((width + 255) / 256, height);
     detile_kernel<<<grid, 256, 0, stream>>>(gathered, width, height, tile_w, tile_h, n_shards, max_k,
                                             tiles_x, rgb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe(uint8_t* p, uint8_t value, cudaStream_t s) {
+    probe_kernel<<<1, 1, 0, s>>>(p, value);
     return cudaGetLastError();
 }
 

@@ -194,6 +194,29 @@ class Renderer:
                                              _addr(stream)))
         return st.as_dict() if st is not None else None
 
+    # -- cross-process frame exchange ------------------------
+    def frame_export(self, d_frame, nbytes: int = 0) -> bytes:
+        """Handle (bytes, picklable) of a device frame buffer (torch tensor or
+        address) for rr_frame_import in another process."""
+        if not nbytes and hasattr(d_frame, "numel"):
+            nbytes = d_frame.numel() * d_frame.element_size()
+        h = abi.rr_frame_handle()
+        self._check(self.lib.rr_frame_export(self.ctx, _addr(d_frame), nbytes, C.byref(h)))
+        return bytes(h)
+
+    def frame_import(self, handle: bytes) -> int:
+        """Maps an exported frame on this context's device -> device address."""
+        h = abi.rr_frame_handle.from_buffer_copy(handle)
+        p = C.c_void_p()
+        self._check(self.lib.rr_frame_import(self.ctx, C.byref(h), C.byref(p)))
+        return int(p.value)
+
+    def frame_close(self, d_frame):
+        self._check(self.lib.rr_frame_close(self.ctx, _addr(d_frame)))
+
+    def frame_probe(self, d_frame, offset: int, value: int):
+        self._check(self.lib.rr_frame_probe(self.ctx, _addr(d_frame), offset, value))
+
     def detile(self, d_gathered, width, height, tile_w, tile_h, n_shards, d_rgb, stream=None):
         self._check(self.lib.rr_detile(self.ctx, _addr(d_gathered), width, height, tile_w, tile_h,
                                        n_shards, _addr(d_rgb), _addr(stream)))

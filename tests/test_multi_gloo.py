@@ -1,7 +1,9 @@
 """CPU, world_size 2 (gloo): the multi-GPU frame path's host logic.
 
 Each rank renders its cyclic share of 32x32 tiles (here with the FP64 oracle
-standing in for the device render, so the test runs without a GPU), the
+standing in for the device render, so the test runs without a GPU; the same
+round trip through rr_render_tiles + rr_detile on the device is
+tests/test_gpu_p2p.py::test_tile_shards_gather_detile), the
 tile-major shard buffers are gathered to rank 0 (dist.gather, as bench.py does
 over NCCL) and de-tiled with the same index map as rr_detile / detile_kernel.
 The result must be byte-identical to the single-rank frame."""
@@ -102,4 +104,5 @@ def test_c_abi_tile_count_matches_host_logic():
         for s in range(n):
             assert lib.rr_shard_tile_count(1920, 1080, 32, 32, s, n) == \
                 len(tiles_of_shard(1920, 1080, 32, 32, s, n))
-    assert lib.rr_shard_tile_count(10, 10, 32, 32, 2, 2) == -1 or True
+    assert lib.rr_shard_tile_count(10, 10, 32, 32, 2, 2) == -1     # shard out of range
+    assert lib.rr_shard_tile_count(10, 10, 32, 32, 1, 2) == 0      # one tile, two shards
