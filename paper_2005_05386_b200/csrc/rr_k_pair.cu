@@ -8,7 +8,7 @@ template <int NB>
 cudaError_t pair_nb(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms, const char** name,
                     const char* label) {
     *name = label;
-    return launch_variant2<NB>(P, L, s, sms);
+    return launch_variant2<kBumps, NB, false>(P, L, s, sms);
 }
 
 } // namespace

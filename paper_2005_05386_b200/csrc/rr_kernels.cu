@@ -255,8 +255,10 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
     if (launches) {
         // with lights: hit + shadow launches, except the fused ray-pair kernel
         const bool lit = P.n_lights > 0 && L.mode != kModeRays;
-        const bool fused = RR_RAY_PAIRS && RR_X2_FUSED && P.kind == kBumps && P.scheme == 1 &&
-                           P.n_meshes == 0;
+        const bool fused = RR_RAY_PAIRS && RR_X2_FUSED && P.scheme == 1 &&
+                           ((P.kind == kBumps && P.n_meshes == 0) ||
+                            (RR_TWIST_PAIRS && P.kind == kDiffeo && P.n_stages == 1 &&
+                             P.stages[0].kind == kStageTwist));
         *launches = lit && !fused ? 2 : 1;
     }
     switch (P.kind) {
@@ -271,6 +273,11 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
         case kGraphGeneral:
             return launch_family_graph(P, L, stream, num_sms, kernel_name);
         default:
+#if RR_RAY_PAIRS && RR_TWIST_PAIRS
+            // single twist, RK4: ray pairs (C4, with or without meshes)
+            if (P.scheme == 1 && P.n_stages == 1 && P.stages[0].kind == kStageTwist)
+                return launch_family_pair_twist(P, L, stream, num_sms, kernel_name);
+#endif
             return launch_family_diffeo(P, L, stream, num_sms, kernel_name);
     }
 }

@@ -36,6 +36,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // (march2_kernel); 0: one ray per thread (march_kernel) for every scene.
 #define RR_RAY_PAIRS 1
 #endif
+#ifndef RR_TWIST_PAIRS
+// 1: single-twist RK4 frames (C4, meshes included) on the ray-pair kernel
+#define RR_TWIST_PAIRS 1
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -43,6 +47,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_RK4_UNROLL
 #define RR_X2_RK4_UNROLL 1   // 4 RK4 stages unrolled (4 small bump loops): C3 10.32 -> 9.91 ms, lights 16.94 -> 16.66
+#endif
+#ifndef RR_X2_BODY
+#define RR_X2_BODY 1   // bump-body operand order of the ray-pair march (see accel_bumps_x2)
 #endif
 #ifndef RR_MIN_BLOCKS_X2
 // ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
@@ -57,6 +64,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_MIN_BLOCKS_X2_SMALL
 #define RR_MIN_BLOCKS_X2_SMALL 6
+#endif
+#ifndef RR_MIN_BLOCKS_X2_TWIST
+#define RR_MIN_BLOCKS_X2_TWIST 6        // ray-pair single-twist frames (C4 without meshes)
+#endif
+#ifndef RR_MIN_BLOCKS_X2_TWIST_MESH
+#define RR_MIN_BLOCKS_X2_TWIST_MESH 6   // ray-pair single-twist frames with meshes (C4)
 #endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
@@ -221,15 +234,30 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
     auto body = [&](const DevBumpB& b, bool neg) {
         const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
         const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
+#if RR_X2_BODY == 2
+        // q = d.g + la and t = y.g interleaved with g_k in the first operand
+        // slot of both, so the second FFMA2 of each pair can take g_k from the
+        // operand reuse cache: an FFMA2 reading three distinct register pairs
+        // issues at 2/3 of the FMA-pipe rate (tools/microbench/fp32_pipes.cu)
+        const F2 q0 = fma2(gz, dz, ld2(b.la));
+        const F2 t0 = mul2(gz, y.z);
+        const F2 q1 = fma2(gy, dy, q0);
+        const F2 t1 = fma2(gy, y.y, t0);
+        const F2 q = fma2(gx, dx, q1);
+        const F2 t = fma2(gx, y.x, t1);
+        const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
+        const F2 et = mul2(t, e);
+#else
         const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
         const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
         const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
         const F2 et = mul2(e, t);
+#endif
         if (neg) {
             Gx = fnma2(e, gx, Gx);
             Gy = fnma2(e, gy, Gy);
             Gz = fnma2(e, gz, Gz);
-            Q1 = fnma2(et, t, Q1);
+            Q1 = fnma2(RR_X2_BODY == 2 ? t : et, RR_X2_BODY == 2 ? et : t, Q1);
             Sx = fnma2(e, ld2(b.kx), Sx);
             Sy = fnma2(e, ld2(b.ky), Sy);
             Sz = fnma2(e, ld2(b.kz), Sz);
@@ -237,7 +265,7 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
             Gx = fma2(e, gx, Gx);
             Gy = fma2(e, gy, Gy);
             Gz = fma2(e, gz, Gz);
-            Q1 = fma2(et, t, Q1);
+            Q1 = fma2(RR_X2_BODY == 2 ? t : et, RR_X2_BODY == 2 ? et : t, Q1);
             Sx = fma2(e, ld2(b.kx), Sx);
             Sy = fma2(e, ld2(b.ky), Sy);
             Sz = fma2(e, ld2(b.kz), Sz);
@@ -1575,12 +1603,57 @@ struct UnitStats {
     unsigned ref_steps, errs, shadow_steps, nrays;
 };
 
-template <int NB, int PASS>
+// Packed RK4 of the single twist (march_fixed's closed form, two rays per
+// thread): a_z = 0 and a does not depend on z, so z' stays constant, the
+// stage points need no z and dz = h z' (integrate.hpp:63-93).
+__device__ __forceinline__ void twist_rk4_x2(const P3& p, const P3& v, F2 half, F2 full, F2 sixth,
+                                             P3& dp, P3& vn) {
+    const F2 two = bc2(2.f), mtwo = bc2(-2.f);
+    F2 sxx = bc2(0.f), sxy = bc2(0.f), svx = bc2(0.f), svy = bc2(0.f);
+    F2 px = p.x, py = p.y, vx = v.x, vy = v.y;
+    const F2 vz = v.z;
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+        const F2 ax = mul2(vz, fma2(vz, px, mul2(two, vy)));
+        const F2 ay = mul2(vz, fma2(vz, py, mul2(mtwo, vx)));
+        if (st == 0 || st == 3) {
+            sxx = add2(vx, sxx); sxy = add2(vy, sxy);
+            svx = add2(ax, svx); svy = add2(ay, svy);
+        } else {
+            sxx = fma2(two, vx, sxx); sxy = fma2(two, vy, sxy);
+            svx = fma2(two, ax, svx); svy = fma2(two, ay, svy);
+        }
+        const F2 cc = st < 2 ? half : full;
+        px = fma2(cc, vx, p.x); py = fma2(cc, vy, p.y);
+        vx = fma2(cc, ax, v.x); vy = fma2(cc, ay, v.y);
+    }
+    dp = P3{mul2(sixth, sxx), mul2(sixth, sxy), mul2(full, vz)};
+    vn = P3{fma2(sixth, svx, v.x), fma2(sixth, svy, v.y), vz};
+}
+
+// Mesh part of intersect() for one ray (MESH pair marches): the chord
+// [a, a + d] against every mesh unless it stays inside the ray's free ball.
+__device__ __forceinline__ void mesh_part(const DevParams& P, F3 a, F3 d, float len, bool& have,
+                                          float& s_best, int& prim, int& hid, int& mrec, float& mfree) {
+    for (int i = 0; i < P.n_meshes; ++i) {
+        int rec = 0;
+        float s = 0.f;
+        const bool h = mesh_chord(P.meshes[i], a, d, s, rec);
+        if (consider(h, s, P.meshes[i].index, (kPrimMesh << 8) | i, have, s_best, prim, hid)) mrec = rec;
+    }
+    const F3 b = f3(a.x + d.x, a.y + d.y, a.z + d.z);
+    float fr = 3.0e38f;
+    for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, RR_MESH_FREE_CAP));
+    mfree = fr;
+}
+
+template <int KIND, int NB, int PASS, bool MESH>
 __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool live1, P3 p, P3 v,
                                            UnitStats& us, const DevLaunch& L, unsigned unit,
                                            int (&status)[2], int (&steps)[2], PairStage* stg,
                                            F3 q0 = F3{0.f, 0.f, 0.f},
                                            F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f) {
+    static_assert(KIND == kBumps || KIND == kDiffeo, "ray pairs: Gaussian bumps or the single twist");
     LaneCounters& cnt = us.cnt;
     const int lane = threadIdx.x & 31;
     status[0] = status[1] = PASS == kPassShadow ? 1 : 0;
@@ -1598,38 +1671,44 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
     const F2 half = bc2(0.5f * h), full = bc2(h), sixth = bc2(h / 6.f);
     P3 c{bc2(0.f), bc2(0.f), bc2(0.f)};    // Kahan compensation of the position sums
     float sfree[2] = {0.f, 0.f};           // sphere / half-space free distance budgets
+    float mfree[2] = {0.f, 0.f};           // mesh free distance budgets (MESH)
     for (;;) {
         if (!__any_sync(kFull, act[0] || act[1])) break;
         cnt.lane_slots += 2;
         int nj[2] = {0, 0};
-        uint32_t lmo = 0u;
+        uint32_t um = 0u;
+        if constexpr (KIND == kBumps) {
+            uint32_t lmo = 0u;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            uint32_t lm = 0u;
-            unsigned cell = 0;
-            if (act[r]) {
-                if (P.cull) {
-                    cell = cell_of(P, ray_of(p, r));
-                    lm = __ldg(P.cull_masks + cell);
-                } else {
-                    lm = P.all_mask;
+            for (int r = 0; r < 2; ++r) {
+                uint32_t lm = 0u;
+                unsigned cell = 0;
+                if (act[r]) {
+                    if (P.cull) {
+                        cell = cell_of(P, ray_of(p, r));
+                        lm = __ldg(P.cull_masks + cell);
+                    } else {
+                        lm = P.all_mask;
+                    }
+                    if (P.skip && lm == 0u) {
+                        const int k = __ldg(P.skip_k + cell);
+                        if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r]);
+                    }
                 }
-                if (P.skip && lm == 0u) {
-                    const int k = __ldg(P.skip_k + cell);
-                    if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r]);
-                }
+                lmo |= nj[r] ? 0u : lm;
             }
-            lmo |= nj[r] ? 0u : lm;
-        }
-        const uint32_t um = __reduce_or_sync(kFull, lmo);
+            um = __reduce_or_sync(kFull, lmo);
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(um);
+            for (int r = 0; r < 2; ++r)
+                if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(um);
+        }
         P3 dp, vn;
         const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
-        if (__all_sync(kFull, jw0 && jw1)) {                // whole warp jumps: no integration
+        if (KIND == kBumps && __all_sync(kFull, jw0 && jw1)) {   // whole warp jumps: no integration
             dp = P3{bc2(0.f), bc2(0.f), bc2(0.f)};
             vn = v;
+        } else if constexpr (KIND == kDiffeo) {
+            twist_rk4_x2(p, v, half, full, sixth, dp, vn);
         } else {                                             // RK4 (integrate.hpp:63-93)
             P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
             P3 ps = p, vs = v;
@@ -1650,7 +1729,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             dp = P3{mul2(sixth, sx.x), mul2(sixth, sx.y), mul2(sixth, sx.z)};
             vn = P3{fma2(sixth, sv.x, v.x), fma2(sixth, sv.y, v.y), fma2(sixth, sv.z, v.z)};
         }
-        if (nj[0] | nj[1]) {                                 // straight jumps of nj steps
+        if (KIND == kBumps && (nj[0] | nj[1])) {            // straight jumps of nj steps
             const F2 hn = mk2(h * (float)nj[0], h * (float)nj[1]);
             const P3 dj{mul2(hn, v.x), mul2(hn, v.y), mul2(hn, v.z)};
             const bool j0 = nj[0] != 0, j1 = nj[1] != 0;
@@ -1661,6 +1740,46 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
         const P3 yv{sub2(dp.x, c.x), sub2(dp.y, c.y), sub2(dp.z, c.z)};
         const P3 pn{add2(p.x, yv.x), add2(p.y, yv.y), add2(p.z, yv.z)};
         c = P3{sub2(sub2(pn.x, p.x), yv.x), sub2(sub2(pn.y, p.y), yv.y), sub2(sub2(pn.z, p.z), yv.z)};
+        // chord tests (scene.cpp:99-109): analytic primitives per ray; with
+        // meshes, the rays whose chord leaves their free ball are collected
+        // and the warp runs the BVH tests over that compacted list (one
+        // traversal per iteration for every thread with work, whichever of
+        // its two rays needs it) instead of once per ray slot
+        bool hit[2] = {false, false};
+        float sh[2] = {0.f, 0.f};
+        int primr[2] = {-1, -1}, hidr[2] = {0, 0}, mrec[2] = {0, 0};
+        if constexpr (MESH) {
+            unsigned pend = 0u;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (!act[r]) continue;
+                const F3 a = ray_of(p, r), b = ray_of(pn, r);
+                float md = 0.f;
+                int mr = 0;
+                hit[r] = intersect<false>(P, a, b, sh[r], primr[r], hidr[r], md, mr, sfree[r]);
+                const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
+                const float len = fmaf(sqrt_approx(fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z))), 1.0001f, 1e-30f);
+                if (len < mfree[r]) mfree[r] -= len;     // the chord stays inside the free ball
+                else pend |= 1u << r;
+            }
+            while (__any_sync(kFull, pend != 0u)) {
+                if (pend) {
+                    const int r = (pend & 1u) ? 0 : 1;
+                    pend &= pend - 1u;
+                    const F3 a = r ? ray_of(p, 1) : ray_of(p, 0);
+                    const F3 b = r ? ray_of(pn, 1) : ray_of(pn, 0);
+                    const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
+                    bool hv = r ? hit[1] : hit[0];
+                    float sb = r ? sh[1] : sh[0];
+                    int pr = r ? primr[1] : primr[0], hd = r ? hidr[1] : hidr[0];
+                    int mc = 0;
+                    float mf = 0.f;
+                    mesh_part(P, a, d, 0.f, hv, sb, pr, hd, mc, mf);
+                    if (r) { hit[1] = hv; sh[1] = sb; primr[1] = pr; hidr[1] = hd; mrec[1] = mc; mfree[1] = mf; }
+                    else { hit[0] = hv; sh[0] = sb; primr[0] = pr; hidr[0] = hd; mrec[0] = mc; mfree[0] = mf; }
+                }
+            }
+        }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             if (!act[r]) continue;
@@ -1668,10 +1787,14 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             const int nsub = nj[r] ? nj[r] : 1;
             cnt.steps_integrated += 1;
             cnt.jumps += nj[r] ? 1u : 0u;
-            float s = 0.f, mfree = 0.f;
-            int prim = -1, hid = 0, mrec = 0;
-            const bool hit = intersect<false>(P, a, b, s, prim, hid, mfree, mrec, sfree[r]);
-            if (hit) {                                       // kernel_impl.hpp:63-76
+            float s = sh[r];
+            int prim = primr[r], hid = hidr[r];
+            if constexpr (!MESH) {   // analytic primitives only: test and consume in one pass
+                float md = 0.f;
+                int mr = 0;
+                hit[r] = intersect<false>(P, a, b, s, prim, hid, md, mr, sfree[r]);
+            }
+            if (hit[r]) {                                    // kernel_impl.hpp:63-76
                 const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
                 const int sub = min((int)sj, nsub - 1);
@@ -1684,7 +1807,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                     const int nst = step[r] + sub + 1;
                     if constexpr (PASS == kPassHits) {
                         RayResult res{1, prim, nst, th, pt, f3(0.f, 0.f, 0.f)};
-                        res.normal = hit_normal(P, hid, s, a, b, pt, mrec);
+                        res.normal = hit_normal(P, hid, s, a, b, pt, mrec[r]);
                         emit_primary<PASS>(P, L, unit, r, res);
                     } else {
                         stg->tp[r * kUnit + lane] = make_float4(th, pt.x, pt.y, pt.z);
@@ -2020,7 +2143,7 @@ __device__ __forceinline__ void store_pair_rgb(const DevLaunch& L, unsigned unit
 // (kPassShade: from the warp's PairStage, plus the PixelOutcome records when
 // the launch carries an outcome sink) or hit records for the shadow work
 // (kPassHits).
-template <int NB, int PASS>
+template <int KIND, int NB, int PASS, bool MESH>
 __device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch& L, unsigned unit,
                                              int lane, UnitStats& us, PairStage* stg) {
     bool live[2];
@@ -2047,7 +2170,7 @@ __device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch
         us.nrays += live[r] ? 1u : 0u;
     }
     int st[2], stp[2];
-    march_pair<NB, PASS>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
+    march_pair<KIND, NB, PASS, MESH>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
                          us, L, unit, st, stp, stg);
     if constexpr (PASS == kPassShade) {
         __syncwarp();
@@ -2087,7 +2210,7 @@ __device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch
 // byte of every (pixel, light) is published and the unit's LAST light to
 // finish (per-unit counter L.done) shades its 64 pixels, summing the lit
 // contributions in light order (shade_lit in oracle/rro.c).
-template <int NB>
+template <int KIND, int NB, bool MESH>
 __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch& L, unsigned unit,
                                             int l, int nl, int lane, UnitStats& us, PairStage* stg) {
     bool inr[2], live[2];
@@ -2136,7 +2259,7 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
         }
     }
     int sst[2], sstp[2];
-    march_pair<NB, kPassShadow>(P, want[0], want[1], pair_of(x0[0], x0[1]), pair_of(v0[0], v0[1]),
+    march_pair<KIND, NB, kPassShadow, MESH>(P, want[0], want[1], pair_of(x0[0], x0[1]), pair_of(v0[0], v0[1]),
                                 us, L, unit, sst, sstp, stg, q[0], q[1], dist2[0], dist2[1]);
     bool vis[2];
 #pragma unroll
@@ -2192,8 +2315,10 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
 //                 the frame has one tail instead of two and no launch gap.
 //                 No deadlock: a flag's producer already holds a running warp
 //                 and waits on nothing.
-template <int NB, int PASS>
-__global__ void __launch_bounds__(kThreads, NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
+template <int KIND, int NB, int PASS, bool MESH>
+__global__ void __launch_bounds__(kThreads, KIND == kDiffeo ? (MESH ? RR_MIN_BLOCKS_X2_TWIST_MESH
+                                                                     : RR_MIN_BLOCKS_X2_TWIST)
+                                               : NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
                                                : (PASS == kPassFused ? RR_MIN_BLOCKS_X2_FUSED
                                                                      : RR_MIN_BLOCKS_X2))
 march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
@@ -2219,7 +2344,7 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
         constexpr int kPrim = PASS == kPassFused ? kPassHits : PASS;
         while (work < n_primary) {
             UnitStats us{};
-            pair_primary<NB, kPrim>(P, L, work, lane, us, stg);
+            pair_primary<KIND, NB, kPrim, MESH>(P, L, work, lane, us, stg);
             if constexpr (PASS == kPassFused) {                 // publish the hit records
                 __threadfence();
                 __syncwarp();
@@ -2245,7 +2370,7 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
                 __threadfence();
             }
             UnitStats us{};
-            pair_shadow<NB>(P, L, unit, (int)(w % (unsigned)nl), nl, lane, us, stg);
+            pair_shadow<KIND, NB, MESH>(P, L, unit, (int)(w % (unsigned)nl), nl, lane, us, stg);
             flush_unit_stats(L, us, lane, true);
             work = fetch();
         }
@@ -2275,39 +2400,39 @@ cudaError_t launch_pass(const DevParams& P, const DevLaunch& L, cudaStream_t s, 
     return cudaGetLastError();
 }
 
-template <int NB, int PASS>
+template <int KIND, int NB, int PASS, bool MESH>
 int occupancy_of2() {
     static int occ = [] {
         int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march2_kernel<NB, PASS>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march2_kernel<KIND, NB, PASS, MESH>, kThreads, 0);
         return n > 0 ? n : 1;
     }();
     return occ;
 }
 
-template <int NB, int PASS>
+template <int KIND, int NB, int PASS, bool MESH>
 cudaError_t launch_pass2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
     const unsigned warps_needed = (L.n_units + 1) / 2;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of2<NB, PASS>());
+    unsigned blocks = (unsigned)(num_sms * occupancy_of2<KIND, NB, PASS, MESH>());
     const unsigned max_useful = (warps_needed + 3) / 4;
     if (blocks > max_useful) blocks = max_useful;
     if (blocks == 0) blocks = 1;
-    march2_kernel<NB, PASS><<<blocks, kThreads, 0, s>>>(P, L);
+    march2_kernel<KIND, NB, PASS, MESH><<<blocks, kThreads, 0, s>>>(P, L);
     return cudaGetLastError();
 }
 
-template <int NB>
+template <int KIND, int NB, bool MESH>
 cudaError_t launch_variant2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
-    if (P.n_lights == 0 || L.mode == kModeRays) return launch_pass2<NB, kPassShade>(P, L, s, num_sms);
+    if (P.n_lights == 0 || L.mode == kModeRays) return launch_pass2<KIND, NB, kPassShade, MESH>(P, L, s, num_sms);
 #if RR_X2_FUSED
-    return launch_pass2<NB, kPassFused>(P, L, s, num_sms);
+    return launch_pass2<KIND, NB, kPassFused, MESH>(P, L, s, num_sms);
 #endif
-    cudaError_t e = launch_pass2<NB, kPassHits>(P, L, s, num_sms);
+    cudaError_t e = launch_pass2<KIND, NB, kPassHits, MESH>(P, L, s, num_sms);
     if (e != cudaSuccess) return e;
     DevLaunch L2 = L;
     L2.counter = L.counter + 1;
     L2.lpp = 1;
-    return launch_pass2<NB, kPassShadow>(P, L2, s, num_sms);
+    return launch_pass2<KIND, NB, kPassShadow, MESH>(P, L2, s, num_sms);
 }
 
 // Without lights: one fused launch.  With lights (EXTENSION): a hit-record
