@@ -114,8 +114,13 @@ struct DevMesh {          // EXTENSION: BVH over a triangle soup (rr_bvh.h layou
     const float4* tris;   // 3 float4 per triangle
     int n_nodes, n_tris;
     int index;            // position in Scene::primitives
-    int pad;
+    int dG;               // free-distance grid: cells per axis (0: none)
     unsigned long long fingerprint;   // host: content hash (scene-change detection)
+    const uint8_t* dist;  // dG^3 lower bounds of the distance from any point of a cell to the
+                          // mesh (to its BVH leaf boxes), in units of dq, over the scene bounds
+    float dlo[3], dinv[3];
+    float dq;
+    int pad2;
 };
 
 struct DevLight {

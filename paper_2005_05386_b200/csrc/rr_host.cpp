@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -925,6 +926,41 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
             np->meshes[m].nodes = reinterpret_cast<const float4*>(dn);
             np->meshes[m].tris = reinterpret_cast<const float4*>(dt);
             np->meshes[m].n_nodes = (int)(bvh.nodes.size() / 8);
+            // free-distance grid over the scene bounds (rays never start a
+            // chord outside them): 128^3 bytes, quantum = extent / 510
+            {
+                // RRAY_MESH_GRID=<cells per axis> overrides the default (tuning)
+                const char* env = std::getenv("RRAY_MESH_GRID");
+                const int G = env ? std::max(8, std::min(512, std::atoi(env))) : 128;
+                float lo[3], cell[3], ext = 0.f;
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = np->lo[k];
+                    cell[k] = (np->hi[k] - np->lo[k]) / G;
+                    ext = std::max(ext, np->hi[k] - np->lo[k]);
+                }
+                const float q = ext / 510.f;
+                void* dd = nullptr;
+                e = cudaMalloc(&dd, (size_t)G * G * G);
+                if (dd) c->d_mesh.push_back(dd);
+                if (e == cudaSuccess && ext > 0.f && std::isfinite(ext))
+                    e = rr::launch_mesh_dist(reinterpret_cast<const float4*>(dn), G, lo, cell, q,
+                                             static_cast<uint8_t*>(dd), c->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+                if (e != cudaSuccess) {
+                    delete np;
+                    return cuda_err(c, e, "mesh distance grid");
+                }
+                rr::DevMesh& dm = np->meshes[m];
+                if (ext > 0.f && std::isfinite(ext)) {
+                    dm.dist = static_cast<const uint8_t*>(dd);
+                    dm.dG = G;
+                    dm.dq = q;
+                    for (int k = 0; k < 3; ++k) {
+                        dm.dlo[k] = lo[k];
+                        dm.dinv[k] = 1.f / cell[k];
+                    }
+                }
+            }
             ++m;
         }
         if (!c->P_key) c->P_key = new DevParams();
@@ -933,6 +969,10 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
             c->P_key->meshes[k].nodes = nullptr;
             c->P_key->meshes[k].tris = nullptr;
             c->P_key->meshes[k].n_nodes = 0;
+            c->P_key->meshes[k].dist = nullptr;
+            c->P_key->meshes[k].dG = 0;
+            c->P_key->meshes[k].dq = 0.f;
+            for (int j = 0; j < 3; ++j) c->P_key->meshes[k].dlo[j] = c->P_key->meshes[k].dinv[j] = 0.f;
         }
         *c->P = *np;
         c->prog = prog;

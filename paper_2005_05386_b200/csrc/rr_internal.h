@@ -52,6 +52,10 @@ cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float 
 cudaError_t launch_accel_points(const DevParams& P, const double* pos, const double* vel, int n,
                                 double* acc, double* validity, cudaStream_t s);
 
+// Mesh free-distance grid (G^3 bytes, units of q) over the box lo + [0, G cell).
+cudaError_t launch_mesh_dist(const float4* nodes, int G, const float lo[3], const float cell[3],
+                             float q, uint8_t* out, cudaStream_t s);
+
 // One-byte device store (+ system fence) through a possibly peer/IPC-mapped
 // pointer: the exchange's mapping probe.
 cudaError_t launch_probe(uint8_t* p, uint8_t value, cudaStream_t s);

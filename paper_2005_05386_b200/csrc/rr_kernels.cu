@@ -79,6 +79,26 @@ __global__ void detile_kernel(const uint8_t* __restrict__ g, int width, int heig
     rgb[dst + 2] = g[src + 2];
 }
 
+// Mesh free-distance grid (per scene upload): cell c gets
+// floor(max(0, d(centre, nearest leaf box) - half diagonal) / q), a lower
+// bound of the distance from any point of the cell to any triangle (every
+// triangle lies in a leaf box), saturating at 255 q.
+__global__ void mesh_dist_kernel(const float4* __restrict__ nodes, int G, float lo0, float lo1,
+                                 float lo2, float c0, float c1, float c2, float q,
+                                 uint8_t* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * G * G) return;
+    const int ix = idx % G, iy = (idx / G) % G, iz = idx / (G * G);
+    const F3 centre = f3(lo0 + (ix + 0.5f) * c0, lo1 + (iy + 0.5f) * c1, lo2 + (iz + 0.5f) * c2);
+    const float half_diag = 0.5f * sqrtf(c0 * c0 + c1 * c1 + c2 * c2);
+    DevMesh M{};
+    M.nodes = nodes;
+    const float d = mesh_free(M, centre, 255.f * q + half_diag + q);
+    // rounding margin of the FP32 distance: 1e-5 relative + 1e-5 absolute
+    const float lb = fmaxf(0.f, d - half_diag - fmaf(1e-5f, d, 1e-5f));
+    out[idx] = (uint8_t)fminf(255.f, floorf(lb / q));
+}
+
 __global__ void probe_kernel(uint8_t* p, uint8_t v) {
     *p = v;
     __threadfence_system();
@@ -258,7 +278,7 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
         const bool fused = RR_RAY_PAIRS && RR_X2_FUSED && P.scheme == 1 &&
                            ((P.kind == kBumps && P.n_meshes == 0) ||
                             (RR_TWIST_PAIRS && P.kind == kDiffeo && P.n_stages == 1 &&
-                             P.stages[0].kind == kStageTwist));
+                             P.stages[0].kind == kStageTwist && (RR_TWIST_PAIRS_MESH || P.n_meshes == 0)));
         *launches = lit && !fused ? 2 : 1;
     }
     switch (P.kind) {
@@ -275,7 +295,8 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
         default:
 #if RR_RAY_PAIRS && RR_TWIST_PAIRS
             // single twist, RK4: ray pairs (C4, with or without meshes)
-            if (P.scheme == 1 && P.n_stages == 1 && P.stages[0].kind == kStageTwist)
+            if (P.scheme == 1 && P.n_stages == 1 && P.stages[0].kind == kStageTwist &&
+                (RR_TWIST_PAIRS_MESH || P.n_meshes == 0))
                 return launch_family_pair_twist(P, L, stream, num_sms, kernel_name);
 #endif
             return launch_family_diffeo(P, L, stream, num_sms, kernel_name);
@@ -301,6 +322,14 @@ cudaError_t launch_detile(const uint8_t* gathered, int width, int height, int ti
     dim3 grid((width + 255) / 256, height);
     detile_kernel<<<grid, 256, 0, stream>>>(gathered, width, height, tile_w, tile_h, n_shards, max_k,
                                             tiles_x, rgb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mesh_dist(const float4* nodes, int G, const float lo[3], const float cell[3],
+                             float q, uint8_t* out, cudaStream_t s) {
+    const int cells = G * G * G;
+    mesh_dist_kernel<<<(cells + 127) / 128, 128, 0, s>>>(nodes, G, lo[0], lo[1], lo[2], cell[0],
+                                                         cell[1], cell[2], q, out);
     return cudaGetLastError();
 }
 

@@ -40,6 +40,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 1: single-twist RK4 frames (C4, meshes included) on the ray-pair kernel
 #define RR_TWIST_PAIRS 1
 #endif
+#ifndef RR_TWIST_PAIRS_MESH
+// 1: single-twist RK4 frames WITH meshes on the ray-pair kernel too
+#define RR_TWIST_PAIRS_MESH 0
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -620,7 +624,7 @@ __device__ __forceinline__ bool hit_half_space(const DevHalf& hs, F3 a, F3 d, fl
 // while the marched path stays inside that ball (sum of chord lengths) no
 // mesh test is needed.  Both are __noinline__ so scenes without meshes keep
 // the march loop's register allocation.
-__device__ __noinline__ bool mesh_chord(const DevMesh& M, F3 a, F3 d, float& best_s, int& best_rec) {
+__device__ __forceinline__ bool mesh_chord_impl(const DevMesh& M, F3 a, F3 d, float& best_s, int& best_rec) {
     const float ix = d.x != 0.f ? 1.f / d.x : 3.0e38f;
     const float iy = d.y != 0.f ? 1.f / d.y : 3.0e38f;
     const float iz = d.z != 0.f ? 1.f / d.z : 3.0e38f;
@@ -711,7 +715,7 @@ __device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
 #define RR_MESH_FREE_CAP 0.5f   // re-measured with rolled diffeo stages + 6 CTAs/SM (profiles/r1k_freecap_ab.log):
                                 // caps 0.25 / 0.5 / 1 / 2: C4 twist 13.0 / 12.8 / 13.3 / 14.2 ms, twist+bend 50.7 / 50.5 / 51.1 / 51.5 ms
 #endif
-__device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
+__device__ __forceinline__ float mesh_free_impl(const DevMesh& M, F3 p, float cap) {
     float best2 = cap * cap;
     int stack[48];
     float sd[48];
@@ -751,6 +755,31 @@ __device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
         if (!found) break;
     }
     return sqrtf(best2);
+}
+
+__device__ __noinline__ bool mesh_chord(const DevMesh& M, F3 a, F3 d, float& best_s, int& best_rec) {
+    return mesh_chord_impl(M, a, d, best_s, best_rec);
+}
+__device__ __noinline__ float mesh_free(const DevMesh& M, F3 p, float cap) {
+    return mesh_free_impl(M, p, cap);
+}
+
+// Free distance of point a from every mesh by its distance grid: a lower
+// bound of the distance from a to any triangle (0 outside the grid or next
+// to the mesh).  One byte load per mesh instead of a nearest-first BVH query.
+__device__ __forceinline__ float mesh_grid_free(const DevParams& P, F3 a) {
+    float fr = 3.0e38f;
+    for (int i = 0; i < P.n_meshes; ++i) {
+        const DevMesh& M = P.meshes[i];
+        if (M.dG == 0) return 0.f;
+        const float fx = (a.x - M.dlo[0]) * M.dinv[0], fy = (a.y - M.dlo[1]) * M.dinv[1];
+        const float fz = (a.z - M.dlo[2]) * M.dinv[2];
+        const float g = (float)M.dG;
+        if (!(fx >= 0.f && fy >= 0.f && fz >= 0.f && fx < g && fy < g && fz < g)) return 0.f;
+        const unsigned cell = ((unsigned)fz * M.dG + (unsigned)fy) * M.dG + (unsigned)fx;
+        fr = fminf(fr, (float)__ldg(M.dist + cell) * M.dq);
+    }
+    return fr;
 }
 
 // Nearest hit over all primitives; ties keep the lower primitive index
@@ -841,8 +870,11 @@ __device__ __forceinline__ bool intersect(const DevParams& P, F3 a, F3 b, float&
         consider(h, s, P.grids[i].index, (kPrimGrid << 8) | i, have, s_best, prim, hid);
     }
     if (MESH) {
+        float gd;
         if (len < mfree) {
             mfree -= len;                 // the chord stays inside the free ball
+        } else if ((gd = mesh_grid_free(P, a)) > len) {
+            mfree = gd - len;             // inside the distance grid's free ball around a
         } else {
             for (int i = 0; i < P.n_meshes; ++i) {
                 int rec = 0;
@@ -1065,7 +1097,8 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
         }
         float valid = 3.0e38f;
         F3 dp, vn;
-        if (__all_sync(kFull, nj != 0 || !active)) {         // whole warp jumps: no integration
+        // whole warp jumps: no integration (only Euclidean and bump metrics jump)
+        if ((KIND == kEuclid || KIND == kBumps) && __all_sync(kFull, nj != 0 || !active)) {
             dp = f3(0.f, 0.f, 0.f);
             vn = v;
         } else if (SCHEME == 0) {                            // Euler (integrate.hpp:55-61)
@@ -1632,18 +1665,27 @@ __device__ __forceinline__ void twist_rk4_x2(const P3& p, const P3& v, F2 half, 
 }
 
 // Mesh part of intersect() for one ray (MESH pair marches): the chord
-// [a, a + d] against every mesh unless it stays inside the ray's free ball.
+// [a, a + d] against every mesh, then the free ball at its end.  The pair
+// kernel has one call site (the compacted test loop), so the traversals are
+// inlined there (RR_MESH_INLINE_PAIRS): a call would save and restore the
+// live state of both rays around it.
+#ifndef RR_MESH_INLINE_PAIRS
+#define RR_MESH_INLINE_PAIRS 1
+#endif
 __device__ __forceinline__ void mesh_part(const DevParams& P, F3 a, F3 d, float len, bool& have,
                                           float& s_best, int& prim, int& hid, int& mrec, float& mfree) {
     for (int i = 0; i < P.n_meshes; ++i) {
         int rec = 0;
         float s = 0.f;
-        const bool h = mesh_chord(P.meshes[i], a, d, s, rec);
+        const bool h = RR_MESH_INLINE_PAIRS ? mesh_chord_impl(P.meshes[i], a, d, s, rec)
+                                            : mesh_chord(P.meshes[i], a, d, s, rec);
         if (consider(h, s, P.meshes[i].index, (kPrimMesh << 8) | i, have, s_best, prim, hid)) mrec = rec;
     }
     const F3 b = f3(a.x + d.x, a.y + d.y, a.z + d.z);
     float fr = 3.0e38f;
-    for (int i = 0; i < P.n_meshes; ++i) fr = fminf(fr, mesh_free(P.meshes[i], b, RR_MESH_FREE_CAP));
+    for (int i = 0; i < P.n_meshes; ++i)
+        fr = fminf(fr, RR_MESH_INLINE_PAIRS ? mesh_free_impl(P.meshes[i], b, RR_MESH_FREE_CAP)
+                                            : mesh_free(P.meshes[i], b, RR_MESH_FREE_CAP));
     mfree = fr;
 }
 
@@ -1759,7 +1801,9 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                 hit[r] = intersect<false>(P, a, b, sh[r], primr[r], hidr[r], md, mr, sfree[r]);
                 const F3 d = f3(b.x - a.x, b.y - a.y, b.z - a.z);
                 const float len = fmaf(sqrt_approx(fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z))), 1.0001f, 1e-30f);
+                float gd;
                 if (len < mfree[r]) mfree[r] -= len;     // the chord stays inside the free ball
+                else if ((gd = mesh_grid_free(P, a)) > len) mfree[r] = gd - len;   // distance grid
                 else pend |= 1u << r;
             }
             while (__any_sync(kFull, pend != 0u)) {
