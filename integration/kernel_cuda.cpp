@@ -290,7 +290,7 @@ int shim_march_both(const char* json, int width, int height, void* ref_out, void
                                                      static_cast<render::PixelOutcome*>(ref_out),
                                                      rays.size());
         const render::MarchFn cuda = render::detail::march_rays_cuda;
-        // the reference's row-at-a-time call pattern (render.cpp:124-128)
+        // the reference's row-at-a-time call pattern (render.cpp:72-76)
         for (int py = 0; py < height; ++py)
             cuda(ctx, rays.data() + static_cast<std::size_t>(py) * width,
                  static_cast<render::PixelOutcome*>(cuda_out) + static_cast<std::size_t>(py) * width,

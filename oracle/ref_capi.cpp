@@ -122,7 +122,7 @@ int refc_render(const char* json, int kernel, int workers, int width, int height
 }
 
 // Deterministic row subsample of a frame: rows row0, row0+step, ... of the
-// full width x height frame.  Same per-row work item as render.cpp:117-146
+// full width x height frame.  Same per-row work item as render.cpp:67-90
 // (pixel_direction per pixel, one MarchFn call per row, shade per pixel) on
 // a pool of `workers` threads; used to time the reference on frames too
 // large to render whole inside the bench budget.

@@ -881,7 +881,7 @@ int rr_set_scene(rr_ctx* c, const rr_metric_desc* m, const rr_scene_desc* sc) {
         }
     }
     // Re-uploading an unchanged scene (the reference's per-row MarchFn calls,
-    // render.cpp:124-128; per-frame uploads of a static scene) keeps the
+    // render.cpp:72-76; per-frame uploads of a static scene) keeps the
     // compiled program and its culling grid: compare against the pristine
     // parameter block of the last upload (launches mutate the live one).
     DevParams* np = new DevParams();

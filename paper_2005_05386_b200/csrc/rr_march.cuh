@@ -1000,7 +1000,12 @@ struct LaneCounters {
     unsigned jumps;            // integrated steps that were straight jumps (no RK4 / metric work)
 };
 
-enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3 };
+// kPassDyn: march_pair serving kPassHits or kPassShadow work chosen per call
+// at run time.  (A fused lit launch looping over both work kinds through one
+// such copy was measured: ptxas then moves every bump loop to the vector
+// datapath — BREV/FLO/LDC instead of UBREV/UFLO/LDCU — so the fused launch
+// keeps two loops and two copies.)
+enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3, kPassDyn = 4 };
 
 // ---------------------------------------------------------------------------
 // March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
@@ -1578,7 +1583,7 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
 // the 64 rays of the unit.
 template <int PASS>
 __device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
-                                          float light_d) {
+                                          float light_d, bool shadow = PASS == kPassShadow) {
     const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
     const float isp = rsqrtf(speed2);
     float L = (float)(k - 1) * P.cell_min;
@@ -1587,7 +1592,7 @@ __device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k,
     if (v.y != 0.f) te = fminf(te, __fdividef((v.y > 0.f ? P.hi[1] : P.lo[1]) - p.y, v.y));
     if (v.z != 0.f) te = fminf(te, __fdividef((v.z > 0.f ? P.hi[2] : P.lo[2]) - p.z, v.z));
     L = fminf(L, te * speed2 * isp);
-    if (PASS == kPassShadow) {
+    if (shadow) {
         const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
         L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
     }
@@ -1694,18 +1699,22 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                                            UnitStats& us, const DevLaunch& L, unsigned unit,
                                            int (&status)[2], int (&steps)[2], PairStage* stg,
                                            F3 q0 = F3{0.f, 0.f, 0.f},
-                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f) {
+                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f,
+                                           bool sh = false) {
     static_assert(KIND == kBumps || KIND == kDiffeo, "ray pairs: Gaussian bumps or the single twist");
+    // pass of this call: compile-time, or (kPassDyn) per work item
+    const bool kShadow = PASS == kPassShadow || (PASS == kPassDyn && sh);
+    const bool kHits = PASS == kPassHits || (PASS == kPassDyn && !sh);
     LaneCounters& cnt = us.cnt;
     const int lane = threadIdx.x & 31;
-    status[0] = status[1] = PASS == kPassShadow ? 1 : 0;
+    status[0] = status[1] = kShadow ? 1 : 0;
     steps[0] = steps[1] = 0;
     bool act[2] = {live0, live1};
     int step[2] = {0, 0};
     const F3 qq[2] = {q0, q1};
     const float dd[2] = {d20, d21};
     float light_d[2] = {0.f, 0.f};
-    if (PASS == kPassShadow) {
+    if (kShadow) {
         light_d[0] = sqrtf(d20);
         light_d[1] = sqrtf(d21);
     }
@@ -1734,7 +1743,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                     }
                     if (P.skip && lm == 0u) {
                         const int k = __ldg(P.skip_k + cell);
-                        if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r]);
+                        if (k >= 2) nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, step[r], qq[r], light_d[r], kShadow);
                     }
                 }
                 lmo |= nj[r] ? 0u : lm;
@@ -1842,17 +1851,17 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                 const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
                 const float sj = s * (float)nsub;            // hit position in reference steps
                 const int sub = min((int)sj, nsub - 1);
-                if constexpr (PASS == kPassShadow) {
+                if (kShadow) {
                     const F3 rr = f3(pt.x - qq[r].x, pt.y - qq[r].y, pt.z - qq[r].z);
                     status[r] = (rr.x * rr.x + rr.y * rr.y + rr.z * rr.z) < dd[r] ? 0 : 1;
                     steps[r] = step[r] + sub + 1;
                 } else {
                     const float th = ((float)step[r] + sj) * h;
                     const int nst = step[r] + sub + 1;
-                    if constexpr (PASS == kPassHits) {
+                    if (kHits) {
                         RayResult res{1, prim, nst, th, pt, f3(0.f, 0.f, 0.f)};
                         res.normal = hit_normal(P, hid, s, a, b, pt, mrec[r]);
-                        emit_primary<PASS>(P, L, unit, r, res);
+                        emit_primary<kPassHits>(P, L, unit, r, res);
                     } else {
                         stg->tp[r * kUnit + lane] = make_float4(th, pt.x, pt.y, pt.z);
                         stg->sp[r * kUnit + lane] = make_int2(1 | ((prim + 1) << 8), nst);
@@ -1860,7 +1869,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                     us.ref_steps += (unsigned)nst;
                 }
                 act[r] = false;
-            } else if (PASS == kPassShadow &&
+            } else if (kShadow &&
                        (b.x - qq[r].x) * (b.x - qq[r].x) + (b.y - qq[r].y) * (b.y - qq[r].y) +
                                (b.z - qq[r].z) * (b.z - qq[r].z) >= dd[r]) {
                 status[r] = 1;                               // reached the light's sphere
@@ -1872,13 +1881,13 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                 if (out || step[r] >= P.max_steps) {         // kernel_impl.hpp:87-91
                     const int nst = out ? step[r] : P.max_steps;
                     act[r] = false;
-                    if constexpr (PASS == kPassShadow) {
+                    if (kShadow) {
                         status[r] = 1;
                         steps[r] = nst;
                     } else {
-                        if constexpr (PASS == kPassHits) {
+                        if (kHits) {
                             RayResult res{0, -1, nst, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
-                            emit_primary<PASS>(P, L, unit, r, res);
+                            emit_primary<kPassHits>(P, L, unit, r, res);
                         } else {
                             stg->tp[r * kUnit + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                             stg->sp[r * kUnit + lane] = make_int2(0, nst);
@@ -2375,7 +2384,10 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
     auto fetch = [&]() {
         unsigned w = 0;
         if (lane == 0) w = atomicAdd(L.counter, 1u);
-        return __shfl_sync(kFull, w, 0);
+        // broadcast through REDUX (a uniform-register result), so that
+        // everything derived from the work item — the unified loop's
+        // per-item pass switch included — stays on the uniform datapath
+        return __reduce_max_sync(kFull, w);
     };
     // Two sequential loops (no if/else between the unit kinds inside one
     // loop body: that made ptxas treat the bump loops as divergent and drop

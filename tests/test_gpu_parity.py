@@ -83,9 +83,11 @@ def test_frame_parity_vs_oracle(renderer, oracle_lib, cfg_name, w, h):
 
 
 def test_culling_is_parity_neutral(renderer, oracle_lib):
-    """Per-warp bump culling (uniform 5.5 sigma, and the default equal-error
-    radii) must stay inside the parity contract, change the image by at most
-    rounding, and the equal-error radii must evaluate fewer bumps."""
+    """Per-warp bump culling (the default uniform 5.5 sigma radius, cull=1, and
+    the equal-error radii, cull=2) must stay inside the parity contract,
+    change the image by at most rounding, and the equal-error radii must
+    evaluate fewer bumps than the uniform radius, which evaluates fewer than
+    no culling (cull=0)."""
     from oracle.parity import compare_outcomes, compare_rgb
     from paper_2005_05386_b200.config import load_config
     cfg = load_config(os.path.join(ROOT, "configs", "c3_bumps16_1080p.json"))

@@ -1,6 +1,6 @@
 """GPU: the reference-side binding (integration/kernel_cuda.cpp) works as a
 drop-in inside the reference's own code: a MarchFn called row by row exactly
-like render.cpp:124-128, and render() routed as whole frames, both compared
+like render.cpp:72-76, and render() routed as whole frames, both compared
 with the reference's Scalar kernel under the parity contract."""
 import ctypes
 import json
