@@ -191,6 +191,8 @@ struct DevLaunch {
     uint8_t* outcomes;            // 48-byte PixelOutcome records: RAYS (by ray), frames when
                                   // non-null (outcome sink, row-major pixel index)
     int vec16;                    // ray-pair epilogue may store 16x4 RGB blocks as 16-B words
+    unsigned long long out_pixels;    // pixels of the rgb / hit-record buffers (RR_CHECKS bounds)
+    unsigned long long n_outcomes;    // records of the outcome sink (RR_CHECKS bounds)
     unsigned long long n_rays;
     unsigned* counter;            // unit dispensers [2] (zeroed per launch)
     unsigned long long* stats;    // [0] steps [1] errors [2] integrated [3] bump evals [4] rays

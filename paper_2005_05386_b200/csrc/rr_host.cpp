@@ -658,6 +658,15 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
         L.vis = reinterpret_cast<uint8_t*>(c->d_vis) + flag_bytes;
         RR_CUDA(c, cudaMemsetAsync(c->d_vis, 0, 2 * pairs * sizeof(unsigned), s));
     }
+    L.out_pixels = L.mode == rr::kModeFrame ? (unsigned long long)L.width * L.height
+                                            : (unsigned long long)L.n_units * rr::kUnit;
+    L.n_outcomes = L.mode == rr::kModeRays ? L.n_rays : (unsigned long long)L.width * L.height;
+#if RR_CHECKS
+    // debug launches: visibility bytes start as 0xff (never published), so
+    // the device checks catch a shade that reads an unpublished byte
+    if (c->P->n_lights > 0 && L.mode != rr::kModeRays && L.vis)
+        RR_CUDA(c, cudaMemsetAsync(L.vis, 0xff, L.out_pixels * (size_t)c->P->n_lights, s));
+#endif
     RR_CUDA(c, cudaMemsetAsync(c->d_aux, 0, 8 + 8 * rr::kStatSlots, s));
     L.counter = reinterpret_cast<unsigned*>(c->d_aux);
     L.stats = reinterpret_cast<unsigned long long*>(c->d_aux + 8);

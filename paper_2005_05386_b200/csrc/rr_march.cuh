@@ -89,6 +89,28 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_MIN_BLOCKS_MESH 6
 #endif
 
+// Device-side bounds / protocol checks (compute-sanitizer is not available
+// on this pool): build with -DRR_CHECKS=1 (tools/build_variants.sh) and run
+// tools/sanitize_frames.py; a failed check prints its site and traps.
+#ifndef RR_CHECKS
+#define RR_CHECKS 0
+#endif
+#if RR_CHECKS
+#include <cstdio>
+#define RR_CHECK(cond, what)                                                                   \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("RR_CHECK failed: %s (line %d) block %d thread %d\n", what, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define RR_CHECK(cond, what) \
+    do {                     \
+    } while (0)
+#endif
+
 struct F3 {
     float x, y, z;
 };
@@ -1620,7 +1642,9 @@ struct PairStage {
 // render::PixelOutcome (kernel.hpp:33-39, 48 B) from FP32 results: prim -1,
 // point 0 and t 0 unless hit, exactly as march_kernel's batch mode.
 __device__ __forceinline__ void write_outcome(uint8_t* base, unsigned long long idx, int status,
-                                              int prim, F3 pt, float t, int steps) {
+                                              int prim, F3 pt, float t, int steps,
+                                              unsigned long long cap) {
+    RR_CHECK(idx < cap, "outcome index");
     const bool hit = status == 1;
     const double x = hit ? (double)pt.x : 0.0, y = hit ? (double)pt.y : 0.0;
     const double z = hit ? (double)pt.z : 0.0, tt = hit ? (double)t : 0.0;
@@ -1964,6 +1988,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             const int ppu = kUnit / L.lpp;
             const int li = lane / ppu;
             HitRec hr{};
+            RR_CHECK(!live || pix < L.out_pixels, "hit record read (one-ray)");
             if (live) hr = L.hits[pix];
             const bool hit = live && (hr.status == 1);
             const F3 q = f3(hr.p[0], hr.p[1], hr.p[2]);
@@ -2011,9 +2036,10 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                     write_outcome(L.outcomes,
                                   L.mode == kModeRays ? ray_index
                                                       : (unsigned long long)py * L.width + px,
-                                  r.status, r.prim, r.point, r.t, r.steps);
+                                  r.status, r.prim, r.point, r.t, r.steps, L.n_outcomes);
                 if (L.mode == kModeRays) {
                 } else if constexpr (PASS == kPassHits) {
+                    RR_CHECK(pix < L.out_pixels, "hit record index (one-ray)");
                     HitRec hr;
                     hr.p[0] = r.point.x;
                     hr.p[1] = r.point.y;
@@ -2025,6 +2051,7 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                     hr.status = r.status;
                     L.hits[pix] = hr;
                 } else {
+                    RR_CHECK(pix < L.out_pixels, "rgb pixel index (one-ray)");
                     shade(P, r, L.rgb + 3 * pix);
                 }
             } else if (L.mode == kModeTiles && PASS == kPassShade) {
@@ -2110,10 +2137,11 @@ __device__ __forceinline__ void emit_primary(const DevParams& P, const DevLaunch
         h.n[1] = res.normal.y;
         h.n[2] = res.normal.z;
         h.status = res.status;
+        RR_CHECK(live && pix < L.out_pixels, "hit record index");
         L.hits[pix] = h;
         if (L.outcomes)
             write_outcome(L.outcomes, (unsigned long long)py * L.width + px, res.status, res.prim,
-                          res.point, res.t, res.steps);
+                          res.point, res.t, res.steps, L.n_outcomes);
     }
 }
 
@@ -2172,6 +2200,7 @@ __device__ __forceinline__ void store_pair_rgb(const DevLaunch& L, unsigned unit
         __syncwarp();
         const unsigned long long rowpix = __shfl_sync(kFull, pix[0], (lane / 3 & 3) * 8);
         if (lane < 12) {
+            RR_CHECK(rowpix + 2 * kMicroW <= L.out_pixels && ((3 * rowpix) & 15) == 0, "rgb block row");
             const uint4 v = reinterpret_cast<const uint4*>(stg->rgb)[lane];
             *reinterpret_cast<uint4*>(L.rgb + 3 * rowpix + 16 * (lane % 3)) = v;
         }
@@ -2181,6 +2210,7 @@ __device__ __forceinline__ void store_pair_rgb(const DevLaunch& L, unsigned unit
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         if (live[r] || (inr[r] && L.mode == kModeTiles)) {
+            RR_CHECK(pix[r] < L.out_pixels, "rgb pixel index");
             uint8_t* dst = L.rgb + 3 * pix[r];
             const uint32_t c = live[r] ? rgb[r] : 0u;
             dst[0] = (uint8_t)(c & 0xff);
@@ -2249,7 +2279,7 @@ __device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch
                     pixel_of(L, 2 * unit + r, lane, inr, lv, px, py, pix);
                     idx = (unsigned long long)py * L.width + px;
                 }
-                write_outcome(L.outcomes, idx, status, (sp.x >> 8) - 1, pt, tp.x, sp.y);
+                write_outcome(L.outcomes, idx, status, (sp.x >> 8) - 1, pt, tp.x, sp.y, L.n_outcomes);
             }
         }
         if (!rays) store_pair_rgb(L, unit, lane, rgb, stg);
@@ -2324,12 +2354,17 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
     if (nl > 1) {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
-            if (live[r]) L.vis[pix[r] * (unsigned)nl + l] = vis[r] ? 1 : 0;
+            if (live[r]) {
+                RR_CHECK(pix[r] < L.out_pixels, "visibility index");
+                L.vis[pix[r] * (unsigned)nl + l] = vis[r] ? 1 : 0;
+            }
         __threadfence();
         __syncwarp();
         unsigned before = 0;
+        RR_CHECK(unit < (L.n_units + 1) / 2, "unit counter index");
         if (lane == 0) before = atomicAdd(L.done + unit, 1u);
         before = __shfl_sync(kFull, before, 0);
+        RR_CHECK(before < (unsigned)nl, "lights-finished counter overrun");
         last = before == (unsigned)nl - 1u;
         if (last) __threadfence();
     }
@@ -2342,6 +2377,12 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
             float contrib = 0.f;
             if (status[r] == 1) {
                 for (int k = 0; k < nl; ++k) {
+#if RR_CHECKS
+                    // debug launches pre-fill the visibility bytes with 0xff:
+                    // the last finisher must see every other light's byte
+                    RR_CHECK(k == l || __ldcg(L.vis + pix[r] * (unsigned)nl + k) <= 1u,
+                             "visibility byte not yet published");
+#endif
                     const bool lit = k == l ? vis[r] : __ldcg(L.vis + pix[r] * (unsigned)nl + k) != 0;
                     if (!lit) continue;
                     const DevLight& Lk = P.lights[k];
@@ -2415,6 +2456,7 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
             const unsigned w = work - n_primary;
             const unsigned unit = w / (unsigned)nl;
             if constexpr (PASS == kPassFused) {
+                RR_CHECK(unit < n_pairs, "ready flag index");
                 // whole-warp polling of the unit's ready flag (dispensed
                 // n_pairs items after its primary unit: normally already set)
                 for (;;) {
