@@ -48,7 +48,9 @@ constexpr int kStatSlots = 11;    // 64-bit device counters per launch (DevLaunc
 constexpr float kBeta = -1.3862943611198906f;   // -2 ln 2
 constexpr float kHalfLog2e = 0.7213475204444817f;
 
-enum Kind : int { kEuclid = 0, kBumps = 1, kGraphGeneral = 2, kDiffeo = 3 };
+enum Kind : int { kEuclid = 0, kBumps = 1, kGraphGeneral = 2, kDiffeo = 3,
+                  kBumpsRk23 = 4 /* kernel-template tag only: Gaussian bumps with the adaptive
+                                    rk23 scheme on the ray-pair kernel (P.kind is kBumps) */ };
 enum Stage : int { kStageAffine = 0, kStageTwist = 1, kStageBump = 2, kStageBend = 3 };
 enum Prim : int { kPrimGrid = 0, kPrimSphere = 1, kPrimHalfSpace = 2, kPrimMesh = 3 };
 enum Mode : int { kModeFrame = 0, kModeTiles = 1, kModeRays = 2 };

@@ -22,6 +22,8 @@ cudaError_t launch_family_pair(const DevParams& P, const DevLaunch& L, cudaStrea
                                const char** name);
 cudaError_t launch_family_pair_twist(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
                                      const char** name);
+cudaError_t launch_family_pair_rk23(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                    const char** name);
 cudaError_t launch_family_bumps(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
                                 const char** name);
 cudaError_t launch_family_diffeo(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,

@@ -275,9 +275,11 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
     if (launches) {
         // with lights: hit + shadow launches, except the fused ray-pair kernel
         const bool lit = P.n_lights > 0 && L.mode != kModeRays;
-        const bool fused = RR_RAY_PAIRS && RR_X2_FUSED && P.scheme == 1 &&
-                           ((P.kind == kBumps && P.n_meshes == 0) ||
-                            (RR_TWIST_PAIRS && P.kind == kDiffeo && P.n_stages == 1 &&
+        const bool fused = RR_RAY_PAIRS && RR_X2_FUSED &&
+                           ((P.kind == kBumps && P.n_meshes == 0 &&
+                             (P.scheme == 1 || (RR_RK23_PAIRS && P.scheme == 2))) ||
+                            (P.scheme == 1 &&
+                             RR_TWIST_PAIRS && P.kind == kDiffeo && P.n_stages == 1 &&
                              P.stages[0].kind == kStageTwist && (RR_TWIST_PAIRS_MESH || P.n_meshes == 0)));
         *launches = lit && !fused ? 2 : 1;
     }
@@ -288,6 +290,10 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
 #if RR_RAY_PAIRS
             if (P.scheme == 1 && P.n_meshes == 0)   // ray-pair frames and batches (RK4, mesh-free)
                 return launch_family_pair(P, L, stream, num_sms, kernel_name);
+#if RR_RK23_PAIRS
+            if (P.scheme == 2 && P.n_meshes == 0)   // adaptive rk23 (EXT), mesh-free
+                return launch_family_pair_rk23(P, L, stream, num_sms, kernel_name);
+#endif
 #endif
             return launch_family_bumps(P, L, stream, num_sms, kernel_name);
         case kGraphGeneral:

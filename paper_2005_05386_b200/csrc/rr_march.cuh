@@ -44,6 +44,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 1: single-twist RK4 frames WITH meshes on the ray-pair kernel too
 #define RR_TWIST_PAIRS_MESH 0
 #endif
+#ifndef RR_RK23_PAIRS
+// 1: Gaussian-bump rk23 frames (mesh-free) on the ray-pair kernel
+#define RR_RK23_PAIRS 1
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -74,6 +78,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_MIN_BLOCKS_X2_TWIST_MESH
 #define RR_MIN_BLOCKS_X2_TWIST_MESH 6   // ray-pair single-twist frames with meshes (C4)
+#endif
+#ifndef RR_MIN_BLOCKS_X2_RK23
+#define RR_MIN_BLOCKS_X2_RK23 5         // ray-pair rk23 (FSAL stage + error terms per ray pair)
 #endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
@@ -1605,7 +1612,8 @@ __device__ __forceinline__ void raygen(const DevCamera& c, int px, int py, int w
 // the 64 rays of the unit.
 template <int PASS>
 __device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k, int step, F3 q,
-                                          float light_d, bool shadow = PASS == kPassShadow) {
+                                          float light_d, bool shadow = PASS == kPassShadow,
+                                          float inv_step = 0.f) {
     const float speed2 = fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z));
     const float isp = rsqrtf(speed2);
     float L = (float)(k - 1) * P.cell_min;
@@ -1618,7 +1626,8 @@ __device__ __forceinline__ int jump_steps(const DevParams& P, F3 p, F3 v, int k,
         const F3 r = f3(p.x - q.x, p.y - q.y, p.z - q.z);
         L = fminf(L, light_d - sqrtf(fmaf(r.x, r.x, fmaf(r.y, r.y, r.z * r.z))));
     }
-    const float n = floorf(L * isp * P.inv_h) - 1.f;   // fast division: the -1 step margin covers it
+    // fast division: the -1 step margin covers it
+    const float n = floorf(L * isp * (inv_step > 0.f ? inv_step : P.inv_h)) - 1.f;
     const int nj = (int)fminf(fmaxf(n, 0.f), (float)(P.max_steps - step));
     return nj < 2 ? 0 : nj;
 }
@@ -1718,6 +1727,216 @@ __device__ __forceinline__ void mesh_part(const DevParams& P, F3 a, F3 d, float 
     mfree = fr;
 }
 
+// EXTENSION: the adaptive Bogacki-Shampine 3(2) march (march_unit_rk23,
+// oracle/rro.c rk23_core) for a ray pair: per-ray step size h, FSAL k1, the
+// three stage evaluations packed (FFMA2) with per-ray coefficients, the
+// embedded error norm and the step-size control per ray; bump mask from the
+// culling level that covers each ray's h, OR-reduced over the warp's 64 rays;
+// rays at h_max in empty cells take straight jumps of h_max steps.  Output
+// rules exactly as march_pair.
+template <int NB, int PASS>
+__device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, bool live1, P3 p, P3 v,
+                                                UnitStats& us, const DevLaunch& L, unsigned unit,
+                                                int (&status)[2], int (&steps)[2], PairStage* stg,
+                                                F3 q0, F3 q1, float d20, float d21) {
+    constexpr bool kShadow = PASS == kPassShadow;
+    constexpr bool kHits = PASS == kPassHits;
+    LaneCounters& cnt = us.cnt;
+    const int lane = threadIdx.x & 31;
+    status[0] = status[1] = kShadow ? 1 : 0;
+    steps[0] = steps[1] = 0;
+    bool act[2] = {live0, live1};
+    const F3 qq[2] = {q0, q1};
+    const float dd[2] = {d20, d21};
+    float light_d[2] = {0.f, 0.f};
+    if (kShadow) {
+        light_d[0] = sqrtf(d20);
+        light_d[1] = sqrtf(d21);
+    }
+    const float h0 = P.h, hmin = h0 / 64.f, hmax = 4.f * h0, tol = P.tol;
+    const float inv_hmax = 0.25f * P.inv_h;
+    float hh[2] = {h0, h0}, tt[2] = {0.f, 0.f};
+    int stp[2] = {0, 0}, att[2] = {0, 0};
+    bool have_k1[2] = {false, false};
+    P3 k1v{bc2(0.f), bc2(0.f), bc2(0.f)};
+    float sfree[2] = {0.f, 0.f};
+    for (;;) {
+        if (!__any_sync(kFull, act[0] || act[1])) break;
+        cnt.lane_slots += 2;
+        int nj[2] = {0, 0};
+        uint32_t lmo = 0u;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (!act[r]) continue;
+            unsigned cell = 0;
+            if (P.cull) cell = cell_of(P, ray_of(p, r));
+            // straight jumps: a ray at h_max in a cell empty at the widest
+            // level (dilated for 4 h0) moves x + j h_max y (rk23 in flat space)
+            if (P.skip && P.cull && hh[r] >= hmax && __ldg(P.cull_masks + 2u * P.cull_cells + cell) == 0u) {
+                const int k = __ldg(P.skip_k + cell);
+                if (k >= 2)
+                    nj[r] = jump_steps<PASS>(P, ray_of(p, r), ray_of(v, r), k, stp[r], qq[r], light_d[r],
+                                             kShadow, inv_hmax);
+            }
+            if (!nj[r]) {   // the mask level whose dilation covers this ray's h
+                const unsigned lvl = hh[r] <= h0 ? 0u : (hh[r] <= 2.f * h0 ? 1u : 2u);
+                lmo |= P.cull ? __ldg(P.cull_masks + lvl * P.cull_cells + cell) : P.all_mask;
+            }
+        }
+        const uint32_t um = __reduce_or_sync(kFull, lmo);
+        // first step of a ray: k1 = a(x, y) (FSAL afterwards)
+        if (!__all_sync(kFull, (have_k1[0] || !act[0]) && (have_k1[1] || !act[1]))) {
+            const P3 a = accel_bumps_x2<NB>(P, um, p, v);
+            k1v = P3{sel2(have_k1[0], have_k1[1], k1v.x, a.x), sel2(have_k1[0], have_k1[1], k1v.y, a.y),
+                     sel2(have_k1[0], have_k1[1], k1v.z, a.z)};
+            have_k1[0] = have_k1[1] = true;
+        }
+        P3 xn = p, vn = v, k4v{bc2(0.f), bc2(0.f), bc2(0.f)};
+        float e[2] = {0.f, 0.f};
+        const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
+        if (!__all_sync(kFull, jw0 && jw1)) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (act[r] && !nj[r]) cnt.bump_evals += 3u * __popc(um);
+            const F2 H = mk2(hh[0], hh[1]);
+            const F2 c05 = mul2(bc2(0.5f), H), c075 = mul2(bc2(0.75f), H);
+            // stages k2, k3, k4 (march_unit_rk23 order of operations)
+            P3 ps{fma2(c05, v.x, p.x), fma2(c05, v.y, p.y), fma2(c05, v.z, p.z)};
+            P3 vs{fma2(c05, k1v.x, v.x), fma2(c05, k1v.y, v.y), fma2(c05, k1v.z, v.z)};
+            const P3 k2x = vs;
+            const P3 k2v = accel_bumps_x2<NB>(P, um, ps, vs);
+            ps = P3{fma2(c075, k2x.x, p.x), fma2(c075, k2x.y, p.y), fma2(c075, k2x.z, p.z)};
+            vs = P3{fma2(c075, k2v.x, v.x), fma2(c075, k2v.y, v.y), fma2(c075, k2v.z, v.z)};
+            const P3 k3x = vs;
+            const P3 k3v = accel_bumps_x2<NB>(P, um, ps, vs);
+            const F2 c1 = mul2(bc2(2.f / 9.f), H), c2 = mul2(bc2(1.f / 3.f), H), c3 = mul2(bc2(4.f / 9.f), H);
+            xn = P3{fma2(c1, v.x, fma2(c2, k2x.x, fma2(c3, k3x.x, p.x))),
+                    fma2(c1, v.y, fma2(c2, k2x.y, fma2(c3, k3x.y, p.y))),
+                    fma2(c1, v.z, fma2(c2, k2x.z, fma2(c3, k3x.z, p.z)))};
+            vn = P3{fma2(c1, k1v.x, fma2(c2, k2v.x, fma2(c3, k3v.x, v.x))),
+                    fma2(c1, k1v.y, fma2(c2, k2v.y, fma2(c3, k3v.y, v.y))),
+                    fma2(c1, k1v.z, fma2(c2, k2v.z, fma2(c3, k3v.z, v.z)))};
+            const P3 k4x = vn;
+            k4v = accel_bumps_x2<NB>(P, um, xn, vn);
+            // embedded error, mixed abs/rel scale, per ray
+            const F2 e1 = mul2(bc2(-5.f / 72.f), H), e2 = mul2(bc2(1.f / 12.f), H);
+            const F2 e3 = mul2(bc2(1.f / 9.f), H), e4 = mul2(bc2(-1.f / 8.f), H);
+            const F2 ka[6] = {v.x, v.y, v.z, k1v.x, k1v.y, k1v.z};
+            const F2 kb[6] = {k2x.x, k2x.y, k2x.z, k2v.x, k2v.y, k2v.z};
+            const F2 kc[6] = {k3x.x, k3x.y, k3x.z, k3v.x, k3v.y, k3v.z};
+            const F2 kd[6] = {k4x.x, k4x.y, k4x.z, k4v.x, k4v.y, k4v.z};
+            const F2 y0[6] = {p.x, p.y, p.z, v.x, v.y, v.z};
+            const F2 y1[6] = {xn.x, xn.y, xn.z, vn.x, vn.y, vn.z};
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const F2 err = fma2(e1, ka[i], fma2(e2, kb[i], fma2(e3, kc[i], mul2(e4, kd[i]))));
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const float sc = tol * (1.f + fmaxf(fabsf(get2(y0[i], r)), fabsf(get2(y1[i], r))));
+                    e[r] = fmaxf(e[r], __fdividef(fabsf(get2(err, r)), sc));
+                }
+            }
+        }
+        if (nj[0] | nj[1]) {                                 // straight jumps of nj h_max steps
+            const F2 hn = mk2(hmax * (float)nj[0], hmax * (float)nj[1]);
+            const bool j0 = nj[0] != 0, j1 = nj[1] != 0;
+            const P3 xj{fma2(hn, v.x, p.x), fma2(hn, v.y, p.y), fma2(hn, v.z, p.z)};
+            xn = P3{sel2(j0, j1, xj.x, xn.x), sel2(j0, j1, xj.y, xn.y), sel2(j0, j1, xj.z, xn.z)};
+            vn = P3{sel2(j0, j1, v.x, vn.x), sel2(j0, j1, v.y, vn.y), sel2(j0, j1, v.z, vn.z)};
+            const F2 z = bc2(0.f);
+            k4v = P3{sel2(j0, j1, z, k4v.x), sel2(j0, j1, z, k4v.y), sel2(j0, j1, z, k4v.z)};
+            if (j0) e[0] = 0.f;
+            if (j1) e[1] = 0.f;
+        }
+        bool upd[2] = {false, false};   // accepted, still marching: the state moves to (xn, vn)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (!act[r]) continue;
+            const bool accept = e[r] <= 1.f || hh[r] <= hmin;
+            const int nsub = nj[r] ? nj[r] : 1;
+            const float hstep = nj[r] ? hmax * (float)nj[r] : hh[r];
+            cnt.steps_integrated += 1;
+            cnt.jumps += nj[r] ? 1u : 0u;
+            att[r] += nsub;
+            if (accept) {
+                const F3 a = ray_of(p, r), b = ray_of(xn, r);
+                float s = 0.f, md = 0.f;
+                int prim = -1, hid = 0, mr = 0;
+                if (intersect<false>(P, a, b, s, prim, hid, md, mr, sfree[r])) {
+                    const F3 pt = f3(fmaf(s, b.x - a.x, a.x), fmaf(s, b.y - a.y, a.y), fmaf(s, b.z - a.z, a.z));
+                    const int sub = min((int)(s * (float)nsub), nsub - 1);
+                    if constexpr (kShadow) {
+                        const F3 rr = f3(pt.x - qq[r].x, pt.y - qq[r].y, pt.z - qq[r].z);
+                        status[r] = (rr.x * rr.x + rr.y * rr.y + rr.z * rr.z) < dd[r] ? 0 : 1;
+                        steps[r] = stp[r] + sub + 1;
+                    } else {
+                        const float th = fmaf(s, hstep, tt[r]);
+                        const int nst = stp[r] + sub + 1;
+                        if constexpr (kHits) {
+                            RayResult res{1, prim, nst, th, pt, f3(0.f, 0.f, 0.f)};
+                            res.normal = hit_normal(P, hid, s, a, b, pt, 0);
+                            emit_primary<kPassHits>(P, L, unit, r, res);
+                        } else {
+                            stg->tp[r * kUnit + lane] = make_float4(th, pt.x, pt.y, pt.z);
+                            stg->sp[r * kUnit + lane] = make_int2(1 | ((prim + 1) << 8), nst);
+                        }
+                        us.ref_steps += (unsigned)nst;
+                    }
+                    act[r] = false;
+                } else {
+                    stp[r] += nsub;
+                    const bool crossed = kShadow && (b.x - qq[r].x) * (b.x - qq[r].x) +
+                                                            (b.y - qq[r].y) * (b.y - qq[r].y) +
+                                                            (b.z - qq[r].z) * (b.z - qq[r].z) >= dd[r];
+                    if (crossed || !inside_bounds(P, b)) {
+                        act[r] = false;
+                        if constexpr (kShadow) {
+                            status[r] = 1;
+                            steps[r] = stp[r];
+                        } else {
+                            if constexpr (kHits) {
+                                RayResult res{0, -1, stp[r], 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
+                                emit_primary<kPassHits>(P, L, unit, r, res);
+                            } else {
+                                stg->tp[r * kUnit + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                                stg->sp[r * kUnit + lane] = make_int2(0, stp[r]);
+                            }
+                            us.ref_steps += (unsigned)stp[r];
+                        }
+                    } else {
+                        tt[r] += hstep;
+                        upd[r] = true;
+                    }
+                }
+            }
+            if (act[r]) {
+                const float fac = e[r] > 0.f ? fminf(5.f, fmaxf(0.2f, 0.9f * ex2(-__log2f(e[r]) / 3.f))) : 5.f;
+                hh[r] = fminf(hmax, fmaxf(hmin, hh[r] * fac));
+                if (stp[r] >= P.max_steps || att[r] >= 16 * P.max_steps) {
+                    act[r] = false;
+                    if constexpr (kShadow) {
+                        status[r] = 1;
+                        steps[r] = stp[r];
+                    } else {
+                        if constexpr (kHits) {
+                            RayResult res{0, -1, stp[r], 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
+                            emit_primary<kPassHits>(P, L, unit, r, res);
+                        } else {
+                            stg->tp[r * kUnit + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            stg->sp[r * kUnit + lane] = make_int2(0, stp[r]);
+                        }
+                        us.ref_steps += (unsigned)stp[r];
+                    }
+                }
+            }
+        }
+        p = P3{sel2(upd[0], upd[1], xn.x, p.x), sel2(upd[0], upd[1], xn.y, p.y), sel2(upd[0], upd[1], xn.z, p.z)};
+        v = P3{sel2(upd[0], upd[1], vn.x, v.x), sel2(upd[0], upd[1], vn.y, v.y), sel2(upd[0], upd[1], vn.z, v.z)};
+        k1v = P3{sel2(upd[0], upd[1], k4v.x, k1v.x), sel2(upd[0], upd[1], k4v.y, k1v.y),
+                 sel2(upd[0], upd[1], k4v.z, k1v.z)};
+    }
+}
+
 template <int KIND, int NB, int PASS, bool MESH>
 __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool live1, P3 p, P3 v,
                                            UnitStats& us, const DevLaunch& L, unsigned unit,
@@ -1725,7 +1944,12 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                                            F3 q0 = F3{0.f, 0.f, 0.f},
                                            F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f,
                                            bool sh = false) {
-    static_assert(KIND == kBumps || KIND == kDiffeo, "ray pairs: Gaussian bumps or the single twist");
+    static_assert(KIND == kBumps || KIND == kDiffeo || KIND == kBumpsRk23,
+                  "ray pairs: Gaussian bumps (RK4 / rk23) or the single twist");
+    if constexpr (KIND == kBumpsRk23) {
+        march_pair_rk23<NB, PASS>(P, live0, live1, p, v, us, L, unit, status, steps, stg, q0, q1, d20, d21);
+        return;
+    }
     // pass of this call: compile-time, or (kPassDyn) per work item
     const bool kShadow = PASS == kPassShadow || (PASS == kPassDyn && sh);
     const bool kHits = PASS == kPassHits || (PASS == kPassDyn && !sh);
@@ -2410,7 +2634,8 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
 //                 No deadlock: a flag's producer already holds a running warp
 //                 and waits on nothing.
 template <int KIND, int NB, int PASS, bool MESH>
-__global__ void __launch_bounds__(kThreads, KIND == kDiffeo ? (MESH ? RR_MIN_BLOCKS_X2_TWIST_MESH
+__global__ void __launch_bounds__(kThreads, KIND == kBumpsRk23 ? RR_MIN_BLOCKS_X2_RK23
+                                               : KIND == kDiffeo ? (MESH ? RR_MIN_BLOCKS_X2_TWIST_MESH
                                                                      : RR_MIN_BLOCKS_X2_TWIST)
                                                : NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
                                                : (PASS == kPassFused ? RR_MIN_BLOCKS_X2_FUSED
