@@ -559,6 +559,7 @@ def run_b200(args, cfg):
         extras = {}
         for name, cpu_kind in (("c1_gauss1_512", "reference"), ("c2_flat_1080p", "reference"),
                                ("c4_twist_1080p", "reference"), ("c4_twist_mesh_1080p", "oracle"),
+                               ("c4_twist_bend_mesh_1080p", "oracle"),
                                ("c5_bumps16_4k", "reference"), ("c3_bumps16_rk23_1080p", "oracle")):
             ecfg = load_config(os.path.join(ROOT, "configs", name + ".json"))
             ew, eh = ecfg.output.width, ecfg.output.height

@@ -48,6 +48,11 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 1: Gaussian-bump rk23 frames (mesh-free) on the ray-pair kernel
 #define RR_RK23_PAIRS 1
 #endif
+#ifndef RR_X2_HITS_STAGED
+// 1: primary hit records of the lit launch are produced after the unit's
+// march from shared-memory staged chords (hit_normal out of the march loop)
+#define RR_X2_HITS_STAGED 1
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -58,6 +63,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_BODY
 #define RR_X2_BODY 1   // bump-body operand order of the ray-pair march (see accel_bumps_x2)
+#endif
+#ifndef RR_X2_RK4_UNROLL_LIT
+#define RR_X2_RK4_UNROLL_LIT RR_X2_RK4_UNROLL
 #endif
 #ifndef RR_MIN_BLOCKS_X2
 // ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
@@ -1646,6 +1654,10 @@ struct PairStage {
     float4 tp[2 * kUnit];     // t, point.x, point.y, point.z
     int2 sp[2 * kUnit];       // status | (prim + 1) << 8, steps
     uint32_t rgb[48];         // 4 rows x 48 bytes of the 16x4 pixel block
+    float4* chord;            // kPassHits (RR_X2_HITS_STAGED): 4 x 32 float4 per ray pair unit —
+                              // [r][lane] = (chord start, s), [2 + r][lane] = (chord end,
+                              // hid | mrec << 12) — so the hit normal and the 32-B hit
+                              // record are produced after the march, not inside its loop
 };
 
 // render::PixelOutcome (kernel.hpp:33-39, 48 B) from FP32 results: prim -1,
@@ -1872,11 +1884,16 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
                     } else {
                         const float th = fmaf(s, hstep, tt[r]);
                         const int nst = stp[r] + sub + 1;
-                        if constexpr (kHits) {
+                        if constexpr (kHits && !RR_X2_HITS_STAGED) {
                             RayResult res{1, prim, nst, th, pt, f3(0.f, 0.f, 0.f)};
                             res.normal = hit_normal(P, hid, s, a, b, pt, 0);
                             emit_primary<kPassHits>(P, L, unit, r, res);
                         } else {
+                            if constexpr (kHits) {
+                                stg->chord[r * kUnit + lane] = make_float4(a.x, a.y, a.z, s);
+                                stg->chord[(2 + r) * kUnit + lane] =
+                                    make_float4(b.x, b.y, b.z, __int_as_float(hid));
+                            }
                             stg->tp[r * kUnit + lane] = make_float4(th, pt.x, pt.y, pt.z);
                             stg->sp[r * kUnit + lane] = make_int2(1 | ((prim + 1) << 8), nst);
                         }
@@ -1894,7 +1911,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
                             status[r] = 1;
                             steps[r] = stp[r];
                         } else {
-                            if constexpr (kHits) {
+                            if constexpr (kHits && !RR_X2_HITS_STAGED) {
                                 RayResult res{0, -1, stp[r], 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
                                 emit_primary<kPassHits>(P, L, unit, r, res);
                             } else {
@@ -1918,7 +1935,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
                         status[r] = 1;
                         steps[r] = stp[r];
                     } else {
-                        if constexpr (kHits) {
+                        if constexpr (kHits && !RR_X2_HITS_STAGED) {
                             RayResult res{0, -1, stp[r], 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
                             emit_primary<kPassHits>(P, L, unit, r, res);
                         } else {
@@ -2011,12 +2028,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
         } else {                                             // RK4 (integrate.hpp:63-93)
             P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
             P3 ps = p, vs = v;
-#if RR_X2_RK4_UNROLL
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
-            for (int st = 0; st < 4; ++st) {   // one call site: the bump block is inlined once
+            auto stage = [&](int st) {
                 const P3 a = accel_bumps_x2<NB>(P, um, ps, vs);
                 const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
                 sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
@@ -2024,6 +2036,16 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                 const F2 cc = st < 2 ? half : full;
                 ps = P3{fma2(cc, vs.x, p.x), fma2(cc, vs.y, p.y), fma2(cc, vs.z, p.z)};
                 vs = P3{fma2(cc, a.x, v.x), fma2(cc, a.y, v.y), fma2(cc, a.z, v.z)};
+            };
+            // unlit frames: the four stages unrolled (four bump loops); the lit
+            // launch carries two march copies, RR_X2_RK4_UNROLL_LIT picks its form
+            constexpr bool kUnrollStages = PASS == kPassShade ? RR_X2_RK4_UNROLL : RR_X2_RK4_UNROLL_LIT;
+            if constexpr (kUnrollStages) {
+#pragma unroll
+                for (int st = 0; st < 4; ++st) stage(st);
+            } else {
+#pragma unroll 1
+                for (int st = 0; st < 4; ++st) stage(st);   // one call site: the bump block is inlined once
             }
             dp = P3{mul2(sixth, sx.x), mul2(sixth, sx.y), mul2(sixth, sx.z)};
             vn = P3{fma2(sixth, sv.x, v.x), fma2(sixth, sv.y, v.y), fma2(sixth, sv.z, v.z)};
@@ -2106,11 +2128,16 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                 } else {
                     const float th = ((float)step[r] + sj) * h;
                     const int nst = step[r] + sub + 1;
-                    if (kHits) {
+                    if (kHits && !RR_X2_HITS_STAGED) {
                         RayResult res{1, prim, nst, th, pt, f3(0.f, 0.f, 0.f)};
                         res.normal = hit_normal(P, hid, s, a, b, pt, mrec[r]);
                         emit_primary<kPassHits>(P, L, unit, r, res);
                     } else {
+                        if (kHits) {
+                            stg->chord[r * kUnit + lane] = make_float4(a.x, a.y, a.z, s);
+                            stg->chord[(2 + r) * kUnit + lane] =
+                                make_float4(b.x, b.y, b.z, __int_as_float(hid | (mrec[r] << 12)));
+                        }
                         stg->tp[r * kUnit + lane] = make_float4(th, pt.x, pt.y, pt.z);
                         stg->sp[r * kUnit + lane] = make_int2(1 | ((prim + 1) << 8), nst);
                     }
@@ -2133,7 +2160,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                         status[r] = 1;
                         steps[r] = nst;
                     } else {
-                        if (kHits) {
+                        if (kHits && !RR_X2_HITS_STAGED) {
                             RayResult res{0, -1, nst, 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
                             emit_primary<kPassHits>(P, L, unit, r, res);
                         } else {
@@ -2479,6 +2506,29 @@ __device__ __forceinline__ void pair_primary(const DevParams& P, const DevLaunch
     int st[2], stp[2];
     march_pair<KIND, NB, PASS, MESH>(P, live[0], live[1], pair_of(pos[0], pos[1]), pair_of(dir[0], dir[1]),
                          us, L, unit, st, stp, stg);
+    if constexpr (PASS == kPassHits && RR_X2_HITS_STAGED) {
+        // hit records (normal, 32-B HitRec) + outcome records from the stage
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (!live[r] || rays) continue;
+            const float4 tp = stg->tp[r * kUnit + lane];
+            const int2 sp = stg->sp[r * kUnit + lane];
+            const int status = sp.x & 0xff;
+            RayResult res{status, (sp.x >> 8) - 1, sp.y, tp.x, f3(tp.y, tp.z, tp.w), f3(0.f, 0.f, 0.f)};
+            if (status == 1) {
+                const float4 ca = stg->chord[r * kUnit + lane];
+                const float4 cb = stg->chord[(2 + r) * kUnit + lane];
+                const int hm = __float_as_int(cb.w);
+                res.normal = hit_normal(P, hm & 0xfff, ca.w, f3(ca.x, ca.y, ca.z), f3(cb.x, cb.y, cb.z),
+                                        res.point, hm >> 12);
+            } else {
+                res.prim = -1;
+            }
+            emit_primary<kPassHits>(P, L, unit, r, res);
+        }
+        __syncwarp();
+    }
     if constexpr (PASS == kPassShade) {
         __syncwarp();
         uint32_t rgb[2];
@@ -2661,6 +2711,10 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
     // n_primary carries that item into the shadow loop.
     __shared__ PairStage s_stage[kThreads / 32];
     PairStage* stg = &s_stage[threadIdx.x >> 5];
+    if constexpr (RR_X2_HITS_STAGED && (PASS == kPassHits || PASS == kPassFused)) {
+        __shared__ float4 s_chord[kThreads / 32][4 * kUnit];
+        stg->chord = s_chord[threadIdx.x >> 5];
+    }
     unsigned work = fetch();
     if constexpr (PASS != kPassShadow) {
         constexpr int kPrim = PASS == kPassFused ? kPassHits : PASS;

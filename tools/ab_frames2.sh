@@ -1,0 +1,7 @@
+# A/B of build/exp variants on the C3 rk23 / lit frames under gpurun
+cd ${GRAFT_REPO_ROOT:-.}
+echo "== default"; python tools/prof_frame.py configs/c3_bumps16_rk23_1080p.json configs/c3_bumps16_shadows_1080p.json --frames 10 --warmup 2 --time
+for v in build/exp/librray_*.so; do
+  echo "== $(basename $v .so)"
+  RRAY_CUDA_LIB=$PWD/$v python tools/prof_frame.py configs/c3_bumps16_rk23_1080p.json configs/c3_bumps16_shadows_1080p.json --frames 10 --warmup 2 --time
+done
