@@ -62,7 +62,7 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_X2_RK4_UNROLL 1   // 4 RK4 stages unrolled (4 small bump loops): C3 10.32 -> 9.91 ms, lights 16.94 -> 16.66
 #endif
 #ifndef RR_X2_BODY
-#define RR_X2_BODY 1   // bump-body operand order of the ray-pair march (see accel_bumps_x2)
+#define RR_X2_BODY 3   // bump body of the ray-pair march: 1 = G accumulated, 3 = T-trick (accel_bumps_x2)
 #endif
 #ifndef RR_X2_RK4_UNROLL_LIT
 #define RR_X2_RK4_UNROLL_LIT RR_X2_RK4_UNROLL
@@ -275,38 +275,33 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
     auto body = [&](const DevBumpB& b, bool neg) {
         const F2 dx = add2(p.x, ld2(b.ncx)), dy = add2(p.y, ld2(b.ncy)), dz = add2(p.z, ld2(b.ncz));
         const F2 gx = mul2(dx, ld2(b.kx)), gy = mul2(dy, ld2(b.ky)), gz = mul2(dz, ld2(b.kz));
-#if RR_X2_BODY == 2
-        // q = d.g + la and t = y.g interleaved with g_k in the first operand
-        // slot of both, so the second FFMA2 of each pair can take g_k from the
-        // operand reuse cache: an FFMA2 reading three distinct register pairs
-        // issues at 2/3 of the FMA-pipe rate (tools/microbench/fp32_pipes.cu)
-        const F2 q0 = fma2(gz, dz, ld2(b.la));
-        const F2 t0 = mul2(gz, y.z);
-        const F2 q1 = fma2(gy, dy, q0);
-        const F2 t1 = fma2(gy, y.y, t0);
-        const F2 q = fma2(gx, dx, q1);
-        const F2 t = fma2(gx, y.x, t1);
-        const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
-        const F2 et = mul2(t, e);
-#else
         const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, ld2(b.la))));
         const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
         const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
         const F2 et = mul2(e, t);
+#if RR_X2_BODY == 3
+        // T-trick: accumulate T = sum e K.c (a constant operand: FFMA2 with
+        // two register pairs, full rate) instead of G = sum e g (three
+        // register pairs, 2/3 rate, tools/microbench/fp32_pipes.cu); G = p.S - T
+        // after the loop.  C3 9.45 -> 9.36 ms, full-frame endpoint max
+        // 3.04e-5 -> 2.76e-5 (profiles/r2j_body_ab.log)
+        const F2 gxx = ld2(b.kcx), gyy = ld2(b.kcy), gzz = ld2(b.kcz);
+#else
+        const F2 gxx = gx, gyy = gy, gzz = gz;
 #endif
         if (neg) {
-            Gx = fnma2(e, gx, Gx);
-            Gy = fnma2(e, gy, Gy);
-            Gz = fnma2(e, gz, Gz);
-            Q1 = fnma2(RR_X2_BODY == 2 ? t : et, RR_X2_BODY == 2 ? et : t, Q1);
+            Gx = fnma2(e, gxx, Gx);
+            Gy = fnma2(e, gyy, Gy);
+            Gz = fnma2(e, gzz, Gz);
+            Q1 = fnma2(et, t, Q1);
             Sx = fnma2(e, ld2(b.kx), Sx);
             Sy = fnma2(e, ld2(b.ky), Sy);
             Sz = fnma2(e, ld2(b.kz), Sz);
         } else {
-            Gx = fma2(e, gx, Gx);
-            Gy = fma2(e, gy, Gy);
-            Gz = fma2(e, gz, Gz);
-            Q1 = fma2(RR_X2_BODY == 2 ? t : et, RR_X2_BODY == 2 ? et : t, Q1);
+            Gx = fma2(e, gxx, Gx);
+            Gy = fma2(e, gyy, Gy);
+            Gz = fma2(e, gzz, Gz);
+            Q1 = fma2(et, t, Q1);
             Sx = fma2(e, ld2(b.kx), Sx);
             Sy = fma2(e, ld2(b.ky), Sy);
             Sz = fma2(e, ld2(b.kz), Sz);
@@ -326,6 +321,11 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
         m &= m - 1u;
         body(P.bumpsb[j], true);
     }
+#if RR_X2_BODY == 3
+    Gx = sub2(mul2(p.x, Sx), Gx);
+    Gy = sub2(mul2(p.y, Sy), Gy);
+    Gz = sub2(mul2(p.z, Sz), Gz);
+#endif
     const F2 ys = fma2(mul2(y.x, y.x), Sx, fma2(mul2(y.y, y.y), Sy, mul2(mul2(y.z, y.z), Sz)));
     const F2 Q = fma2(bc2(kBeta * kBeta), Q1, mul2(bc2(-kBeta), ys));
     const F2 w = fma2(bc2(kBeta * kBeta), fma2(Gx, Gx, fma2(Gy, Gy, mul2(Gz, Gz))), bc2(1.f));
