@@ -217,9 +217,11 @@ def spill_report():
     (paper_2005_05386_b200/csrc/ptxas.log, written by the build)."""
     import re
     path = os.path.join(ROOT, "paper_2005_05386_b200", "csrc", "ptxas.log")
-    want = {"march2_kernel<16,shade>": "march2_kernelILi16ELi0EE",
-            "march2_kernel<16,fused_lit>": "march2_kernelILi16ELi3EE",
-            "march_kernel<diffeo,rk4,mesh>": "march_kernelILi3ELi0ELi1ELi0ELb1EE"}
+    want = {"march2_kernel<bumps16> (C3 frame)": "march2_kernelILi1ELi16ELi0ELb0EE",
+            "march2_kernel<bumps16> fused lit (C3 + lights)": "march2_kernelILi1ELi16ELi3ELb0EE",
+            "march2_kernel<bumps16,rk23>": "march2_kernelILi4ELi16ELi0ELb0EE",
+            "march2_kernel<twist> (C4)": "march2_kernelILi3ELi0ELi0ELb0EE",
+            "march_kernel<diffeo,mesh> (C4 + mesh)": "march_kernelILi3ELi0ELi1ELi0ELb1EE"}
     out = {}
     try:
         lines = open(path).read().split("\n")

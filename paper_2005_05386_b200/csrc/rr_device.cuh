@@ -193,6 +193,7 @@ struct DevLaunch {
     uint8_t* outcomes;            // 48-byte PixelOutcome records: RAYS (by ray), frames when
                                   // non-null (outcome sink, row-major pixel index)
     int vec16;                    // ray-pair epilogue may store 16x4 RGB blocks as 16-B words
+    int vec8;                     // one-ray epilogue may store 8x4 RGB micro-tiles as 8-B words
     unsigned long long out_pixels;    // pixels of the rgb / hit-record buffers (RR_CHECKS bounds)
     unsigned long long n_outcomes;    // records of the outcome sink (RR_CHECKS bounds)
     unsigned long long n_rays;

@@ -747,6 +747,10 @@ int setup_frame_launch(rr_ctx* c, const rr_camera* cam, int width, int height, i
         L.vec16 = even_mpr && aligned && ((size_t)3 * width) % 16 == 0;
     else
         L.vec16 = even_mpr && aligned && (3 * tile_w) % 16 == 0 && (3 * tile_w * tile_h) % 16 == 0;
+    // 8x4 micro-tiles of the one-ray kernel as 8-B words (24-B rows; tile
+    // widths are multiples of 8 pixels)
+    const bool aligned8 = (reinterpret_cast<uintptr_t>(rgb) & 7u) == 0;
+    L.vec8 = aligned8 && (mode != rr::kModeFrame || ((size_t)3 * width) % 8 == 0);
     return RR_OK;
 }
 

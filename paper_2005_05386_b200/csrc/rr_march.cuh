@@ -2179,11 +2179,43 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
     }
 }
 
+// RGB8 of a one-ray unit's 8x4 micro-tile: when every lane writes its pixel
+// and the rows are 8-B aligned (L.vec8), the 4 x 24-byte block is assembled
+// in shared memory and stored as 12 8-byte words (sector-friendly over
+// PCIe/NVLink for UVA / peer frames), else byte-wise.
+__device__ __forceinline__ void store_unit_rgb(const DevLaunch& L, int lane, unsigned long long pix,
+                                               uint32_t rgb, bool writer, uint32_t* smem24) {
+    if (L.vec8 && __all_sync(kFull, writer)) {
+        uint8_t* sb = reinterpret_cast<uint8_t*>(smem24);
+        const int off = (lane >> 3) * 24 + (lane & 7) * 3;
+        sb[off] = (uint8_t)(rgb & 0xff);
+        sb[off + 1] = (uint8_t)((rgb >> 8) & 0xff);
+        sb[off + 2] = (uint8_t)((rgb >> 16) & 0xff);
+        __syncwarp();
+        const unsigned long long rowpix = __shfl_sync(kFull, pix, (lane / 3 & 3) * 8);
+        if (lane < 12) {
+            RR_CHECK(rowpix + kMicroW <= L.out_pixels && ((3 * rowpix) & 7) == 0, "rgb micro-tile row");
+            *reinterpret_cast<uint2*>(L.rgb + 3 * rowpix + 8 * (lane % 3)) =
+                reinterpret_cast<const uint2*>(smem24)[lane];
+        }
+        __syncwarp();
+        return;
+    }
+    if (writer) {
+        RR_CHECK(pix < L.out_pixels, "rgb pixel index (one-ray)");
+        uint8_t* dst = L.rgb + 3 * pix;
+        dst[0] = (uint8_t)(rgb & 0xff);
+        dst[1] = (uint8_t)((rgb >> 8) & 0xff);
+        dst[2] = (uint8_t)((rgb >> 16) & 0xff);
+    }
+}
+
 template <int KIND, int NB, int SCHEME, int PASS, bool MESH>
 __global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23
                                          : (MESH ? RR_MIN_BLOCKS_MESH : RR_MIN_BLOCKS))
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
+    __shared__ uint32_t s_rgb[kThreads / 32][24];   // 8x4 RGB8 micro-tile per warp
     for (;;) {
         unsigned unit = 0;
         if (lane == 0) unit = atomicAdd(L.counter, 1u);
@@ -2271,11 +2303,18 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             }
             // sum over the lanes of a pixel (same lane % ppu), in light order
             for (int o = ppu; o < kUnit; o <<= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
-            if (live && li == 0) {
-                RayResult r{hr.status, 0, 0, hr.t, q, n};
-                shade(P, r, L.rgb + 3 * pix, P.ambient + contrib);
-            }
+            uint32_t rgbw = 0u;
+            if (live && li == 0) rgbw = shade_rgb(P, hr.status, hr.t, q, P.ambient + contrib);
             pad_writer = li == 0;     // one writer per pixel for the tile padding
+            if (L.lpp == 1) {
+                store_unit_rgb(L, lane, pix, rgbw, live || L.mode == kModeTiles, s_rgb[threadIdx.x >> 5]);
+                pad_writer = false;   // the padding went with the block
+            } else if (live && li == 0) {
+                uint8_t* dst = L.rgb + 3 * pix;
+                dst[0] = (uint8_t)(rgbw & 0xff);
+                dst[1] = (uint8_t)((rgbw >> 8) & 0xff);
+                dst[2] = (uint8_t)((rgbw >> 16) & 0xff);
+            }
         } else {
             const RayResult r = march_unit<KIND, NB, SCHEME, PASS, MESH>(P, live, pos, dir, cnt);
             ref_steps = live ? (unsigned)r.steps : 0u;
@@ -2301,13 +2340,12 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
                     hr.n[2] = r.normal.z;
                     hr.status = r.status;
                     L.hits[pix] = hr;
-                } else {
-                    RR_CHECK(pix < L.out_pixels, "rgb pixel index (one-ray)");
-                    shade(P, r, L.rgb + 3 * pix);
                 }
-            } else if (L.mode == kModeTiles && PASS == kPassShade) {
-                uint8_t* dst = L.rgb + 3 * pix;                    // zero partial-tile padding
-                dst[0] = dst[1] = dst[2] = 0;
+            }
+            if (L.mode != kModeRays && PASS == kPassShade) {
+                // the micro-tile's pixels (zero partial-tile padding in tile mode)
+                const uint32_t rgbw = live ? shade_rgb(P, r.status, r.t, r.point) : 0u;
+                store_unit_rgb(L, lane, pix, rgbw, live || L.mode == kModeTiles, s_rgb[threadIdx.x >> 5]);
             }
         }
         if (PASS == kPassShadow && !live && pad_writer && L.mode == kModeTiles) {
