@@ -15,7 +15,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -177,18 +179,26 @@ void flatten_scene(const Scene& s, std::vector<rr_primitive>& prims, rr_scene_de
 
 namespace {
 
-// One context per process (device 0 unless RRAY_CUDA_DEVICE is set); the
-// reference calls MarchFn from RRAY_THREADS workers, rr_* serialises inside.
+// One context per calling thread (device 0 unless RRAY_CUDA_DEVICE is set).
+// render() calls MarchFn from RRAY_THREADS workers at once (render.cpp:67-104):
+// each worker's rows run on its own context — its own stream, scene copy and
+// scratch — so the workers' row batches overlap on the GPU instead of queueing
+// on one context's mutex.  Contexts live until the process exits.
 rr_ctx* context() {
-    static std::once_flag once;
-    static rr_ctx* ctx = nullptr;
-    static int rc = 0;
-    std::call_once(once, [] {
+    struct Holder {
+        rr_ctx* ctx = nullptr;
+        int rc = -1;
+        ~Holder() {
+            if (ctx) rr_destroy(ctx);
+        }
+    };
+    static thread_local Holder h;
+    if (h.rc < 0) {
         const char* dev = std::getenv("RRAY_CUDA_DEVICE");
-        rc = rr_create(&ctx, dev ? std::atoi(dev) : 0);
-    });
-    if (rc) throw ValidationError(std::string("kernel 'cuda' is not available: ") + rr_last_error(nullptr));
-    return ctx;
+        h.rc = rr_create(&h.ctx, dev ? std::atoi(dev) : 0);
+    }
+    if (h.rc) throw ValidationError(std::string("kernel 'cuda' is not available: ") + rr_last_error(nullptr));
+    return h.ctx;
 }
 
 void check(int rc, rr_ctx* ctx) {
@@ -205,8 +215,6 @@ rr_integrator integ_of(const geodesics::IntegratorConfig& c) {
                          c.scheme == geodesics::Scheme::Euler ? RR_SCHEME_EULER : RR_SCHEME_RK4, 0.0};
 }
 
-std::mutex g_scene_mu;
-
 void upload(rr_ctx* ctx, const metrics::MetricField& m, const Scene& s) {
     FlatMetric fm;
     flatten_metric(m, fm);
@@ -221,10 +229,9 @@ void upload(rr_ctx* ctx, const metrics::MetricField& m, const Scene& s) {
 // MarchFn for KernelKind::Cuda (kernel.hpp:47).
 void march_rays_cuda(const MarchContext& mc, const RayStart* rays, PixelOutcome* out,
                      std::size_t n) {
-    rr_ctx* ctx = context();
+    rr_ctx* ctx = context();                      // this worker's context
     const rr_integrator integ = integ_of(mc.integ);
-    std::lock_guard<std::mutex> lk(g_scene_mu);   // scene + march as one unit
-    upload(ctx, *mc.metric, *mc.scene);
+    upload(ctx, *mc.metric, *mc.scene);           // no-op when unchanged (per-row calls)
     check(rr_march(ctx, &integ, reinterpret_cast<const rr_ray_start*>(rays),
                    reinterpret_cast<rr_pixel_outcome*>(out), n),
           ctx);
@@ -248,11 +255,8 @@ RenderResult render_cuda(const metrics::MetricField& m, const Scene& scene, cons
     RenderResult out;
     out.image = Image(width, height);
     rr_stats st{};
-    {
-        std::lock_guard<std::mutex> lk(g_scene_mu);
-        upload(ctx, m, scene);
-        check(rr_render(ctx, &c, &integ, width, height, out.image.data.data(), &st), ctx);
-    }
+    upload(ctx, m, scene);
+    check(rr_render(ctx, &c, &integ, width, height, out.image.data.data(), &st), ctx);
     out.stats.rays = static_cast<long long>(width) * height;
     out.stats.total_steps = st.total_steps;
     out.stats.pixel_errors = st.pixel_errors;
@@ -295,6 +299,76 @@ int shim_march_both(const char* json, int width, int height, void* ref_out, void
             cuda(ctx, rays.data() + static_cast<std::size_t>(py) * width,
                  static_cast<render::PixelOutcome*>(cuda_out) + static_cast<std::size_t>(py) * width,
                  static_cast<std::size_t>(width));
+        return 0;
+    } catch (const std::exception& e) {
+        g_shim_err = e.what();
+        return 1;
+    }
+}
+
+// The reference's frame loop (render.cpp:57-104: an atomic row counter,
+// `workers` threads, one MarchFn call per row, shade per pixel) with the CUDA
+// MarchFn: the drop-in path a maintainer gets from march_fn(KernelKind::Cuda)
+// alone, without routing whole frames.  Writes the image and returns the
+// wall time and total steps.
+int shim_render_rows_cuda(const char* json, int workers, std::uint8_t* rgb, double* seconds,
+                          long long* steps) {
+    using namespace rray;
+    try {
+        const config::RunConfig cfg = config::parse_config(json);
+        const int w = cfg.output.width, h = cfg.output.height;
+        const auto cam = render::build_camera(cfg.metric, cfg.camera.position, cfg.camera.look_dir,
+                                              cfg.camera.up_hint, cfg.camera.fov_deg * M_PI / 180.0);
+        render::MarchContext ctx;
+        ctx.metric = &cfg.metric;
+        ctx.scene = &cfg.scene;
+        ctx.integ = cfg.integrator;
+        const render::MarchFn march = render::detail::march_rays_cuda;
+        std::atomic<int> next{0};
+        std::atomic<long long> total{0};
+        std::atomic<int> failed{0};
+        std::string err;
+        std::mutex err_mu;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto work = [&] {
+            try {
+                std::vector<render::RayStart> rays(static_cast<std::size_t>(w));
+                std::vector<render::PixelOutcome> res(static_cast<std::size_t>(w));
+                long long st = 0;
+                for (;;) {
+                    const int py = next.fetch_add(1);
+                    if (py >= h) break;
+                    for (int px = 0; px < w; ++px)
+                        rays[px] = render::RayStart{cam.position, render::pixel_direction(cam, px, py, w, h)};
+                    march(ctx, rays.data(), res.data(), rays.size());
+                    for (int px = 0; px < w; ++px) {
+                        const auto& o = res[px];
+                        st += o.steps;
+                        render::Rgb8 c;
+                        if (o.status == render::RayStatus::Failed) c = {255, 0, 255};
+                        else if (o.status == render::RayStatus::Hit)
+                            c = render::shade(render::Hit{o.point, o.t, o.prim}, cfg.scene.fog_density);
+                        else c = render::shade(std::nullopt, cfg.scene.fog_density);
+                        std::uint8_t* p = rgb + 3 * (static_cast<std::size_t>(py) * w + px);
+                        p[0] = c.r; p[1] = c.g; p[2] = c.b;
+                    }
+                }
+                total += st;
+            } catch (const std::exception& e) {
+                std::lock_guard<std::mutex> lk(err_mu);
+                err = e.what();
+                failed = 1;
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int i = 0; i < (workers > 0 ? workers : 1); ++i) pool.emplace_back(work);
+        for (auto& t : pool) t.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *steps = total.load();
+        if (failed) {
+            g_shim_err = err;
+            return 1;
+        }
         return 0;
     } catch (const std::exception& e) {
         g_shim_err = e.what();

@@ -58,3 +58,36 @@ def test_render_shim_matches_reference_render(shim, name):
     assert np.array_equal(ref, z["rgb"])           # the reference itself, as dumped
     assert compare_rgb(cuda, ref, z["flags"]).ok
     assert abs(cs.value - rs.value) <= max(2, 0.01 * rs.value)
+
+
+def test_marchfn_row_pattern_threads(shim):
+    """render()'s frame loop (render.cpp:57-104) with the CUDA MarchFn from 1
+    and 16 worker threads, each on its own context: images byte-identical
+    across worker counts (acceptance.cpp:243-253) and within parity of the
+    FP64 oracle; the row-pattern wall time is logged (RR_PARITY_LOG)."""
+    import time
+    from oracle import Oracle
+    from oracle.parity import compare_rgb
+    from paper_2005_05386_b200.config import load_config
+    cfg = load_config(os.path.join(ROOT, "configs", "c3_bumps16_1080p.json"))
+    cfg.output.width, cfg.output.height = 320, 180
+    from paper_2005_05386_b200.config import reference_json
+    doc = reference_json(cfg).encode()
+    shim.shim_render_rows_cuda.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_longlong)]
+    imgs, times = {}, {}
+    for workers in (1, 16, 16):
+        img = np.zeros((180, 320, 3), np.uint8)
+        sec, steps = ctypes.c_double(), ctypes.c_longlong()
+        rc = shim.shim_render_rows_cuda(doc, workers, img.ctypes.data, ctypes.byref(sec), ctypes.byref(steps))
+        assert rc == 0, shim.shim_last_error()
+        imgs[workers], times[workers] = img, sec.value
+    assert np.array_equal(imgs[1], imgs[16])
+    ref_rgb, _, _, flags = Oracle().render(cfg, 320, 180, with_flags=True)
+    assert compare_rgb(imgs[16], ref_rgb, flags).ok
+    path = os.environ.get("RR_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": "MarchFn row pattern 320x180 (C3)", "seconds_1_worker": times[1],
+                                "seconds_16_workers": times[16]}) + "\n")
