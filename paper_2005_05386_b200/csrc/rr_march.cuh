@@ -53,6 +53,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // march from shared-memory staged chords (hit_normal out of the march loop)
 #define RR_X2_HITS_STAGED 1
 #endif
+#ifndef RR_COUNT_OWN_MASK
+#define RR_COUNT_OWN_MASK 0   // diagnostics build: count each ray's own culling mask, not the warp union
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -66,6 +69,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_RK4_UNROLL_LIT
 #define RR_X2_RK4_UNROLL_LIT RR_X2_RK4_UNROLL
+#endif
+#ifndef RR_X2_RK4_UNROLL_SHADOW
+#define RR_X2_RK4_UNROLL_SHADOW RR_X2_RK4_UNROLL_LIT
 #endif
 #ifndef RR_MIN_BLOCKS_X2
 // ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
@@ -2012,11 +2018,16 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                     }
                 }
                 lmo |= nj[r] ? 0u : lm;
+#if RR_COUNT_OWN_MASK
+                if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(lm);   // diagnostics: per-ray N_eff
+#endif
             }
             um = __reduce_or_sync(kFull, lmo);
+#if !RR_COUNT_OWN_MASK
 #pragma unroll
             for (int r = 0; r < 2; ++r)
                 if (act[r] && !nj[r]) cnt.bump_evals += 4u * __popc(um);
+#endif
         }
         P3 dp, vn;
         const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
@@ -2039,7 +2050,9 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             };
             // unlit frames: the four stages unrolled (four bump loops); the lit
             // launch carries two march copies, RR_X2_RK4_UNROLL_LIT picks its form
-            constexpr bool kUnrollStages = PASS == kPassShade ? RR_X2_RK4_UNROLL : RR_X2_RK4_UNROLL_LIT;
+            constexpr bool kUnrollStages = PASS == kPassShade ? RR_X2_RK4_UNROLL
+                                         : PASS == kPassShadow ? RR_X2_RK4_UNROLL_SHADOW
+                                                               : RR_X2_RK4_UNROLL_LIT;
             if constexpr (kUnrollStages) {
 #pragma unroll
                 for (int st = 0; st < 4; ++st) stage(st);
