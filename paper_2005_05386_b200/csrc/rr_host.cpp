@@ -117,6 +117,7 @@ struct rr_ctx {
     bool launched = false;
     cudaStream_t last_stream = nullptr;
     std::map<void*, void*> imports;          // imported frame address -> IPC mapping base
+    std::vector<std::pair<std::string, void*>> import_handles;   // open IPC handles -> base
 };
 
 namespace {
@@ -808,7 +809,7 @@ void rr_destroy(rr_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto& kv : c->imports) cudaIpcCloseMemHandle(kv.second);
+    for (auto& kv : c->import_handles) cudaIpcCloseMemHandle(kv.second);
     if (c->d_masks) cudaFree(c->d_masks);
     if (c->d_skip) cudaFree(c->d_skip);
     if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);
@@ -1291,10 +1292,19 @@ int rr_frame_import(rr_ctx* c, const rr_frame_handle* h, void** d_frame) {
     }
     cudaIpcMemHandle_t ih;
     std::memcpy(&ih, h->ipc, sizeof ih);
+    // a handle opens once per context: a repeated import of the same
+    // allocation reuses the mapping (keyed by the handle bytes)
+    for (const auto& kv : c->import_handles)
+        if (std::memcmp(kv.first.data(), h->ipc, sizeof h->ipc) == 0) {
+            *d_frame = static_cast<uint8_t*>(kv.second) + h->offset;
+            c->imports[*d_frame] = kv.second;
+            return RR_OK;
+        }
     void* base = nullptr;
     RR_CUDA(c, cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess));
     *d_frame = static_cast<uint8_t*>(base) + h->offset;
     c->imports[*d_frame] = base;
+    c->import_handles.emplace_back(std::string(reinterpret_cast<const char*>(h->ipc), sizeof h->ipc), base);
     return RR_OK;
 }
 
@@ -1307,6 +1317,13 @@ int rr_frame_close(rr_ctx* c, void* d_frame) {
     if (c->launched) RR_CUDA(c, cudaEventSynchronize(c->ev1));   // no shard still writing
     void* base = it->second;
     c->imports.erase(it);
+    for (const auto& kv : c->imports)
+        if (kv.second == base) return RR_OK;      // another import still maps it
+    for (size_t i = 0; i < c->import_handles.size(); ++i)
+        if (c->import_handles[i].second == base) {
+            c->import_handles.erase(c->import_handles.begin() + (long)i);
+            break;
+        }
     RR_CUDA(c, cudaIpcCloseMemHandle(base));
     return RR_OK;
 }

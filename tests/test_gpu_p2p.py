@@ -165,3 +165,16 @@ def test_frame_export_import_same_process():
     assert int(buf[1029].item()) == 42
     r.frame_close(p)
     r.close()
+
+
+def test_frame_export_rejects_host_memory():
+    """Exporting memory that is not device memory fails with a clean status
+    (no crash, no mapping)."""
+    import numpy as np
+    from paper_2005_05386_b200.errors import Error
+    from paper_2005_05386_b200.render import Renderer
+    r = Renderer(0)
+    host = np.zeros(4096, np.uint8)
+    with pytest.raises(Error):
+        r.frame_export(host.ctypes.data, host.nbytes)
+    r.close()
