@@ -49,8 +49,10 @@ constexpr float kBeta = -1.3862943611198906f;   // -2 ln 2
 constexpr float kHalfLog2e = 0.7213475204444817f;
 
 enum Kind : int { kEuclid = 0, kBumps = 1, kGraphGeneral = 2, kDiffeo = 3,
-                  kBumpsRk23 = 4 /* kernel-template tag only: Gaussian bumps with the adaptive
-                                    rk23 scheme on the ray-pair kernel (P.kind is kBumps) */ };
+                  kBumpsRk23 = 4,  /* kernel-template tag only: Gaussian bumps with the adaptive
+                                      rk23 scheme on the ray-pair kernel (P.kind is kBumps) */
+                  kDiffeoChain = 5 /* kernel-template tag only: general diffeo chains (RK4) on
+                                      the ray-pair kernel (P.kind is kDiffeo) */ };
 enum Stage : int { kStageAffine = 0, kStageTwist = 1, kStageBump = 2, kStageBend = 3 };
 enum Prim : int { kPrimGrid = 0, kPrimSphere = 1, kPrimHalfSpace = 2, kPrimMesh = 3 };
 enum Mode : int { kModeFrame = 0, kModeTiles = 1, kModeRays = 2 };
@@ -85,6 +87,8 @@ struct DevStage {         // one stage of a diffeo chain (identity stages droppe
     float v[12];          // AFFINE: m[9] row-major, off[3]
                           // BUMP:   cx,cy,cz, sx,sy,sz (=1/sigma), amp, dx,dy,dz
                           // BEND:   k, 1/k
+    float2 v2[12];        // v as broadcast pairs {v, v} (ray-pair fold: 64-bit constant operands)
+    float2 det2;
 };
 
 struct DevSphere {        // scene.cpp:56-71

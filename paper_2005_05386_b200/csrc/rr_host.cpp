@@ -313,6 +313,8 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
             }
             d.v[6] = (float)s.g.a;
         }
+        for (int k = 0; k < 12; ++k) d.v2[k] = make_float2(d.v[k], d.v[k]);
+        d.det2 = make_float2(d.det, d.det);
     }
     P.n_prims = sc->n_primitives;
     P.n_spheres = P.n_halves = P.n_grids = P.n_meshes = 0;

@@ -24,6 +24,8 @@ cudaError_t launch_family_pair_twist(const DevParams& P, const DevLaunch& L, cud
                                      const char** name);
 cudaError_t launch_family_pair_rk23(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
                                     const char** name);
+cudaError_t launch_family_pair_chain(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
+                                     const char** name);
 cudaError_t launch_family_bumps(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,
                                 const char** name);
 cudaError_t launch_family_diffeo(const DevParams& P, const DevLaunch& L, cudaStream_t s, int sms,

@@ -280,7 +280,10 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
                              (P.scheme == 1 || (RR_RK23_PAIRS && P.scheme == 2))) ||
                             (P.scheme == 1 &&
                              RR_TWIST_PAIRS && P.kind == kDiffeo && P.n_stages == 1 &&
-                             P.stages[0].kind == kStageTwist && (RR_TWIST_PAIRS_MESH || P.n_meshes == 0)));
+                             P.stages[0].kind == kStageTwist && (RR_TWIST_PAIRS_MESH || P.n_meshes == 0)) ||
+                            (P.scheme == 1 && RR_CHAIN_PAIRS && P.kind == kDiffeo &&
+                             !(P.n_stages == 1 && P.stages[0].kind == kStageTwist) &&
+                             (RR_CHAIN_PAIRS_MESH || P.n_meshes == 0)));
         *launches = lit && !fused ? 2 : 1;
     }
     switch (P.kind) {
@@ -304,6 +307,12 @@ cudaError_t launch_march(const DevParams& P, const DevLaunch& L, cudaStream_t st
             if (P.scheme == 1 && P.n_stages == 1 && P.stages[0].kind == kStageTwist &&
                 (RR_TWIST_PAIRS_MESH || P.n_meshes == 0))
                 return launch_family_pair_twist(P, L, stream, num_sms, kernel_name);
+#endif
+#if RR_RAY_PAIRS && RR_CHAIN_PAIRS
+            // general chains, RK4: ray pairs (packed jet fold)
+            if (P.scheme == 1 && !(P.n_stages == 1 && P.stages[0].kind == kStageTwist) &&
+                (RR_CHAIN_PAIRS_MESH || P.n_meshes == 0))
+                return launch_family_pair_chain(P, L, stream, num_sms, kernel_name);
 #endif
             return launch_family_diffeo(P, L, stream, num_sms, kernel_name);
     }

@@ -56,6 +56,13 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_COUNT_OWN_MASK
 #define RR_COUNT_OWN_MASK 0   // diagnostics build: count each ray's own culling mask, not the warp union
 #endif
+#ifndef RR_CHAIN_PAIRS
+// 1: general diffeo chains (RK4) on the ray-pair kernel (kDiffeoChain)
+#define RR_CHAIN_PAIRS 1
+#endif
+#ifndef RR_CHAIN_PAIRS_MESH
+#define RR_CHAIN_PAIRS_MESH 1
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -92,6 +99,13 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_MIN_BLOCKS_X2_TWIST_MESH
 #define RR_MIN_BLOCKS_X2_TWIST_MESH 6   // ray-pair single-twist frames with meshes (C4)
+#endif
+#ifndef RR_MIN_BLOCKS_X2_CHAIN
+// ray-pair general diffeo chains: the packed fold (J, q, w pairs) is register
+// heavy; 4 CTAs (128 registers) beat 5 and 6 (twist o bend: 45.1 / 45.9 /
+// 48.1 ms, one ray per thread 46.9; with the 100k mesh 46.8 / 47.4 / 49.1 vs
+// 49.0; profiles/r2p_chain_ab.log)
+#define RR_MIN_BLOCKS_X2_CHAIN 4
 #endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
 #define RR_MIN_BLOCKS_X2_RK23 5         // ray-pair rk23 (FSAL stage + error terms per ray pair)
@@ -542,6 +556,165 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
     const float id = -rcp_approx(d);
     return f3(id * (c00 * q0 + c01 * q1 + c02 * q2), id * (c10 * q0 + c11 * q1 + c12 * q2),
               id * (c20 * q0 + c21 * q1 + c22 * q2));
+}
+
+// accel_diffeo for a ray pair (general chains; ray-pair kernel kDiffeoChain):
+// the same directional-jet fold innermost-first with every per-ray operation
+// packed (stage constants as broadcast pairs, DevStage::v2), sin/cos per ray,
+// and the validity bound per ray.
+__device__ __forceinline__ F2 neg2(F2 a) { return mul2(a, bc2(-1.f)); }
+
+__device__ __forceinline__ P3 accel_diffeo_x2(const DevParams& P, const P3& p, const P3& y,
+                                              float (&valid)[2]) {
+    F2 x0 = p.x, x1 = p.y, x2 = p.z;           // current point
+    F2 w0 = y.x, w1 = y.y, w2 = y.z;           // J_inner y
+    F2 q0 = bc2(0.f), q1 = bc2(0.f), q2 = bc2(0.f);   // D^2 Phi_inner[y, y]
+    F2 J[9] = {bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f)};
+    float vmin[2] = {3.0e38f, 3.0e38f}, dprod[2] = {1.f, 1.f};
+    for (int s = 0; s < P.n_stages; ++s) {
+        const DevStage& st = P.stages[s];
+        F2 det;
+        if (st.kind == kStageAffine) {                       // diffeo.hpp:133-141
+            F2 m[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) m[k] = ld2(st.v2[k]);
+            const F2 n0 = add2(fma2(m[2], x2, fma2(m[1], x1, mul2(m[0], x0))), m[9]);
+            const F2 n1 = add2(fma2(m[5], x2, fma2(m[4], x1, mul2(m[3], x0))), m[10]);
+            const F2 n2 = add2(fma2(m[8], x2, fma2(m[7], x1, mul2(m[6], x0))), m[11]);
+            const F2 a0 = fma2(m[2], q2, fma2(m[1], q1, mul2(m[0], q0)));
+            const F2 a1 = fma2(m[5], q2, fma2(m[4], q1, mul2(m[3], q0)));
+            const F2 a2 = fma2(m[8], q2, fma2(m[7], q1, mul2(m[6], q0)));
+            q0 = a0; q1 = a1; q2 = a2;
+            const F2 b0 = fma2(m[2], w2, fma2(m[1], w1, mul2(m[0], w0)));
+            const F2 b1 = fma2(m[5], w2, fma2(m[4], w1, mul2(m[3], w0)));
+            const F2 b2 = fma2(m[8], w2, fma2(m[7], w1, mul2(m[6], w0)));
+            w0 = b0; w1 = b1; w2 = b2;
+            F2 R[9];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                R[c] = fma2(m[2], J[6 + c], fma2(m[1], J[3 + c], mul2(m[0], J[c])));
+                R[3 + c] = fma2(m[5], J[6 + c], fma2(m[4], J[3 + c], mul2(m[3], J[c])));
+                R[6 + c] = fma2(m[8], J[6 + c], fma2(m[7], J[3 + c], mul2(m[6], J[c])));
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) J[k] = R[k];
+            x0 = n0; x1 = n1; x2 = n2;
+            det = ld2(st.det2);
+        } else if (st.kind == kStageTwist) {                 // diffeo.hpp:143-173
+            float sa, ca, sb, cb;
+            __sincosf(lo2(x2), &sa, &ca);
+            __sincosf(hi2(x2), &sb, &cb);
+            const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
+            const F2 j02 = neg2(fma2(x1, cs, mul2(x0, sn)));            // d(image_0)/dz
+            const F2 j12 = fnma2(x1, sn, mul2(x0, cs));                 // d(image_1)/dz
+            const F2 two = bc2(2.f);
+            // w^T H[0] w and w^T H[1] w (H[2] = 0)
+            const F2 d0 = neg2(mul2(w2, fma2(two, fma2(w1, cs, mul2(w0, sn)), mul2(w2, j12))));
+            const F2 d1 = mul2(w2, fma2(two, fnma2(w1, sn, mul2(w0, cs)), mul2(w2, j02)));
+            const F2 a0 = fma2(j02, q2, fnma2(sn, q1, fma2(cs, q0, d0)));
+            const F2 a1 = fma2(j12, q2, fma2(cs, q1, fma2(sn, q0, d1)));
+            q0 = a0; q1 = a1;
+            const F2 b0 = fma2(j02, w2, fnma2(sn, w1, mul2(cs, w0)));
+            const F2 b1 = fma2(j12, w2, fma2(cs, w1, mul2(sn, w0)));
+            w0 = b0; w1 = b1;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const F2 r0 = fma2(j02, J[6 + c], fnma2(sn, J[3 + c], mul2(cs, J[c])));
+                const F2 r1 = fma2(j12, J[6 + c], fma2(cs, J[3 + c], mul2(sn, J[c])));
+                J[c] = r0;
+                J[3 + c] = r1;
+            }
+            x0 = j12;                                         // x c - y s
+            x1 = neg2(j02);                                   // x s + y c
+            det = fma2(sn, sn, mul2(cs, cs));
+        } else if (st.kind == kStageBend) {                   // EXTENSION (oracle/rro.c)
+            const F2 k = ld2(st.v2[0]), c = ld2(st.v2[1]);
+            const F2 kx = mul2(k, x0);
+            float sa, ca, sb, cb;
+            __sincosf(lo2(kx), &sa, &ca);
+            __sincosf(hi2(kx), &sb, &cb);
+            const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
+            const F2 yc = sub2(x1, c);
+            const F2 kcs = mul2(k, cs), ksn = mul2(k, sn);
+            const F2 j00 = neg2(mul2(kcs, yc)), j10 = neg2(mul2(ksn, yc));   // j01 = -sn, j11 = cs
+            const F2 wxx = mul2(w0, w0), wxy = mul2(bc2(2.f), mul2(w0, w1));
+            const F2 d0 = fnma2(wxy, kcs, mul2(wxx, mul2(mul2(k, ksn), yc)));
+            const F2 d1 = neg2(fma2(wxy, ksn, mul2(wxx, mul2(mul2(k, kcs), yc))));
+            const F2 a0 = fnma2(sn, q1, fma2(j00, q0, d0));
+            const F2 a1 = fma2(cs, q1, fma2(j10, q0, d1));
+            q0 = a0; q1 = a1;
+            const F2 b0 = fnma2(sn, w1, mul2(j00, w0));
+            const F2 b1 = fma2(cs, w1, mul2(j10, w0));
+            w0 = b0; w1 = b1;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const F2 r0 = fnma2(sn, J[3 + cc], mul2(j00, J[cc]));
+                const F2 r1 = fma2(cs, J[3 + cc], mul2(j10, J[cc]));
+                J[cc] = r0;
+                J[3 + cc] = r1;
+            }
+            x0 = neg2(mul2(sn, yc));
+            x1 = fma2(cs, yc, c);
+            det = neg2(mul2(k, yc));
+        } else {                                              // diffeo.hpp:175-193
+            const F2 cx = ld2(st.v2[0]), cy = ld2(st.v2[1]), cz = ld2(st.v2[2]);
+            const F2 sx = ld2(st.v2[3]), sy = ld2(st.v2[4]), sz = ld2(st.v2[5]);
+            const F2 amp = ld2(st.v2[6]), dx = ld2(st.v2[7]), dy = ld2(st.v2[8]), dz = ld2(st.v2[9]);
+            const F2 ux = mul2(sub2(x0, cx), sx), uy = mul2(sub2(x1, cy), sy), uz = mul2(sub2(x2, cz), sz);
+            const F2 uu = fma2(uz, uz, fma2(uy, uy, mul2(ux, ux)));
+            const F2 ee = mul2(bc2(-0.5f), uu);
+            const F2 e = mul2(amp, mk2(__expf(lo2(ee)), __expf(hi2(ee))));
+            const F2 gx = mul2(ux, sx), gy = mul2(uy, sy), gz = mul2(uz, sz);   // grad f = -e g
+            const F2 wg = fma2(w2, gz, fma2(w1, gy, mul2(w0, gx)));
+            const F2 ws = fma2(mul2(w2, w2), mul2(sz, sz),
+                               fma2(mul2(w1, w1), mul2(sy, sy), mul2(mul2(w0, w0), mul2(sx, sx))));
+            const F2 whw = mul2(e, fnma2(bc2(1.f), ws, mul2(wg, wg)));         // w^T Hess f w
+            const F2 fq = neg2(mul2(e, fma2(gz, q2, fma2(gy, q1, mul2(gx, q0)))));   // grad f . q
+            const F2 fw = neg2(mul2(e, wg));                                  // grad f . w
+            const F2 hq = add2(whw, fq);
+            q0 = fma2(dx, hq, q0);
+            q1 = fma2(dy, hq, q1);
+            q2 = fma2(dz, hq, q2);
+            w0 = fma2(dx, fw, w0);
+            w1 = fma2(dy, fw, w1);
+            w2 = fma2(dz, fw, w2);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const F2 r = neg2(mul2(e, fma2(gz, J[6 + c], fma2(gy, J[3 + c], mul2(gx, J[c])))));
+                J[c] = fma2(dx, r, J[c]);
+                J[3 + c] = fma2(dy, r, J[3 + c]);
+                J[6 + c] = fma2(dz, r, J[6 + c]);
+            }
+            x0 = fma2(e, dx, x0);
+            x1 = fma2(e, dy, x1);
+            x2 = fma2(e, dz, x2);
+            det = fnma2(e, fma2(dz, gz, fma2(dy, gy, mul2(dx, gx))), bc2(1.f));
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const float dt = get2(det, r);
+            vmin[r] = fminf(vmin[r], fabsf(dt));
+            dprod[r] *= dt;
+            vmin[r] = fminf(vmin[r], fabsf(dprod[r]));
+        }
+    }
+    // a = -J^-1 q via the adjugate (linalg.hpp:223-236)
+    const F2 c00 = fnma2(J[5], J[7], mul2(J[4], J[8]));
+    const F2 c01 = fnma2(J[1], J[8], mul2(J[2], J[7]));
+    const F2 c02 = fnma2(J[2], J[4], mul2(J[1], J[5]));
+    const F2 c10 = fnma2(J[3], J[8], mul2(J[5], J[6]));
+    const F2 c11 = fnma2(J[2], J[6], mul2(J[0], J[8]));
+    const F2 c12 = fnma2(J[0], J[5], mul2(J[2], J[3]));
+    const F2 c20 = fnma2(J[4], J[6], mul2(J[3], J[7]));
+    const F2 c21 = fnma2(J[0], J[7], mul2(J[1], J[6]));
+    const F2 c22 = fnma2(J[1], J[3], mul2(J[0], J[4]));
+    const F2 d = fma2(J[2], c20, fma2(J[1], c10, mul2(J[0], c00)));
+#pragma unroll
+    for (int r = 0; r < 2; ++r) valid[r] = fminf(valid[r], fminf(vmin[r], fabsf(get2(d, r))));
+    const F2 id = neg2(mk2(rcp_approx(lo2(d)), rcp_approx(hi2(d))));
+    return P3{mul2(id, fma2(c02, q2, fma2(c01, q1, mul2(c00, q0)))),
+              mul2(id, fma2(c12, q2, fma2(c11, q1, mul2(c10, q0)))),
+              mul2(id, fma2(c22, q2, fma2(c21, q1, mul2(c20, q0))))};
 }
 
 template <int KIND, int NB>
@@ -1967,8 +2140,8 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                                            F3 q0 = F3{0.f, 0.f, 0.f},
                                            F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f,
                                            bool sh = false) {
-    static_assert(KIND == kBumps || KIND == kDiffeo || KIND == kBumpsRk23,
-                  "ray pairs: Gaussian bumps (RK4 / rk23) or the single twist");
+    static_assert(KIND == kBumps || KIND == kDiffeo || KIND == kBumpsRk23 || KIND == kDiffeoChain,
+                  "ray pairs: Gaussian bumps (RK4 / rk23), the single twist or diffeo chains");
     if constexpr (KIND == kBumpsRk23) {
         march_pair_rk23<NB, PASS>(P, live0, live1, p, v, us, L, unit, status, steps, stg, q0, q1, d20, d21);
         return;
@@ -2030,12 +2203,28 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
 #endif
         }
         P3 dp, vn;
+        float vld[2] = {3.0e38f, 3.0e38f};                  // diffeo chains: min |det J| of the step
         const bool jw0 = nj[0] != 0 || !act[0], jw1 = nj[1] != 0 || !act[1];
         if (KIND == kBumps && __all_sync(kFull, jw0 && jw1)) {   // whole warp jumps: no integration
             dp = P3{bc2(0.f), bc2(0.f), bc2(0.f)};
             vn = v;
         } else if constexpr (KIND == kDiffeo) {
             twist_rk4_x2(p, v, half, full, sixth, dp, vn);
+        } else if constexpr (KIND == kDiffeoChain) {        // RK4 over the packed jet fold
+            P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
+            P3 ps = p, vs = v;
+#pragma unroll 1
+            for (int st = 0; st < 4; ++st) {   // rolled: one copy of the fold (instruction cache)
+                const P3 a = accel_diffeo_x2(P, ps, vs, vld);
+                const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
+                sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
+                sv = P3{fma2(wgt, a.x, sv.x), fma2(wgt, a.y, sv.y), fma2(wgt, a.z, sv.z)};
+                const F2 cc = st < 2 ? half : full;
+                ps = P3{fma2(cc, vs.x, p.x), fma2(cc, vs.y, p.y), fma2(cc, vs.z, p.z)};
+                vs = P3{fma2(cc, a.x, v.x), fma2(cc, a.y, v.y), fma2(cc, a.z, v.z)};
+            }
+            dp = P3{mul2(sixth, sx.x), mul2(sixth, sx.y), mul2(sixth, sx.z)};
+            vn = P3{fma2(sixth, sv.x, v.x), fma2(sixth, sv.y, v.y), fma2(sixth, sv.z, v.z)};
         } else {                                             // RK4 (integrate.hpp:63-93)
             P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
             P3 ps = p, vs = v;
@@ -2123,6 +2312,25 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             const int nsub = nj[r] ? nj[r] : 1;
             cnt.steps_integrated += 1;
             cnt.jumps += nj[r] ? 1u : 0u;
+            if constexpr (KIND == kDiffeoChain) {
+                if (!(vld[r] > 1e-14f)) {                   // kernel_impl.hpp:54-61: Failed
+                    act[r] = false;
+                    if (kShadow) {
+                        status[r] = 0;
+                        steps[r] = step[r];
+                    } else {
+                        if (kHits && !RR_X2_HITS_STAGED) {
+                            RayResult res{2, -1, step[r], 0.f, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f)};
+                            emit_primary<kPassHits>(P, L, unit, r, res);
+                        } else {
+                            stg->tp[r * kUnit + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            stg->sp[r * kUnit + lane] = make_int2(2, step[r]);
+                        }
+                        us.ref_steps += (unsigned)step[r];
+                    }
+                    continue;
+                }
+            }
             float s = sh[r];
             int prim = primr[r], hid = hidr[r];
             if constexpr (!MESH) {   // analytic primitives only: test and consume in one pass
@@ -2736,6 +2944,7 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
 //                 and waits on nothing.
 template <int KIND, int NB, int PASS, bool MESH>
 __global__ void __launch_bounds__(kThreads, KIND == kBumpsRk23 ? RR_MIN_BLOCKS_X2_RK23
+                                               : KIND == kDiffeoChain ? RR_MIN_BLOCKS_X2_CHAIN
                                                : KIND == kDiffeo ? (MESH ? RR_MIN_BLOCKS_X2_TWIST_MESH
                                                                      : RR_MIN_BLOCKS_X2_TWIST)
                                                : NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
