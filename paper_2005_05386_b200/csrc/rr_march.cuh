@@ -927,6 +927,11 @@ __device__ __forceinline__ float box_dist2(float4 n0, float4 n1, F3 p) {
 #ifndef RR_TWIST_RK4
 #define RR_TWIST_RK4 1     // z-free RK4 for a single-twist metric (march_fixed)
 #endif
+#ifndef RR_TWIST_XY_PAIRS
+// one-ray twist RK4 with the (x, y) components of the ray packed as FFMA2
+// pairs: C4 twist + 100k mesh 10.17 -> 9.35 ms (profiles/r2s_twist_xy_ab.log)
+#define RR_TWIST_XY_PAIRS 1
+#endif
 #ifndef RR_MESH_FREE_CAP
 #define RR_MESH_FREE_CAP 0.5f   // re-measured with rolled diffeo stages + 6 CTAs/SM (profiles/r1k_freecap_ab.log):
                                 // caps 0.25 / 0.5 / 1 / 2: C4 twist 13.0 / 12.8 / 13.3 / 14.2 ms, twist+bend 50.7 / 50.5 / 51.1 / 51.5 ms
@@ -1330,6 +1335,33 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
             // RK4 of the single twist (integrate.hpp:63-93 with accel_diffeo's
             // closed form): a_z = 0 and a does not depend on z, so z' stays
             // constant, the stage points need no z and dz = h z'.
+#if RR_TWIST_XY_PAIRS
+            // (x, y) components of one ray as packed pairs: a = vz (vz P +
+            // 2 (vy, -vx)) is two FFMA2-class ops on the swizzled velocity
+            const F2 P0 = mk2(p.x, p.y), V0 = mk2(v.x, v.y);
+            const F2 vz2 = bc2(v.z), two = bc2(2.f);
+            const F2 c_half = bc2(half), c_full = bc2(h);
+            F2 SX = bc2(0.f), SV = bc2(0.f), Pp = P0, Vp = V0;
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                const F2 swz = mk2(hi2(Vp), -lo2(Vp));                     // (vy, -vx)
+                const F2 A = mul2(vz2, fma2(vz2, Pp, mul2(two, swz)));
+                if (st == 0 || st == 3) {
+                    SX = add2(Vp, SX);
+                    SV = add2(A, SV);
+                } else {
+                    SX = fma2(two, Vp, SX);
+                    SV = fma2(two, A, SV);
+                }
+                const F2 cc = st < 2 ? c_half : c_full;
+                Pp = fma2(cc, Vp, P0);
+                Vp = fma2(cc, A, V0);
+            }
+            valid = 1.f;
+            const F2 DXY = mul2(bc2(sixth), SX), VXY = fma2(bc2(sixth), SV, V0);
+            dp = f3(lo2(DXY), hi2(DXY), h * v.z);
+            vn = f3(lo2(VXY), hi2(VXY), v.z);
+#else
             float sxx = 0.f, sxy = 0.f, svx = 0.f, svy = 0.f;
             float px = p.x, py = p.y, vx = v.x, vy = v.y;
             const float vz = v.z;
@@ -1346,6 +1378,7 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
             valid = 1.f;
             dp = f3(sixth * sxx, sixth * sxy, h * vz);
             vn = f3(fmaf(sixth, svx, v.x), fmaf(sixth, svy, v.y), vz);
+#endif
         } else {                                             // RK4 (integrate.hpp:63-93)
             F3 sx = f3(0.f, 0.f, 0.f), sv = f3(0.f, 0.f, 0.f);
             F3 ps = p, vs = v;
