@@ -63,6 +63,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_CHAIN_PAIRS_MESH
 #define RR_CHAIN_PAIRS_MESH 1
 #endif
+#ifndef RR_X2_KAHAN
+// compensated position sums in the ray-pair march.  Without them C3 runs 1.3%
+// faster but C1 (2000-step marches at h = 0.01) reaches 7.4e-5 endpoint error
+// against the 1e-4 contract (3.2e-5 with them): profiles/r2v_kahan_ab.log
+#define RR_X2_KAHAN 1
+#endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
 // (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
@@ -2293,9 +2299,14 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             vn = P3{sel2(j0, j1, v.x, vn.x), sel2(j0, j1, v.y, vn.y), sel2(j0, j1, v.z, vn.z)};
         }
         // compensated position update: pn = p + dp carrying the rounding error
+#if RR_X2_KAHAN
         const P3 yv{sub2(dp.x, c.x), sub2(dp.y, c.y), sub2(dp.z, c.z)};
         const P3 pn{add2(p.x, yv.x), add2(p.y, yv.y), add2(p.z, yv.z)};
         c = P3{sub2(sub2(pn.x, p.x), yv.x), sub2(sub2(pn.y, p.y), yv.y), sub2(sub2(pn.z, p.z), yv.z)};
+#else
+        (void)c;
+        const P3 pn{add2(p.x, dp.x), add2(p.y, dp.y), add2(p.z, dp.z)};
+#endif
         // chord tests (scene.cpp:99-109): analytic primitives per ray; with
         // meshes, the rays whose chord leaves their free ball are collected
         // and the warp runs the BVH tests over that compacted list (one
