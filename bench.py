@@ -517,6 +517,20 @@ def run_b200(args, cfg):
     achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
     traffic = load_traffic().get(r.last_kernel)
 
+    # ---- dispatch-order ablation (single GPU): the timed frames dispatch ray-
+    #      pair units expensive-first using the previous frame's per-unit costs
+    #      (rr_options.order_units, temporal coherence; outputs unaffected);
+    #      the same frame with the plain tile order, for comparison
+    unit_order = None
+    if world == 1:
+        r.set_options(order_units=0)
+        off_ms = statistics.mean(device_time(lambda: r.render_device(cam, integ, w, h, frame, stream=sp),
+                                             max(3, args.steps // 2), 1))
+        r.set_options(order_units=1)
+        r.set_config(cfg)
+        unit_order = {"timed_frames": "expensive-first (previous frame's unit costs)",
+                      "ms_per_frame_plain_order": off_ms}
+
     # ---- EXTENSION: the north-star frame — the same 1080p frame with shadow
     #      geodesics to 2 point lights (BASELINE configs[2] as specified), one
     #      fused launch, device-timed the same way, with its own roofline,
@@ -675,6 +689,7 @@ def run_b200(args, cfg):
             "spills": spill_report(),
             "e2e": e2e,
             "parity": parity,
+            "unit_order": unit_order,
             "shadows": shadows,
             "workloads": extras,
             "gpu_launches": args.steps * (1 if world == 1 or exchange == "p2p-epilogue" else 2),

@@ -235,6 +235,9 @@ typedef struct rr_options {
     int32_t block_x, block_y;         /* frame tile ordering the warp units (default 32 x 32) */
     int32_t persistent;               /* 1: persistent CTAs pulling warp units (default 1) */
     int32_t skip;                     /* 1: empty-space skipping of bump-free cells (default 1) */
+    int32_t order_units;              /* 1: ray-pair frames dispatch their units expensive-first,
+                                         ordered by the previous launch's per-unit cost with the
+                                         same unit layout (default 1; outputs are unaffected) */
 } rr_options;
 
 typedef struct rr_ctx rr_ctx;

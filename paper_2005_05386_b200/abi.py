@@ -120,7 +120,8 @@ class rr_stats(C.Structure):
 class rr_options(C.Structure):
     _fields_ = [("cull", C.c_int32), ("cull_grid", C.c_int32),
                 ("cull_radius_sigma", C.c_double), ("block_x", C.c_int32),
-                ("block_y", C.c_int32), ("persistent", C.c_int32), ("skip", C.c_int32)]
+                ("block_y", C.c_int32), ("persistent", C.c_int32), ("skip", C.c_int32),
+                ("order_units", C.c_int32)]
 
 
 class rr_frame_handle(C.Structure):
@@ -142,7 +143,7 @@ EXPECTED_SIZES = {
     "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
     "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 24,
     "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 112,
-    "rr_options": 32, "rr_frame_handle": 96,
+    "rr_options": 40, "rr_frame_handle": 96,
 }
 
 STRUCTS = {

@@ -198,6 +198,12 @@ struct DevLaunch {
                                   // non-null (outcome sink, row-major pixel index)
     int vec16;                    // ray-pair epilogue may store 16x4 RGB blocks as 16-B words
     int vec8;                     // one-ray epilogue may store 8x4 RGB micro-tiles as 8-B words
+    const unsigned* order;        // ray-pair kernels: dispatch order of the primary units
+                                  // (expensive first, from the previous frame's costs) or null
+    unsigned short* unit_cost;    // ray-pair kernels: warp-loop iterations per primary unit (or null)
+    const unsigned* order2;       // fused lit launch: dispatch order of the units' shadow items
+    unsigned* unit_cost2;         // fused lit launch: shadow iterations per unit (max over lights;
+                                  // zeroed per launch)
     unsigned long long out_pixels;    // pixels of the rgb / hit-record buffers (RR_CHECKS bounds)
     unsigned long long n_outcomes;    // records of the outcome sink (RR_CHECKS bounds)
     unsigned long long n_rays;

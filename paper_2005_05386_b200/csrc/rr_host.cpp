@@ -66,6 +66,7 @@ struct Options {
         o.block_y = 32;
         o.persistent = 1;
         o.skip = 1;
+        o.order_units = 1;
     }
 };
 
@@ -116,6 +117,22 @@ struct rr_ctx {
     // the previous launch (ev1, recorded after it).
     bool launched = false;
     cudaStream_t last_stream = nullptr;
+    // expensive-first dispatch of ray-pair units (rr_options.order_units):
+    // each launch records its units' warp-loop iteration counts; the next
+    // launch with the same unit layout dispatches them in descending order
+    unsigned short* d_cost = nullptr;
+    unsigned short* d_cost_keys = nullptr;
+    unsigned* d_iota = nullptr;
+    unsigned* d_order = nullptr;
+    unsigned* d_cost2 = nullptr;             // lit launches: shadow cost per unit, its sort keys
+    unsigned* d_cost2_keys = nullptr;        // and the shadow items' dispatch order
+    unsigned* d_order2 = nullptr;
+    bool have_cost2 = false;
+    void* d_sort_temp = nullptr;
+    size_t sort_temp_bytes = 0;
+    size_t order_cap = 0;
+    long long order_key[7] = {-1, -1, -1, -1, -1, -1, -1};
+    bool have_cost = false;
     std::map<void*, void*> imports;          // imported frame address -> IPC mapping base
     std::vector<std::pair<std::string, void*>> import_handles;   // open IPC handles -> base
 };
@@ -661,6 +678,56 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
         L.vis = reinterpret_cast<uint8_t*>(c->d_vis) + flag_bytes;
         RR_CUDA(c, cudaMemsetAsync(c->d_vis, 0, 2 * pairs * sizeof(unsigned), s));
     }
+    // expensive-first unit order for the ray-pair kernels (frames and tiles)
+    L.order = L.order2 = nullptr;
+    L.unit_cost = nullptr;
+    L.unit_cost2 = nullptr;
+    if (L.mode != rr::kModeRays && c->opt.o.order_units && rr::uses_pair_kernel(*c->P)) {
+        const size_t pairs = ((size_t)L.n_units + 1) / 2;
+        if (c->order_cap < pairs) {
+            for (void* p : {(void*)c->d_cost, (void*)c->d_cost_keys, (void*)c->d_iota, (void*)c->d_order,
+                            (void*)c->d_cost2, (void*)c->d_cost2_keys, (void*)c->d_order2, c->d_sort_temp})
+                if (p) cudaFree(p);
+            c->d_cost = c->d_cost_keys = nullptr;
+            c->d_iota = c->d_order = nullptr;
+            c->d_cost2 = c->d_cost2_keys = c->d_order2 = nullptr;
+            c->d_sort_temp = nullptr;
+            c->order_cap = 0;
+            c->have_cost = c->have_cost2 = false;
+            c->sort_temp_bytes = rr::unit_order_temp_bytes((int)pairs);
+            RR_CUDA(c, cudaMalloc(&c->d_cost, pairs * sizeof(unsigned short)));
+            RR_CUDA(c, cudaMalloc(&c->d_cost_keys, pairs * sizeof(unsigned short)));
+            RR_CUDA(c, cudaMalloc(&c->d_iota, pairs * sizeof(unsigned)));
+            RR_CUDA(c, cudaMalloc(&c->d_order, pairs * sizeof(unsigned)));
+            RR_CUDA(c, cudaMalloc(&c->d_cost2, pairs * sizeof(unsigned)));
+            RR_CUDA(c, cudaMalloc(&c->d_cost2_keys, pairs * sizeof(unsigned)));
+            RR_CUDA(c, cudaMalloc(&c->d_order2, pairs * sizeof(unsigned)));
+            RR_CUDA(c, cudaMalloc(&c->d_sort_temp, std::max<size_t>(c->sort_temp_bytes, 16)));
+            c->order_cap = pairs;
+        }
+        const long long key[7] = {L.mode, L.width, L.height, L.tile_w, L.tile_h, L.shard, L.n_shards};
+        const bool same = std::memcmp(key, c->order_key, sizeof key) == 0;
+        if (c->have_cost && same) {
+            RR_CUDA(c, rr::launch_unit_order(c->d_cost, c->d_cost_keys, c->d_iota, c->d_order, (int)pairs,
+                                             c->d_sort_temp, c->sort_temp_bytes, s));
+            L.order = c->d_order;
+        }
+        if (c->P->n_lights > 0) {                // fused lit launch: the shadow items too
+            if (c->have_cost2 && same) {
+                RR_CUDA(c, rr::launch_unit_order32(c->d_cost2, c->d_cost2_keys, c->d_iota, c->d_order2,
+                                                   (int)pairs, c->d_sort_temp, c->sort_temp_bytes, s));
+                L.order2 = c->d_order2;
+            }
+            RR_CUDA(c, cudaMemsetAsync(c->d_cost2, 0, pairs * sizeof(unsigned), s));
+            L.unit_cost2 = c->d_cost2;
+            c->have_cost2 = true;
+        } else {
+            c->have_cost2 = false;
+        }
+        std::memcpy(c->order_key, key, sizeof key);
+        L.unit_cost = c->d_cost;
+        c->have_cost = true;
+    }
     L.out_pixels = L.mode == rr::kModeFrame ? (unsigned long long)L.width * L.height
                                             : (unsigned long long)L.n_units * rr::kUnit;
     L.n_outcomes = L.mode == rr::kModeRays ? L.n_rays : (unsigned long long)L.width * L.height;
@@ -812,6 +879,9 @@ void rr_destroy(rr_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->import_handles) cudaIpcCloseMemHandle(kv.second);
+    for (void* p : {(void*)c->d_cost, (void*)c->d_cost_keys, (void*)c->d_iota, (void*)c->d_order,
+                    (void*)c->d_cost2, (void*)c->d_cost2_keys, (void*)c->d_order2, c->d_sort_temp})
+        if (p) cudaFree(p);
     if (c->d_masks) cudaFree(c->d_masks);
     if (c->d_skip) cudaFree(c->d_skip);
     if (c->d_cull_scratch) cudaFree(c->d_cull_scratch);

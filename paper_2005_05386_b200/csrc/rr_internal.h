@@ -56,6 +56,18 @@ cudaError_t launch_trace(const DevParams& P, const double* starts, int n, float 
 cudaError_t launch_accel_points(const DevParams& P, const double* pos, const double* vel, int n,
                                 double* acc, double* validity, cudaStream_t s);
 
+// True when launch_march runs a ray-pair (march2) kernel for P.
+bool uses_pair_kernel(const DevParams& P);
+
+// Expensive-first dispatch order of ray-pair units: order = unit ids sorted
+// by descending cost (device radix sort on 16-bit keys, on `s`).
+size_t unit_order_temp_bytes(int n);
+cudaError_t launch_unit_order(const unsigned short* cost, unsigned short* keys_out, unsigned* iota,
+                              unsigned* order, int n, void* temp, size_t temp_bytes, cudaStream_t s);
+
+cudaError_t launch_unit_order32(const unsigned* cost, unsigned* keys_out, unsigned* iota,
+                                unsigned* order, int n, void* temp, size_t temp_bytes, cudaStream_t s);
+
 // Mesh free-distance grid (G^3 bytes, units of q) over the box lo + [0, G cell).
 cudaError_t launch_mesh_dist(const float4* nodes, int G, const float lo[3], const float cell[3],
                              float q, uint8_t* out, cudaStream_t s);

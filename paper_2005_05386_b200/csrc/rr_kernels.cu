@@ -5,6 +5,8 @@
 // rr_k_diffeo.cu and rr_k_flat.cu (Euclidean + general graph fields).
 #include "rr_march.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace rr {
 namespace {
 
@@ -346,6 +348,54 @@ cudaError_t launch_mesh_dist(const float4* nodes, int G, const float lo[3], cons
     mesh_dist_kernel<<<(cells + 127) / 128, 128, 0, s>>>(nodes, G, lo[0], lo[1], lo[2], cell[0],
                                                          cell[1], cell[2], q, out);
     return cudaGetLastError();
+}
+
+bool uses_pair_kernel(const DevParams& P) {
+#if RR_RAY_PAIRS
+    if (P.kind == kBumps && P.n_meshes == 0) return P.scheme == 1 || (RR_RK23_PAIRS && P.scheme == 2);
+    if (P.kind == kDiffeo && P.scheme == 1) {
+        const bool twist1 = P.n_stages == 1 && P.stages[0].kind == kStageTwist;
+        if (twist1) return RR_TWIST_PAIRS && (RR_TWIST_PAIRS_MESH || P.n_meshes == 0);
+        return RR_CHAIN_PAIRS && (RR_CHAIN_PAIRS_MESH || P.n_meshes == 0);
+    }
+#endif
+    (void)P;
+    return false;
+}
+
+namespace {
+__global__ void iota_kernel(unsigned* v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (unsigned)i;
+}
+} // namespace
+
+size_t unit_order_temp_bytes(int n) {
+    size_t b16 = 0, b32 = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b16, (const unsigned short*)nullptr,
+                                              (unsigned short*)nullptr, (const unsigned*)nullptr,
+                                              (unsigned*)nullptr, n, 0, 16);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b32, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                              (const unsigned*)nullptr, (unsigned*)nullptr, n, 0, 16);
+    return b16 > b32 ? b16 : b32;
+}
+
+cudaError_t launch_unit_order(const unsigned short* cost, unsigned short* keys_out, unsigned* iota,
+                              unsigned* order, int n, void* temp, size_t temp_bytes, cudaStream_t s) {
+    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(iota, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, cost, keys_out, iota, order, n,
+                                                     0, 16, s);
+}
+
+cudaError_t launch_unit_order32(const unsigned* cost, unsigned* keys_out, unsigned* iota,
+                                unsigned* order, int n, void* temp, size_t temp_bytes, cudaStream_t s) {
+    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(iota, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, cost, keys_out, iota, order, n,
+                                                     0, 16, s);
 }
 
 cudaError_t launch_probe(uint8_t* p, uint8_t value, cudaStream_t s) {

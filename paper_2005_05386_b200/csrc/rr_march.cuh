@@ -3023,12 +3023,17 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
     if constexpr (PASS != kPassShadow) {
         constexpr int kPrim = PASS == kPassFused ? kPassHits : PASS;
         while (work < n_primary) {
+            // expensive units first (L.order: the previous frame's costs,
+            // sorted on the device); outputs do not depend on the order
+            const unsigned unit = L.order ? __ldg(L.order + work) : work;
             UnitStats us{};
-            pair_primary<KIND, NB, kPrim, MESH>(P, L, work, lane, us, stg);
+            pair_primary<KIND, NB, kPrim, MESH>(P, L, unit, lane, us, stg);
+            if (L.unit_cost && lane == 0)                       // warp-loop iterations of the unit
+                L.unit_cost[unit] = (unsigned short)min(us.cnt.lane_slots / 2u, 65535u);
             if constexpr (PASS == kPassFused) {                 // publish the hit records
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) atomicExch(L.ready + work, 1u);
+                if (lane == 0) atomicExch(L.ready + unit, 1u);
             }
             flush_unit_stats(L, us, lane, false);
             work = fetch();
@@ -3037,7 +3042,7 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
     if constexpr (kShadowWork) {
         while (work < n_work) {
             const unsigned w = work - n_primary;
-            const unsigned unit = w / (unsigned)nl;
+            const unsigned unit = L.order2 ? __ldg(L.order2 + w / (unsigned)nl) : w / (unsigned)nl;
             if constexpr (PASS == kPassFused) {
                 RR_CHECK(unit < n_pairs, "ready flag index");
                 // whole-warp polling of the unit's ready flag (dispensed
@@ -3052,6 +3057,8 @@ march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLa
             }
             UnitStats us{};
             pair_shadow<KIND, NB, MESH>(P, L, unit, (int)(w % (unsigned)nl), nl, lane, us, stg);
+            if (L.unit_cost2 && lane == 0)                      // max over the unit's lights
+                atomicMax(L.unit_cost2 + unit, min(us.cnt.lane_slots / 2u, 65535u));
             flush_unit_stats(L, us, lane, true);
             work = fetch();
         }

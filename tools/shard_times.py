@@ -14,13 +14,16 @@ def main():
     import torch
     from paper_2005_05386_b200.config import load_config
     from paper_2005_05386_b200.render import Renderer
-    path = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else \
-        os.path.join(ROOT, "configs", "c3_bumps16_1080p.json")
+    cfgs = [a for a in sys.argv[1:] if a.endswith(".json")]
+    path = cfgs[0] if cfgs else os.path.join(ROOT, "configs", "c3_bumps16_1080p.json")
     frames = int(sys.argv[sys.argv.index("--frames") + 1]) if "--frames" in sys.argv else 10
     cfg = load_config(path)
     cfg.scene.lights = []
     w, h, T = cfg.output.width, cfg.output.height, 32
     r = Renderer(0)
+    for o in [a for a in sys.argv if "=" in a]:     # rr_options, e.g. order_units=0
+        k, v = o.split("=", 1)
+        r.set_options(**{k: int(v)})
     r.set_config(cfg)
     cam = r.build_camera(cfg.camera)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
