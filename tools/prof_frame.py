@@ -57,7 +57,8 @@ def main():
         if a.time:
             ts.sort()
             print(f"{os.path.basename(path)} {w}x{h}: median {ts[len(ts)//2]:.3f} ms "
-                  f"min {ts[0]:.3f} kernel={r.last_kernel} steps={st['total_steps']}")
+                  f"min {ts[0]:.3f} kernel={r.last_kernel} steps={st['total_steps']} "
+                  f"integrated={st.get('integrated_steps')} bump_evals={st.get('bump_evals')}")
     r.close()
 
 
