@@ -20,6 +20,7 @@ def main():
     nlines = int(sys.argv[sys.argv.index("--lines") + 1]) if "--lines" in sys.argv else 30
     raw = rows(base + "_raw.csv")
     h = raw[0]
+    units = dict(zip(h, raw[1]))
     for r in raw[2:]:
         d = dict(zip(h, r))
         print(d["Kernel Name"][:80])
@@ -31,7 +32,7 @@ def main():
                        ("dram__bytes_read.sum", "DRAM read"), ("dram__bytes_write.sum", "DRAM write"),
                        ("launch__registers_per_thread", "regs")]:
             if k in d:
-                print(f"  {lab:14s} {d[k]}")
+                print(f"  {lab:14s} {d[k]} {units.get(k, '')}".rstrip())
         st = sorted(((k, float(v or 0)) for k, v in d.items()
                      if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")),
                     key=lambda kv: -kv[1])
