@@ -9,6 +9,7 @@ python tools/prof_frame.py configs/c3_bumps16_1080p.json [--frames 1] [--time]
 from __future__ import annotations
 
 import argparse
+import hashlib
 import os
 import sys
 
@@ -58,7 +59,8 @@ def main():
             ts.sort()
             print(f"{os.path.basename(path)} {w}x{h}: median {ts[len(ts)//2]:.3f} ms "
                   f"min {ts[0]:.3f} kernel={r.last_kernel} steps={st['total_steps']} "
-                  f"integrated={st.get('integrated_steps')} bump_evals={st.get('bump_evals')}")
+                  f"integrated={st.get('integrated_steps')} bump_evals={st.get('bump_evals')} "
+                  f"digest={hashlib.sha1(rgb.cpu().numpy().tobytes()).hexdigest()[:12]}")
     r.close()
 
 
