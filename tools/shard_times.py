@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Device time of one shard of an N-way tile split on one GPU (the per-GPU
 work of the multi-GPU run, exchange excluded): rr_render_tiles(shard, N),
-CUDA events, L2 flushed.  python tools/shard_times.py [config] [--frames K]"""
+CUDA events, L2 flushed.
+python tools/shard_times.py [config] [--frames K] [--tile T] [--all] [option=value ...]
+(--all times every shard; default the first and the last)"""
 import os
 import statistics
 import sys
@@ -19,7 +21,8 @@ def main():
     frames = int(sys.argv[sys.argv.index("--frames") + 1]) if "--frames" in sys.argv else 10
     cfg = load_config(path)
     cfg.scene.lights = []
-    w, h, T = cfg.output.width, cfg.output.height, 32
+    T = int(sys.argv[sys.argv.index("--tile") + 1]) if "--tile" in sys.argv else 32
+    w, h = cfg.output.width, cfg.output.height
     r = Renderer(0)
     for o in [a for a in sys.argv if "=" in a]:     # rr_options, e.g. order_units=0
         k, v = o.split("=", 1)
@@ -33,7 +36,7 @@ def main():
     base = None
     for n in (1, 2, 4, 8):
         worst = 0.0
-        for shard in sorted({0, n - 1}):
+        for shard in (range(n) if "--all" in sys.argv else sorted({0, n - 1})):
             k = r.shard_tile_count(w, h, T, T, shard, n)
             tiles = torch.zeros(k * T * T * 3, dtype=torch.uint8, device="cuda")
             ts = []
@@ -48,7 +51,7 @@ def main():
                     ts.append(a.elapsed_time(b))
             worst = max(worst, statistics.median(ts))
         base = base or worst
-        print(f"{os.path.basename(path)} N={n}: slowest shard {worst:.3f} ms  "
+        print(f"{os.path.basename(path)} T={T} N={n}: slowest shard {worst:.3f} ms  "
               f"ideal {base / n:.3f} ms  efficiency {base / n / worst:.3f}", flush=True)
 
 
