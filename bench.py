@@ -692,7 +692,10 @@ def run_b200(args, cfg):
             "unit_order": unit_order,
             "shadows": shadows,
             "workloads": extras,
-            "gpu_launches": args.steps * (1 if world == 1 or exchange == "p2p-epilogue" else 2),
+            # kernels per frame counted by the library (march + the graph-replayed
+            # dispatch-order sort), + rank 0's detile on the gather exchange
+            "gpu_launches": args.steps * (int(st["kernel_launches"]) +
+                                          (0 if world == 1 or exchange == "p2p-epilogue" else 1)),
             "simt_efficiency": simt(st),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

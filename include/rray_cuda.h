@@ -216,7 +216,7 @@ typedef struct rr_stats {
                                          through metric-free space counts once), all passes */
     int64_t bump_evals;               /* Gaussian-term evaluations executed (N_eff accounting) */
     int64_t shadow_steps;             /* steps spent on shadow geodesics (EXT) */
-    int64_t kernel_launches;          /* launches issued by the call */
+    int64_t kernel_launches;          /* kernels the call launched (march + the dispatch-order sort) */
     int64_t lane_slots;               /* primary: warp loop iterations x 32 (SIMT efficiency = integrated / slots) */
     int64_t shadow_lane_slots;        /* same for the shadow pass (EXT) */
     int64_t jump_steps;               /* primary integrated steps that were straight jumps through

@@ -134,6 +134,13 @@ struct rr_ctx {
     size_t order_cap = 0;
     long long order_key[7] = {-1, -1, -1, -1, -1, -1, -1};
     bool have_cost = false;
+    // the two cost sorts (primary units, shadow items) as CUDA graphs captured
+    // once per unit count: one graph launch per frame instead of the iota +
+    // CUB radix-sort launches, and an exact count of the kernels they run
+    cudaGraphExec_t sort_exec[2] = {nullptr, nullptr};
+    int sort_n[2] = {0, 0};
+    int sort_kernels[2] = {0, 0};
+    int last_sort_kernels = 0;               // sort kernels of the last launch (rr_stats)
     std::map<void*, void*> imports;          // imported frame address -> IPC mapping base
     std::vector<std::pair<std::string, void*>> import_handles;   // open IPC handles -> base
 };
@@ -657,6 +664,49 @@ int check_ready(rr_ctx* c, const rr_integrator* integ, cudaStream_t s) {
     return ensure_masks(c, integ->h, s, integ->scheme == RR_SCHEME_RK23 ? 3 : 1);
 }
 
+// Sorts the recorded unit costs into a dispatch order on `s`: which = 0
+// primary units (16-bit costs -> d_order), 1 shadow items (d_cost2 ->
+// d_order2).  The sort (iota + CUB radix sort) is captured on the context's
+// own stream into a graph once per unit count and buffer set, then replayed.
+int run_unit_sort(rr_ctx* c, int which, int n, cudaStream_t s) {
+    if (!c->sort_exec[which] || c->sort_n[which] != n) {
+        if (c->sort_exec[which]) cudaGraphExecDestroy(c->sort_exec[which]);
+        c->sort_exec[which] = nullptr;
+        RR_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const cudaError_t e =
+            which == 0 ? rr::launch_unit_order(c->d_cost, c->d_cost_keys, c->d_iota, c->d_order, n,
+                                               c->d_sort_temp, c->sort_temp_bytes, c->stream)
+                       : rr::launch_unit_order32(c->d_cost2, c->d_cost2_keys, c->d_iota, c->d_order2, n,
+                                                 c->d_sort_temp, c->sort_temp_bytes, c->stream);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+        if (e != cudaSuccess || e2 != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            return cuda_err(c, e != cudaSuccess ? e : e2, "unit order sort capture");
+        }
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+        int kernels = 0;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+        }
+        const cudaError_t e3 = cudaGraphInstantiate(&c->sort_exec[which], g, 0);
+        cudaGraphDestroy(g);
+        if (e3 != cudaSuccess) {
+            c->sort_exec[which] = nullptr;
+            return cuda_err(c, e3, "unit order sort instantiate");
+        }
+        c->sort_n[which] = n;
+        c->sort_kernels[which] = kernels;
+    }
+    RR_CUDA(c, cudaGraphLaunch(c->sort_exec[which], s));
+    c->last_sort_kernels += c->sort_kernels[which];
+    return RR_OK;
+}
+
 // Launch one march over `units` warp units; zeroes counters+stats first.
 int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
     if (c->P->n_lights > 0 && L.mode != rr::kModeRays) {
@@ -683,6 +733,7 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
     L.order = L.order2 = nullptr;
     L.unit_cost = nullptr;
     L.unit_cost2 = nullptr;
+    c->last_sort_kernels = 0;
     if (L.mode != rr::kModeRays && c->opt.o.order_units && rr::uses_pair_kernel(*c->P)) {
         const size_t pairs = ((size_t)L.n_units + 1) / 2;
         if (c->order_cap < pairs) {
@@ -694,6 +745,10 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
             c->d_cost2 = c->d_cost2_keys = c->d_order2 = nullptr;
             c->d_sort_temp = nullptr;
             c->order_cap = 0;
+            for (int k = 0; k < 2; ++k) {      // captured with the old buffers
+                if (c->sort_exec[k]) cudaGraphExecDestroy(c->sort_exec[k]);
+                c->sort_exec[k] = nullptr;
+            }
             c->have_cost = c->have_cost2 = false;
             c->sort_temp_bytes = rr::unit_order_temp_bytes((int)pairs);
             RR_CUDA(c, cudaMalloc(&c->d_cost, pairs * sizeof(unsigned short)));
@@ -709,14 +764,14 @@ int run_launch(rr_ctx* c, rr::DevLaunch& L, cudaStream_t s) {
         const long long key[7] = {L.mode, L.width, L.height, L.tile_w, L.tile_h, L.shard, L.n_shards};
         const bool same = std::memcmp(key, c->order_key, sizeof key) == 0;
         if (c->have_cost && same) {
-            RR_CUDA(c, rr::launch_unit_order(c->d_cost, c->d_cost_keys, c->d_iota, c->d_order, (int)pairs,
-                                             c->d_sort_temp, c->sort_temp_bytes, s));
+            const int rc = run_unit_sort(c, 0, (int)pairs, s);
+            if (rc) return rc;
             L.order = c->d_order;
         }
         if (c->P->n_lights > 0) {                // fused lit launch: the shadow items too
             if (c->have_cost2 && same) {
-                RR_CUDA(c, rr::launch_unit_order32(c->d_cost2, c->d_cost2_keys, c->d_iota, c->d_order2,
-                                                   (int)pairs, c->d_sort_temp, c->sort_temp_bytes, s));
+                const int rc = run_unit_sort(c, 1, (int)pairs, s);
+                if (rc) return rc;
                 L.order2 = c->d_order2;
             }
             RR_CUDA(c, cudaMemsetAsync(c->d_cost2, 0, pairs * sizeof(unsigned), s));
@@ -768,7 +823,7 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->jump_steps = (int64_t)c->h_stats[8];
         st->shadow_jump_steps = (int64_t)c->h_stats[9];
         st->shadow_integrated_steps = (int64_t)c->h_stats[10];
-        st->kernel_launches = c->last_launches;
+        st->kernel_launches = c->last_launches + c->last_sort_kernels;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
         st->wall_seconds = now - wall0_s;
@@ -880,6 +935,8 @@ void rr_destroy(rr_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->import_handles) cudaIpcCloseMemHandle(kv.second);
+    for (cudaGraphExec_t g : c->sort_exec)
+        if (g) cudaGraphExecDestroy(g);
     for (void* p : {(void*)c->d_cost, (void*)c->d_cost_keys, (void*)c->d_iota, (void*)c->d_order,
                     (void*)c->d_cost2, (void*)c->d_cost2_keys, (void*)c->d_order2, c->d_sort_temp})
         if (p) cudaFree(p);
