@@ -223,6 +223,8 @@ typedef struct rr_stats {
                                          metric-free space (no RK4 / metric evaluation) */
     int64_t shadow_jump_steps;        /* same for the shadow pass (EXT) */
     int64_t shadow_integrated_steps;  /* the shadow pass's share of integrated_steps (EXT) */
+    int64_t sort_kernels;             /* of kernel_launches: the dispatch-order sort's kernels
+                                         (rr_options.order_units); the rest are march launches */
 } rr_stats;
 
 /* ---- tuning knobs (extension; defaults are parity-safe) ------------------- */

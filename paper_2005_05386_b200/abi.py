@@ -111,7 +111,8 @@ class rr_stats(C.Structure):
                 ("bump_evals", C.c_int64), ("shadow_steps", C.c_int64),
                 ("kernel_launches", C.c_int64), ("lane_slots", C.c_int64),
                 ("shadow_lane_slots", C.c_int64), ("jump_steps", C.c_int64),
-                ("shadow_jump_steps", C.c_int64), ("shadow_integrated_steps", C.c_int64)]
+                ("shadow_jump_steps", C.c_int64), ("shadow_integrated_steps", C.c_int64),
+                ("sort_kernels", C.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -142,7 +143,7 @@ EXPECTED_SIZES = {
     "rr_vec3": 24, "rr_aabb": 48, "rr_gaussian": 56, "rr_poly_term": 24,
     "rr_field_node": 72, "rr_diffeo_node": 200, "rr_metric_desc": 56,
     "rr_primitive": 160, "rr_light": 32, "rr_scene_desc": 88, "rr_integrator": 24,
-    "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 112,
+    "rr_ray_start": 48, "rr_pixel_outcome": 48, "rr_camera": 200, "rr_stats": 120,
     "rr_options": 40, "rr_frame_handle": 96,
 }
 

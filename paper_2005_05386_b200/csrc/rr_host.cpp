@@ -824,6 +824,7 @@ int collect_stats(rr_ctx* c, cudaStream_t s, rr_stats* st, double wall0_s) {
         st->shadow_jump_steps = (int64_t)c->h_stats[9];
         st->shadow_integrated_steps = (int64_t)c->h_stats[10];
         st->kernel_launches = c->last_launches + c->last_sort_kernels;
+        st->sort_kernels = c->last_sort_kernels;
         const double now = std::chrono::duration<double>(
                                std::chrono::steady_clock::now().time_since_epoch()).count();
         st->wall_seconds = now - wall0_s;

@@ -18,7 +18,7 @@ import enum
 import os
 import threading
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, fields
 from typing import Optional
 
 import numpy as np
@@ -312,6 +312,15 @@ class RenderStats:                    # render.hpp:24-33 (+ device extensions)
     kernel_launches: int = 0
     lane_slots: int = 0
     shadow_lane_slots: int = 0
+    jump_steps: int = 0
+    shadow_jump_steps: int = 0
+    shadow_integrated_steps: int = 0
+    sort_kernels: int = 0
+
+    @classmethod
+    def from_dict(cls, st: dict) -> "RenderStats":
+        names = {f.name for f in fields(cls)}
+        return cls(**{k: v for k, v in st.items() if k in names})
 
     def avg_steps_per_ray(self) -> float:
         return self.total_steps / self.rays if self.rays > 0 else 0.0
@@ -398,7 +407,7 @@ def render(metric, scene: Scene, cam: Camera, integ: IntegratorConfig, width: in
         rgb, st = r.render(cam.raw, integ, width, height)
     st["wall_seconds"] = time.perf_counter() - t0
     st["rays"] = width * height
-    return RenderResult(Image(width, height, rgb), RenderStats(**st))
+    return RenderResult(Image(width, height, rgb), RenderStats.from_dict(st))
 
 
 @dataclass

@@ -60,3 +60,12 @@ def test_no_cpu_fallback_when_library_missing(tmp_path):
             render.load_library(str(tmp_path / "missing.so"))
     finally:
         render._lib = old
+
+
+def test_render_stats_mirror_covers_rr_stats():
+    """render.RenderStats (the reference's RenderStats + device extensions)
+    carries every rr_stats field, so render() can return the library's stats."""
+    from paper_2005_05386_b200.render import RenderStats
+    st = abi.rr_stats().as_dict()
+    assert set(st) <= set(RenderStats.__dataclass_fields__)
+    assert RenderStats.from_dict(dict(st, total_steps=10, rays=4)).avg_steps_per_ray() == 2.5

@@ -151,7 +151,7 @@ def test_c3_lit_1080p_full_frame_vs_oracle(renderer, oracle_lib):
     cfg = _load("c3_bumps16_shadows_1080p")
     w, h = 1920, 1080
     rgb, out, st, kern = _gpu_frame(renderer, cfg, w, h)
-    assert kern == "march2_kernel<bumps16>" and st["kernel_launches"] == 1
+    assert kern == "march2_kernel<bumps16>" and st["kernel_launches"] - st["sort_kernels"] == 1
     rep, cand, ref_st = _check_vs_oracle(oracle_lib, cfg, w, h, rgb, out)
     _log("c3_bumps16_shadows_1080p 1920x1080 full frame vs oracle", rep, cand, kern)
     assert rep.ok, f"{rep.summary()} candidates={cand}"

@@ -46,6 +46,8 @@ def test_order_never_changes_pixels_and_is_counted(cfg):
     # later frames replay the sort graph(s): lit frames sort the shadow items too
     sorts = [st['kernel_launches'] - 1 for _, st in ordered[1:]]
     assert sorts[0] >= 1 and sorts[0] == sorts[1]
+    assert all(st['sort_kernels'] == k for (_, st), k in zip(ordered[1:], sorts))
+    assert ordered[0][1]['sort_kernels'] == 0
     if "shadows" in cfg:
         unlit = _frames("c3_bumps16_1080p.json", 1, n=2)
         assert sorts[0] > unlit[1][1]['kernel_launches'] - 1
