@@ -48,6 +48,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 1: Gaussian-bump rk23 frames (mesh-free) on the ray-pair kernel
 #define RR_RK23_PAIRS 1
 #endif
+#ifndef RR_RK23_K1_PRELOOP
+// 1: the rk23 ray-pair march evaluates every ray's first k1 before its loop
+#define RR_RK23_K1_PRELOOP 1
+#endif
 #ifndef RR_X2_HITS_STAGED
 // 1: primary hit records of the lit launch are produced after the unit's
 // march from shared-memory staged chords (hit_normal out of the march loop)
@@ -1990,6 +1994,21 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
     bool have_k1[2] = {false, false};
     P3 k1v{bc2(0.f), bc2(0.f), bc2(0.f)};
     float sfree[2] = {0.f, 0.f};
+#if RR_RK23_K1_PRELOOP
+    // k1 = a(x0, y0) of every ray before the loop (FSAL afterwards), so the
+    // loop body carries three inlined bump blocks instead of four.  The first
+    // attempt never jumps (h = h0 < h_max), so this is the mask the loop's
+    // first attempt would use: level 0 at each live ray's cell.
+    if (__any_sync(kFull, act[0] || act[1])) {
+        uint32_t l0 = 0u;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (act[r]) l0 |= P.cull ? __ldg(P.cull_masks + cell_of(P, ray_of(p, r))) : P.all_mask;
+        const uint32_t um0 = __reduce_or_sync(kFull, l0);
+        k1v = accel_bumps_x2<NB>(P, um0, p, v);   // (not in bump_evals, as before)
+    }
+    have_k1[0] = have_k1[1] = true;
+#endif
     for (;;) {
         if (!__any_sync(kFull, act[0] || act[1])) break;
         cnt.lane_slots += 2;
@@ -2015,7 +2034,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
         }
         const uint32_t um = __reduce_or_sync(kFull, lmo);
         // first step of a ray: k1 = a(x, y) (FSAL afterwards)
-        if (!__all_sync(kFull, (have_k1[0] || !act[0]) && (have_k1[1] || !act[1]))) {
+        if (!RR_RK23_K1_PRELOOP && !__all_sync(kFull, (have_k1[0] || !act[0]) && (have_k1[1] || !act[1]))) {
             const P3 a = accel_bumps_x2<NB>(P, um, p, v);
             k1v = P3{sel2(have_k1[0], have_k1[1], k1v.x, a.x), sel2(have_k1[0], have_k1[1], k1v.y, a.y),
                      sel2(have_k1[0], have_k1[1], k1v.z, a.z)};
