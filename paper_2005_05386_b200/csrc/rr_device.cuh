@@ -76,6 +76,19 @@ struct alignas(8) DevBumpB {
     float2 kcx, kcy, kcz;  // K * centre
 };
 
+// One bump slot as scalars for the ray-pair march (RR_X2_SCALAR_CONSTS):
+// the packed FP32 ops take each constant as a broadcast uniform-register
+// operand (UR.F32, full rate on sm_100a: tools/microbench/fp32_pipes.cu), so
+// one 64-bit uniform load brings two constants: 5 LDCU.64 per bump instead of
+// DevBumpB's 10.
+struct alignas(8) DevBumpS {
+    float2 ncxy;           // -centre x, y
+    float2 nczkx;          // -centre z, K x
+    float2 kyz;            // K y, z
+    float2 lakcx;          // log2 |amplitude|, (K * centre) x
+    float2 kcyz;           // (K * centre) y, z
+};
+
 struct DevPoly {          // coef * x^a y^b z^c
     float coef;
     int a, b, c;
@@ -166,6 +179,7 @@ struct DevParams {
     float cell_min;               // smallest culling-cell edge (world units)
     DevBump bumps[kMaxBumps];
     DevBumpB bumpsb[32];              // slots 0..31 as broadcast pairs (ray-pair march)
+    DevBumpS bumpss[32];              // slots 0..31 as scalar pairs (ray-pair march, UR.F32 operands)
     DevPoly poly[kMaxPoly];
     DevStage stages[kMaxStages];
     DevSphere spheres[kMaxPrims];

@@ -301,6 +301,12 @@ void fill_params(const Compiled& c, const rr_scene_desc* sc, DevParams& P, std::
     for (int k = 0; k < 32; ++k) {                          // broadcast pairs (ray-pair march)
         const rr::DevBump& a = P.bumps[k];
         rr::DevBumpB& d = P.bumpsb[k];
+        rr::DevBumpS& e = P.bumpss[k];
+        e.ncxy = make_float2(-a.cx, -a.cy);
+        e.nczkx = make_float2(-a.cz, a.kx);
+        e.kyz = make_float2(a.ky, a.kz);
+        e.lakcx = make_float2(a.la, a.kx * a.cx);
+        e.kcyz = make_float2(a.ky * a.cy, a.kz * a.cz);
         d.ncx = make_float2(-a.cx, -a.cx);
         d.ncy = make_float2(-a.cy, -a.cy);
         d.ncz = make_float2(-a.cz, -a.cz);

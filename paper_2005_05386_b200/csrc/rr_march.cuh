@@ -52,6 +52,16 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 1: the rk23 ray-pair march evaluates every ray's first k1 before its loop
 #define RR_RK23_K1_PRELOOP 1
 #endif
+#ifndef RR_X2_SCALAR_CONSTS_LIT
+// bump constants as scalars (DevBumpS: UR.F32 broadcast operands, 5 instead of
+// 10 LDCU.64 per bump) in the lit launch's primary and shadow marches and in
+// rk23; the unlit RK4 frame keeps the broadcast pairs (DevBumpB), measured
+// 0.3% faster there (profiles/r2z_scalar_consts_ab.log)
+#define RR_X2_SCALAR_CONSTS_LIT 1
+#endif
+#ifndef RR_X2_SCALAR_CONSTS_RK23
+#define RR_X2_SCALAR_CONSTS_RK23 1
+#endif
 #ifndef RR_X2_HITS_STAGED
 // 1: primary hit records of the lit launch are produced after the unit's
 // march from shared-memory staged chords (hit_normal out of the march loop)
@@ -298,7 +308,7 @@ __device__ __forceinline__ P3 pair_of(F3 a, F3 b) { return P3{mk2(a.x, b.x), mk2
 // accumulating FFMA2s (negated operand).  Measured alternatives (unrolled
 // slot tests, pairs/groups of slots per test, the sign as an XOR, G = p.S - T,
 // compact or shared-memory slots): profiles/r1g_raypair.md, r1i_shadow_frame.md.
-template <int NB>
+template <int NB, bool SC = false>
 __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, const P3& p, const P3& y) {
     F2 Gx = bc2(0.f), Gy = bc2(0.f), Gz = bc2(0.f), Q1 = bc2(0.f);
     F2 Sx = bc2(0.f), Sy = bc2(0.f), Sz = bc2(0.f);
@@ -337,19 +347,52 @@ __device__ __forceinline__ P3 accel_bumps_x2(const DevParams& P, uint32_t um, co
             Sz = fma2(e, ld2(b.kz), Sz);
         }
     };
+    // SC: the same body over scalar constants: bc2(c) of a uniform scalar is a
+    // broadcast UR.F32 operand, and each 64-bit uniform load carries two
+    auto body_s = [&](const DevBumpS& b, bool neg) {
+        const float2 w0 = b.ncxy, w1 = b.nczkx, w2 = b.kyz, w3 = b.lakcx, w4 = b.kcyz;
+        const F2 dx = add2(p.x, bc2(w0.x)), dy = add2(p.y, bc2(w0.y)), dz = add2(p.z, bc2(w1.x));
+        const F2 kx = bc2(w1.y), ky = bc2(w2.x), kz = bc2(w2.y);
+        const F2 gx = mul2(dx, kx), gy = mul2(dy, ky), gz = mul2(dz, kz);
+        const F2 q = fma2(dx, gx, fma2(dy, gy, fma2(dz, gz, bc2(w3.x))));
+        const F2 e = mk2(ex2(lo2(q)), ex2(hi2(q)));
+        const F2 t = fma2(y.x, gx, fma2(y.y, gy, mul2(y.z, gz)));
+        const F2 et = mul2(e, t);
+        const F2 gxx = bc2(w3.y), gyy = bc2(w4.x), gzz = bc2(w4.y);   // T-trick (RR_X2_BODY 3)
+        if (neg) {
+            Gx = fnma2(e, gxx, Gx);
+            Gy = fnma2(e, gyy, Gy);
+            Gz = fnma2(e, gzz, Gz);
+            Q1 = fnma2(et, t, Q1);
+            Sx = fnma2(e, kx, Sx);
+            Sy = fnma2(e, ky, Sy);
+            Sz = fnma2(e, kz, Sz);
+        } else {
+            Gx = fma2(e, gxx, Gx);
+            Gy = fma2(e, gyy, Gy);
+            Gz = fma2(e, gzz, Gz);
+            Q1 = fma2(et, t, Q1);
+            Sx = fma2(e, kx, Sx);
+            Sy = fma2(e, ky, Sy);
+            Sz = fma2(e, kz, Sz);
+        }
+    };
+    static_assert(!SC || RR_X2_BODY == 3, "scalar constants: T-trick body only");
     uint32_t m = um & ~P.neg_mask;
 #pragma unroll 1
     while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1u;
-        body(P.bumpsb[j], false);
+        if constexpr (SC) body_s(P.bumpss[j], false);
+        else body(P.bumpsb[j], false);
     }
     m = um & P.neg_mask;
 #pragma unroll 1
     while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1u;
-        body(P.bumpsb[j], true);
+        if constexpr (SC) body_s(P.bumpss[j], true);
+        else body(P.bumpsb[j], true);
     }
 #if RR_X2_BODY == 3
     Gx = sub2(mul2(p.x, Sx), Gx);
@@ -2005,7 +2048,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
         for (int r = 0; r < 2; ++r)
             if (act[r]) l0 |= P.cull ? __ldg(P.cull_masks + cell_of(P, ray_of(p, r))) : P.all_mask;
         const uint32_t um0 = __reduce_or_sync(kFull, l0);
-        k1v = accel_bumps_x2<NB>(P, um0, p, v);   // (not in bump_evals, as before)
+        k1v = accel_bumps_x2<NB, RR_X2_SCALAR_CONSTS_RK23>(P, um0, p, v);   // (not in bump_evals, as before)
     }
     have_k1[0] = have_k1[1] = true;
 #endif
@@ -2035,7 +2078,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
         const uint32_t um = __reduce_or_sync(kFull, lmo);
         // first step of a ray: k1 = a(x, y) (FSAL afterwards)
         if (!RR_RK23_K1_PRELOOP && !__all_sync(kFull, (have_k1[0] || !act[0]) && (have_k1[1] || !act[1]))) {
-            const P3 a = accel_bumps_x2<NB>(P, um, p, v);
+            const P3 a = accel_bumps_x2<NB, RR_X2_SCALAR_CONSTS_RK23>(P, um, p, v);
             k1v = P3{sel2(have_k1[0], have_k1[1], k1v.x, a.x), sel2(have_k1[0], have_k1[1], k1v.y, a.y),
                      sel2(have_k1[0], have_k1[1], k1v.z, a.z)};
             have_k1[0] = have_k1[1] = true;
@@ -2053,11 +2096,11 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
             P3 ps{fma2(c05, v.x, p.x), fma2(c05, v.y, p.y), fma2(c05, v.z, p.z)};
             P3 vs{fma2(c05, k1v.x, v.x), fma2(c05, k1v.y, v.y), fma2(c05, k1v.z, v.z)};
             const P3 k2x = vs;
-            const P3 k2v = accel_bumps_x2<NB>(P, um, ps, vs);
+            const P3 k2v = accel_bumps_x2<NB, RR_X2_SCALAR_CONSTS_RK23>(P, um, ps, vs);
             ps = P3{fma2(c075, k2x.x, p.x), fma2(c075, k2x.y, p.y), fma2(c075, k2x.z, p.z)};
             vs = P3{fma2(c075, k2v.x, v.x), fma2(c075, k2v.y, v.y), fma2(c075, k2v.z, v.z)};
             const P3 k3x = vs;
-            const P3 k3v = accel_bumps_x2<NB>(P, um, ps, vs);
+            const P3 k3v = accel_bumps_x2<NB, RR_X2_SCALAR_CONSTS_RK23>(P, um, ps, vs);
             const F2 c1 = mul2(bc2(2.f / 9.f), H), c2 = mul2(bc2(1.f / 3.f), H), c3 = mul2(bc2(4.f / 9.f), H);
             xn = P3{fma2(c1, v.x, fma2(c2, k2x.x, fma2(c3, k3x.x, p.x))),
                     fma2(c1, v.y, fma2(c2, k2x.y, fma2(c3, k3x.y, p.y))),
@@ -2066,7 +2109,7 @@ __device__ __forceinline__ void march_pair_rk23(const DevParams& P, bool live0, 
                     fma2(c1, k1v.y, fma2(c2, k2v.y, fma2(c3, k3v.y, v.y))),
                     fma2(c1, k1v.z, fma2(c2, k2v.z, fma2(c3, k3v.z, v.z)))};
             const P3 k4x = vn;
-            k4v = accel_bumps_x2<NB>(P, um, xn, vn);
+            k4v = accel_bumps_x2<NB, RR_X2_SCALAR_CONSTS_RK23>(P, um, xn, vn);
             // embedded error, mixed abs/rel scale, per ray
             const F2 e1 = mul2(bc2(-5.f / 72.f), H), e2 = mul2(bc2(1.f / 12.f), H);
             const F2 e3 = mul2(bc2(1.f / 9.f), H), e4 = mul2(bc2(-1.f / 8.f), H);
@@ -2287,7 +2330,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             P3 sx{bc2(0.f), bc2(0.f), bc2(0.f)}, sv{bc2(0.f), bc2(0.f), bc2(0.f)};
             P3 ps = p, vs = v;
             auto stage = [&](int st) {
-                const P3 a = accel_bumps_x2<NB>(P, um, ps, vs);
+                const P3 a = accel_bumps_x2<NB, PASS != kPassShade && RR_X2_SCALAR_CONSTS_LIT>(P, um, ps, vs);
                 const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
                 sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
                 sv = P3{fma2(wgt, a.x, sv.x), fma2(wgt, a.y, sv.y), fma2(wgt, a.z, sv.z)};

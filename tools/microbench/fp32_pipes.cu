@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(256) pipe_kernel(const __grid_constant__ Args 
                 if (OP == 8) X[i] = fma2(X[i], X[i], Z[i]);          // FFMA2 R,R(same),R
                 if (OP == 9) X[i] = mul2(X[i], A.a2);                // FMUL2 R,c
                 if (OP == 10) X[i] = fma2(X[i], pk(y[i], y[i]), Z[i]); // FFMA2 R,R.F32(bcast),R
+                if (OP == 11) X[i] = fma2(X[i], pk(A.a, A.a), Z[i]);   // FFMA2 R,UR.F32(bcast),R
+                if (OP == 12) X[i] = fma2(X[i], (i & 1) ? pk(A.b, A.b) : pk(A.a, A.a), Z[i]);  // both halves of one UR pair
+                if (OP == 13) X[i] = add2(X[i], pk(A.a, A.a));         // FADD2 R,UR.F32(bcast)
             }
         }
     }
@@ -131,5 +134,8 @@ int main() {
     run<8>("FFMA2 R,R(same),R", 2);
     run<9>("FMUL2 R,c", 2);
     run<10>("FFMA2 R,Rbcast,R", 2);
+    run<11>("FFMA2 R,URbcast,R", 2);
+    run<12>("FFMA2 R,URbcast2,R", 2);
+    run<13>("FADD2 R,URbcast", 2);
     return 0;
 }
