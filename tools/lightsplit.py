@@ -11,8 +11,9 @@ w, h = cfg.output.width, cfg.output.height
 rgb = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 lights = list(cfg.scene.lights)
-for n in (0, 1, 2):
-    c = copy.deepcopy(cfg); c.scene.lights = lights[:n]
+for sel in ([], [0], [1], [0, 1]):
+    n = len(sel)
+    c = copy.deepcopy(cfg); c.scene.lights = [lights[k] for k in sel]
     r.set_config(c); cam = r.build_camera(c.camera)
     for _ in range(3): r.render_device(cam, c.integrator, w, h, rgb)
     ts = []
@@ -22,4 +23,6 @@ for n in (0, 1, 2):
         e0.record(); st = r.render_device(cam, c.integrator, w, h, rgb, with_stats=True); e1.record()
         torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(f"lights={n}: {ts[5]:.3f} ms kernel={r.last_kernel} shadow_steps={st['shadow_steps']} shadow_int={st['shadow_integrated_steps']} evals={st['bump_evals']}")
+    print(f"lights={sel}: {ts[5]:.3f} ms kernel={r.last_kernel} shadow_steps={st['shadow_steps']} shadow_int={st['shadow_integrated_steps']} evals={st['bump_evals']} "
+          f"shadow_simt={st['shadow_integrated_steps'] / max(1, st['shadow_lane_slots']):.3f} "
+          f"shadow_jumps={st['shadow_jump_steps']}")
