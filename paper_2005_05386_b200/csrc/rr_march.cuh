@@ -1274,12 +1274,11 @@ struct LaneCounters {
     unsigned jumps;            // integrated steps that were straight jumps (no RK4 / metric work)
 };
 
-// kPassDyn: march_pair serving kPassHits or kPassShadow work chosen per call
-// at run time.  (A fused lit launch looping over both work kinds through one
-// such copy was measured: ptxas then moves every bump loop to the vector
-// datapath — BREV/FLO/LDC instead of UBREV/UFLO/LDCU — so the fused launch
-// keeps two loops and two copies.)
-enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3, kPassDyn = 4 };
+// March passes.  (A fused lit launch looping over both work kinds through one
+// march copy with the pass chosen per work item was measured: ptxas then
+// moves every bump loop to the vector datapath — BREV/FLO/LDC instead of
+// UBREV/UFLO/LDCU — so the fused launch keeps two loops and two copies.)
+enum Pass : int { kPassShade = 0, kPassHits = 1, kPassShadow = 2, kPassFused = 3 };
 
 // ---------------------------------------------------------------------------
 // March one warp unit (kernel_impl.hpp:22-94): all 32 lanes step in lockstep
@@ -2239,17 +2238,15 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
                                            UnitStats& us, const DevLaunch& L, unsigned unit,
                                            int (&status)[2], int (&steps)[2], PairStage* stg,
                                            F3 q0 = F3{0.f, 0.f, 0.f},
-                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f,
-                                           bool sh = false) {
+                                           F3 q1 = F3{0.f, 0.f, 0.f}, float d20 = 0.f, float d21 = 0.f) {
     static_assert(KIND == kBumps || KIND == kDiffeo || KIND == kBumpsRk23 || KIND == kDiffeoChain,
                   "ray pairs: Gaussian bumps (RK4 / rk23), the single twist or diffeo chains");
     if constexpr (KIND == kBumpsRk23) {
         march_pair_rk23<NB, PASS>(P, live0, live1, p, v, us, L, unit, status, steps, stg, q0, q1, d20, d21);
         return;
     }
-    // pass of this call: compile-time, or (kPassDyn) per work item
-    const bool kShadow = PASS == kPassShadow || (PASS == kPassDyn && sh);
-    const bool kHits = PASS == kPassHits || (PASS == kPassDyn && !sh);
+    constexpr bool kShadow = PASS == kPassShadow;
+    constexpr bool kHits = PASS == kPassHits;
     LaneCounters& cnt = us.cnt;
     const int lane = threadIdx.x & 31;
     status[0] = status[1] = kShadow ? 1 : 0;
