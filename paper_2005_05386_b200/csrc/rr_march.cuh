@@ -62,6 +62,11 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_X2_SCALAR_CONSTS_RK23
 #define RR_X2_SCALAR_CONSTS_RK23 1
 #endif
+#ifndef RR_CHAIN_STATIC
+// 1: two-stage twist/bend chains use a fold specialised at compile time
+// (rr_k_pair_chain.cu); others (and 0) the run-time stage loop
+#define RR_CHAIN_STATIC 1
+#endif
 #ifndef RR_X2_HITS_STAGED
 // 1: primary hit records of the lit launch are produced after the unit's
 // march from shared-memory staged chords (hit_normal out of the march loop)
@@ -617,132 +622,159 @@ __device__ __forceinline__ F3 accel_diffeo(const DevParams& P, F3 p, F3 y, float
 // and the validity bound per ray.
 __device__ __forceinline__ F2 neg2(F2 a) { return mul2(a, bc2(-1.f)); }
 
-__device__ __forceinline__ P3 accel_diffeo_x2(const DevParams& P, const P3& p, const P3& y,
-                                              float (&valid)[2]) {
-    F2 x0 = p.x, x1 = p.y, x2 = p.z;           // current point
-    F2 w0 = y.x, w1 = y.y, w2 = y.z;           // J_inner y
-    F2 q0 = bc2(0.f), q1 = bc2(0.f), q2 = bc2(0.f);   // D^2 Phi_inner[y, y]
-    F2 J[9] = {bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f)};
-    float vmin[2] = {3.0e38f, 3.0e38f}, dprod[2] = {1.f, 1.f};
-    for (int s = 0; s < P.n_stages; ++s) {
-        const DevStage& st = P.stages[s];
-        F2 det;
-        if (st.kind == kStageAffine) {                       // diffeo.hpp:133-141
-            F2 m[12];
+// State of the fold for a ray pair: the current point x, J_inner y (w),
+// D^2 Phi_inner[y, y] (q) and the Jacobian J of the stages folded so far.
+struct ChainX2 {
+    F2 x0, x1, x2, w0, w1, w2, q0, q1, q2;
+    F2 J[9];
+};
+
+// One stage of each kind; each returns the stage's det J (validity).
+__device__ __forceinline__ F2 stage_affine_x2(const DevStage& st, ChainX2& c) {   // diffeo.hpp:133-141
+    F2 m[12];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) m[k] = ld2(st.v2[k]);
-            const F2 n0 = add2(fma2(m[2], x2, fma2(m[1], x1, mul2(m[0], x0))), m[9]);
-            const F2 n1 = add2(fma2(m[5], x2, fma2(m[4], x1, mul2(m[3], x0))), m[10]);
-            const F2 n2 = add2(fma2(m[8], x2, fma2(m[7], x1, mul2(m[6], x0))), m[11]);
-            const F2 a0 = fma2(m[2], q2, fma2(m[1], q1, mul2(m[0], q0)));
-            const F2 a1 = fma2(m[5], q2, fma2(m[4], q1, mul2(m[3], q0)));
-            const F2 a2 = fma2(m[8], q2, fma2(m[7], q1, mul2(m[6], q0)));
-            q0 = a0; q1 = a1; q2 = a2;
-            const F2 b0 = fma2(m[2], w2, fma2(m[1], w1, mul2(m[0], w0)));
-            const F2 b1 = fma2(m[5], w2, fma2(m[4], w1, mul2(m[3], w0)));
-            const F2 b2 = fma2(m[8], w2, fma2(m[7], w1, mul2(m[6], w0)));
-            w0 = b0; w1 = b1; w2 = b2;
-            F2 R[9];
+    for (int k = 0; k < 12; ++k) m[k] = ld2(st.v2[k]);
+    const F2 n0 = add2(fma2(m[2], c.x2, fma2(m[1], c.x1, mul2(m[0], c.x0))), m[9]);
+    const F2 n1 = add2(fma2(m[5], c.x2, fma2(m[4], c.x1, mul2(m[3], c.x0))), m[10]);
+    const F2 n2 = add2(fma2(m[8], c.x2, fma2(m[7], c.x1, mul2(m[6], c.x0))), m[11]);
+    const F2 a0 = fma2(m[2], c.q2, fma2(m[1], c.q1, mul2(m[0], c.q0)));
+    const F2 a1 = fma2(m[5], c.q2, fma2(m[4], c.q1, mul2(m[3], c.q0)));
+    const F2 a2 = fma2(m[8], c.q2, fma2(m[7], c.q1, mul2(m[6], c.q0)));
+    c.q0 = a0; c.q1 = a1; c.q2 = a2;
+    const F2 b0 = fma2(m[2], c.w2, fma2(m[1], c.w1, mul2(m[0], c.w0)));
+    const F2 b1 = fma2(m[5], c.w2, fma2(m[4], c.w1, mul2(m[3], c.w0)));
+    const F2 b2 = fma2(m[8], c.w2, fma2(m[7], c.w1, mul2(m[6], c.w0)));
+    c.w0 = b0; c.w1 = b1; c.w2 = b2;
+    F2 R[9];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                R[c] = fma2(m[2], J[6 + c], fma2(m[1], J[3 + c], mul2(m[0], J[c])));
-                R[3 + c] = fma2(m[5], J[6 + c], fma2(m[4], J[3 + c], mul2(m[3], J[c])));
-                R[6 + c] = fma2(m[8], J[6 + c], fma2(m[7], J[3 + c], mul2(m[6], J[c])));
-            }
+    for (int k = 0; k < 3; ++k) {
+        R[k] = fma2(m[2], c.J[6 + k], fma2(m[1], c.J[3 + k], mul2(m[0], c.J[k])));
+        R[3 + k] = fma2(m[5], c.J[6 + k], fma2(m[4], c.J[3 + k], mul2(m[3], c.J[k])));
+        R[6 + k] = fma2(m[8], c.J[6 + k], fma2(m[7], c.J[3 + k], mul2(m[6], c.J[k])));
+    }
 #pragma unroll
-            for (int k = 0; k < 9; ++k) J[k] = R[k];
-            x0 = n0; x1 = n1; x2 = n2;
-            det = ld2(st.det2);
-        } else if (st.kind == kStageTwist) {                 // diffeo.hpp:143-173
-            float sa, ca, sb, cb;
-            __sincosf(lo2(x2), &sa, &ca);
-            __sincosf(hi2(x2), &sb, &cb);
-            const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
-            const F2 j02 = neg2(fma2(x1, cs, mul2(x0, sn)));            // d(image_0)/dz
-            const F2 j12 = fnma2(x1, sn, mul2(x0, cs));                 // d(image_1)/dz
-            const F2 two = bc2(2.f);
-            // w^T H[0] w and w^T H[1] w (H[2] = 0)
-            const F2 d0 = neg2(mul2(w2, fma2(two, fma2(w1, cs, mul2(w0, sn)), mul2(w2, j12))));
-            const F2 d1 = mul2(w2, fma2(two, fnma2(w1, sn, mul2(w0, cs)), mul2(w2, j02)));
-            const F2 a0 = fma2(j02, q2, fnma2(sn, q1, fma2(cs, q0, d0)));
-            const F2 a1 = fma2(j12, q2, fma2(cs, q1, fma2(sn, q0, d1)));
-            q0 = a0; q1 = a1;
-            const F2 b0 = fma2(j02, w2, fnma2(sn, w1, mul2(cs, w0)));
-            const F2 b1 = fma2(j12, w2, fma2(cs, w1, mul2(sn, w0)));
-            w0 = b0; w1 = b1;
+    for (int k = 0; k < 9; ++k) c.J[k] = R[k];
+    c.x0 = n0; c.x1 = n1; c.x2 = n2;
+    return ld2(st.det2);
+}
+
+__device__ __forceinline__ F2 stage_twist_x2(ChainX2& c) {                        // diffeo.hpp:143-173
+    float sa, ca, sb, cb;
+    __sincosf(lo2(c.x2), &sa, &ca);
+    __sincosf(hi2(c.x2), &sb, &cb);
+    const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
+    const F2 j02 = neg2(fma2(c.x1, cs, mul2(c.x0, sn)));            // d(image_0)/dz
+    const F2 j12 = fnma2(c.x1, sn, mul2(c.x0, cs));                 // d(image_1)/dz
+    const F2 two = bc2(2.f);
+    // w^T H[0] w and w^T H[1] w (H[2] = 0)
+    const F2 d0 = neg2(mul2(c.w2, fma2(two, fma2(c.w1, cs, mul2(c.w0, sn)), mul2(c.w2, j12))));
+    const F2 d1 = mul2(c.w2, fma2(two, fnma2(c.w1, sn, mul2(c.w0, cs)), mul2(c.w2, j02)));
+    const F2 a0 = fma2(j02, c.q2, fnma2(sn, c.q1, fma2(cs, c.q0, d0)));
+    const F2 a1 = fma2(j12, c.q2, fma2(cs, c.q1, fma2(sn, c.q0, d1)));
+    c.q0 = a0; c.q1 = a1;
+    const F2 b0 = fma2(j02, c.w2, fnma2(sn, c.w1, mul2(cs, c.w0)));
+    const F2 b1 = fma2(j12, c.w2, fma2(cs, c.w1, mul2(sn, c.w0)));
+    c.w0 = b0; c.w1 = b1;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const F2 r0 = fma2(j02, J[6 + c], fnma2(sn, J[3 + c], mul2(cs, J[c])));
-                const F2 r1 = fma2(j12, J[6 + c], fma2(cs, J[3 + c], mul2(sn, J[c])));
-                J[c] = r0;
-                J[3 + c] = r1;
-            }
-            x0 = j12;                                         // x c - y s
-            x1 = neg2(j02);                                   // x s + y c
-            det = fma2(sn, sn, mul2(cs, cs));
-        } else if (st.kind == kStageBend) {                   // EXTENSION (oracle/rro.c)
-            const F2 k = ld2(st.v2[0]), c = ld2(st.v2[1]);
-            const F2 kx = mul2(k, x0);
-            float sa, ca, sb, cb;
-            __sincosf(lo2(kx), &sa, &ca);
-            __sincosf(hi2(kx), &sb, &cb);
-            const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
-            const F2 yc = sub2(x1, c);
-            const F2 kcs = mul2(k, cs), ksn = mul2(k, sn);
-            const F2 j00 = neg2(mul2(kcs, yc)), j10 = neg2(mul2(ksn, yc));   // j01 = -sn, j11 = cs
-            const F2 wxx = mul2(w0, w0), wxy = mul2(bc2(2.f), mul2(w0, w1));
-            const F2 d0 = fnma2(wxy, kcs, mul2(wxx, mul2(mul2(k, ksn), yc)));
-            const F2 d1 = neg2(fma2(wxy, ksn, mul2(wxx, mul2(mul2(k, kcs), yc))));
-            const F2 a0 = fnma2(sn, q1, fma2(j00, q0, d0));
-            const F2 a1 = fma2(cs, q1, fma2(j10, q0, d1));
-            q0 = a0; q1 = a1;
-            const F2 b0 = fnma2(sn, w1, mul2(j00, w0));
-            const F2 b1 = fma2(cs, w1, mul2(j10, w0));
-            w0 = b0; w1 = b1;
+    for (int k = 0; k < 3; ++k) {
+        const F2 r0 = fma2(j02, c.J[6 + k], fnma2(sn, c.J[3 + k], mul2(cs, c.J[k])));
+        const F2 r1 = fma2(j12, c.J[6 + k], fma2(cs, c.J[3 + k], mul2(sn, c.J[k])));
+        c.J[k] = r0;
+        c.J[3 + k] = r1;
+    }
+    c.x0 = j12;                                                     // x c - y s
+    c.x1 = neg2(j02);                                               // x s + y c
+    return fma2(sn, sn, mul2(cs, cs));
+}
+
+__device__ __forceinline__ F2 stage_bend_x2(const DevStage& st, ChainX2& c) {     // EXTENSION (oracle/rro.c)
+    const F2 k = ld2(st.v2[0]), cc = ld2(st.v2[1]);
+    const F2 kx = mul2(k, c.x0);
+    float sa, ca, sb, cb;
+    __sincosf(lo2(kx), &sa, &ca);
+    __sincosf(hi2(kx), &sb, &cb);
+    const F2 sn = mk2(sa, sb), cs = mk2(ca, cb);
+    const F2 yc = sub2(c.x1, cc);
+    const F2 kcs = mul2(k, cs), ksn = mul2(k, sn);
+    const F2 j00 = neg2(mul2(kcs, yc)), j10 = neg2(mul2(ksn, yc));   // j01 = -sn, j11 = cs
+    const F2 wxx = mul2(c.w0, c.w0), wxy = mul2(bc2(2.f), mul2(c.w0, c.w1));
+    const F2 d0 = fnma2(wxy, kcs, mul2(wxx, mul2(mul2(k, ksn), yc)));
+    const F2 d1 = neg2(fma2(wxy, ksn, mul2(wxx, mul2(mul2(k, kcs), yc))));
+    const F2 a0 = fnma2(sn, c.q1, fma2(j00, c.q0, d0));
+    const F2 a1 = fma2(cs, c.q1, fma2(j10, c.q0, d1));
+    c.q0 = a0; c.q1 = a1;
+    const F2 b0 = fnma2(sn, c.w1, mul2(j00, c.w0));
+    const F2 b1 = fma2(cs, c.w1, mul2(j10, c.w0));
+    c.w0 = b0; c.w1 = b1;
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                const F2 r0 = fnma2(sn, J[3 + cc], mul2(j00, J[cc]));
-                const F2 r1 = fma2(cs, J[3 + cc], mul2(j10, J[cc]));
-                J[cc] = r0;
-                J[3 + cc] = r1;
-            }
-            x0 = neg2(mul2(sn, yc));
-            x1 = fma2(cs, yc, c);
-            det = neg2(mul2(k, yc));
-        } else {                                              // diffeo.hpp:175-193
-            const F2 cx = ld2(st.v2[0]), cy = ld2(st.v2[1]), cz = ld2(st.v2[2]);
-            const F2 sx = ld2(st.v2[3]), sy = ld2(st.v2[4]), sz = ld2(st.v2[5]);
-            const F2 amp = ld2(st.v2[6]), dx = ld2(st.v2[7]), dy = ld2(st.v2[8]), dz = ld2(st.v2[9]);
-            const F2 ux = mul2(sub2(x0, cx), sx), uy = mul2(sub2(x1, cy), sy), uz = mul2(sub2(x2, cz), sz);
-            const F2 uu = fma2(uz, uz, fma2(uy, uy, mul2(ux, ux)));
-            const F2 ee = mul2(bc2(-0.5f), uu);
-            const F2 e = mul2(amp, mk2(__expf(lo2(ee)), __expf(hi2(ee))));
-            const F2 gx = mul2(ux, sx), gy = mul2(uy, sy), gz = mul2(uz, sz);   // grad f = -e g
-            const F2 wg = fma2(w2, gz, fma2(w1, gy, mul2(w0, gx)));
-            const F2 ws = fma2(mul2(w2, w2), mul2(sz, sz),
-                               fma2(mul2(w1, w1), mul2(sy, sy), mul2(mul2(w0, w0), mul2(sx, sx))));
-            const F2 whw = mul2(e, fnma2(bc2(1.f), ws, mul2(wg, wg)));         // w^T Hess f w
-            const F2 fq = neg2(mul2(e, fma2(gz, q2, fma2(gy, q1, mul2(gx, q0)))));   // grad f . q
-            const F2 fw = neg2(mul2(e, wg));                                  // grad f . w
-            const F2 hq = add2(whw, fq);
-            q0 = fma2(dx, hq, q0);
-            q1 = fma2(dy, hq, q1);
-            q2 = fma2(dz, hq, q2);
-            w0 = fma2(dx, fw, w0);
-            w1 = fma2(dy, fw, w1);
-            w2 = fma2(dz, fw, w2);
+    for (int m = 0; m < 3; ++m) {
+        const F2 r0 = fnma2(sn, c.J[3 + m], mul2(j00, c.J[m]));
+        const F2 r1 = fma2(cs, c.J[3 + m], mul2(j10, c.J[m]));
+        c.J[m] = r0;
+        c.J[3 + m] = r1;
+    }
+    c.x0 = neg2(mul2(sn, yc));
+    c.x1 = fma2(cs, yc, cc);
+    return neg2(mul2(k, yc));
+}
+
+__device__ __forceinline__ F2 stage_bump_x2(const DevStage& st, ChainX2& c) {     // diffeo.hpp:175-193
+    const F2 cx = ld2(st.v2[0]), cy = ld2(st.v2[1]), cz = ld2(st.v2[2]);
+    const F2 sx = ld2(st.v2[3]), sy = ld2(st.v2[4]), sz = ld2(st.v2[5]);
+    const F2 amp = ld2(st.v2[6]), dx = ld2(st.v2[7]), dy = ld2(st.v2[8]), dz = ld2(st.v2[9]);
+    const F2 ux = mul2(sub2(c.x0, cx), sx), uy = mul2(sub2(c.x1, cy), sy), uz = mul2(sub2(c.x2, cz), sz);
+    const F2 uu = fma2(uz, uz, fma2(uy, uy, mul2(ux, ux)));
+    const F2 ee = mul2(bc2(-0.5f), uu);
+    const F2 e = mul2(amp, mk2(__expf(lo2(ee)), __expf(hi2(ee))));
+    const F2 gx = mul2(ux, sx), gy = mul2(uy, sy), gz = mul2(uz, sz);   // grad f = -e g
+    const F2 wg = fma2(c.w2, gz, fma2(c.w1, gy, mul2(c.w0, gx)));
+    const F2 ws = fma2(mul2(c.w2, c.w2), mul2(sz, sz),
+                       fma2(mul2(c.w1, c.w1), mul2(sy, sy), mul2(mul2(c.w0, c.w0), mul2(sx, sx))));
+    const F2 whw = mul2(e, fnma2(bc2(1.f), ws, mul2(wg, wg)));         // w^T Hess f w
+    const F2 fq = neg2(mul2(e, fma2(gz, c.q2, fma2(gy, c.q1, mul2(gx, c.q0)))));   // grad f . q
+    const F2 fw = neg2(mul2(e, wg));                                  // grad f . w
+    const F2 hq = add2(whw, fq);
+    c.q0 = fma2(dx, hq, c.q0);
+    c.q1 = fma2(dy, hq, c.q1);
+    c.q2 = fma2(dz, hq, c.q2);
+    c.w0 = fma2(dx, fw, c.w0);
+    c.w1 = fma2(dy, fw, c.w1);
+    c.w2 = fma2(dz, fw, c.w2);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const F2 r = neg2(mul2(e, fma2(gz, J[6 + c], fma2(gy, J[3 + c], mul2(gx, J[c])))));
-                J[c] = fma2(dx, r, J[c]);
-                J[3 + c] = fma2(dy, r, J[3 + c]);
-                J[6 + c] = fma2(dz, r, J[6 + c]);
-            }
-            x0 = fma2(e, dx, x0);
-            x1 = fma2(e, dy, x1);
-            x2 = fma2(e, dz, x2);
-            det = fnma2(e, fma2(dz, gz, fma2(dy, gy, mul2(dx, gx))), bc2(1.f));
-        }
+    for (int k = 0; k < 3; ++k) {
+        const F2 r = neg2(mul2(e, fma2(gz, c.J[6 + k], fma2(gy, c.J[3 + k], mul2(gx, c.J[k])))));
+        c.J[k] = fma2(dx, r, c.J[k]);
+        c.J[3 + k] = fma2(dy, r, c.J[3 + k]);
+        c.J[6 + k] = fma2(dz, r, c.J[6 + k]);
+    }
+    c.x0 = fma2(e, dx, c.x0);
+    c.x1 = fma2(e, dy, c.x1);
+    c.x2 = fma2(e, dz, c.x2);
+    return fnma2(e, fma2(dz, gz, fma2(dy, gy, mul2(dx, gx))), bc2(1.f));
+}
+
+template <int KS>
+__device__ __forceinline__ F2 stage_x2(const DevStage& st, ChainX2& c) {
+    if constexpr (KS == kStageAffine) return stage_affine_x2(st, c);
+    else if constexpr (KS == kStageTwist) return stage_twist_x2(c);
+    else if constexpr (KS == kStageBend) return stage_bend_x2(st, c);
+    else return stage_bump_x2(st, c);
+}
+
+// Compile-time chain signatures (the kDiffeoChain kernel's NB template
+// argument): 0 = any chain, folded by a run-time loop over the stage kinds;
+// otherwise n | kind_0 << 4 | kind_1 << 8 | ... (innermost stage first), the
+// fold unrolled with every stage's kind known to the compiler (no kind
+// switch, no phi moves of the fold state at its joins).
+constexpr int chain_sig2(int k0, int k1) { return 2 | (k0 << 4) | (k1 << 8); }
+constexpr int sig_len(int sig) { return sig & 15; }
+constexpr int sig_kind(int sig, int i) { return (sig >> (4 + 4 * i)) & 15; }
+
+template <int SIG, int I>
+__device__ __forceinline__ void fold_static_x2(const DevParams& P, ChainX2& c, float (&vmin)[2],
+                                               float (&dprod)[2]) {
+    if constexpr (I < sig_len(SIG)) {
+        const F2 det = stage_x2<sig_kind(SIG, I)>(P.stages[I], c);
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const float dt = get2(det, r);
@@ -750,7 +782,37 @@ __device__ __forceinline__ P3 accel_diffeo_x2(const DevParams& P, const P3& p, c
             dprod[r] *= dt;
             vmin[r] = fminf(vmin[r], fabsf(dprod[r]));
         }
+        fold_static_x2<SIG, I + 1>(P, c, vmin, dprod);
     }
+}
+
+template <int SIG = 0>
+__device__ __forceinline__ P3 accel_diffeo_x2(const DevParams& P, const P3& p, const P3& y,
+                                              float (&valid)[2]) {
+    ChainX2 c{p.x, p.y, p.z, y.x, y.y, y.z, bc2(0.f), bc2(0.f), bc2(0.f),
+              {bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f)}};
+    float vmin[2] = {3.0e38f, 3.0e38f}, dprod[2] = {1.f, 1.f};
+    if constexpr (SIG != 0) {
+        fold_static_x2<SIG, 0>(P, c, vmin, dprod);
+    } else {
+        for (int s = 0; s < P.n_stages; ++s) {
+            const DevStage& st = P.stages[s];
+            F2 det;
+            if (st.kind == kStageAffine) det = stage_affine_x2(st, c);
+            else if (st.kind == kStageTwist) det = stage_twist_x2(c);
+            else if (st.kind == kStageBend) det = stage_bend_x2(st, c);
+            else det = stage_bump_x2(st, c);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const float dt = get2(det, r);
+                vmin[r] = fminf(vmin[r], fabsf(dt));
+                dprod[r] *= dt;
+                vmin[r] = fminf(vmin[r], fabsf(dprod[r]));
+            }
+        }
+    }
+    const F2 q0 = c.q0, q1 = c.q1, q2 = c.q2;
+    const F2 (&J)[9] = c.J;
     // a = -J^-1 q via the adjugate (linalg.hpp:223-236)
     const F2 c00 = fnma2(J[5], J[7], mul2(J[4], J[8]));
     const F2 c01 = fnma2(J[1], J[8], mul2(J[2], J[7]));
@@ -2313,7 +2375,7 @@ __device__ __forceinline__ void march_pair(const DevParams& P, bool live0, bool 
             P3 ps = p, vs = v;
 #pragma unroll 1
             for (int st = 0; st < 4; ++st) {   // rolled: one copy of the fold (instruction cache)
-                const P3 a = accel_diffeo_x2(P, ps, vs, vld);
+                const P3 a = accel_diffeo_x2<NB>(P, ps, vs, vld);
                 const F2 wgt = bc2((st == 0 || st == 3) ? 1.f : 2.f);
                 sx = P3{fma2(wgt, vs.x, sx.x), fma2(wgt, vs.y, sx.y), fma2(wgt, vs.z, sx.z)};
                 sv = P3{fma2(wgt, a.x, sv.x), fma2(wgt, a.y, sv.y), fma2(wgt, a.z, sv.z)};
