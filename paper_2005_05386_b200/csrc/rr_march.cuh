@@ -132,6 +132,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // 49.0; profiles/r2p_chain_ab.log)
 #define RR_MIN_BLOCKS_X2_CHAIN 4
 #endif
+#ifndef RR_MIN_BLOCKS_X2_CHAIN_STATIC
+// compile-time chain folds (112-116 registers at 4): 5 CTAs/SM, 96
+// registers (C4 twist + bend + mesh 34.0 / 32.7 / 35.7 ms at 4 / 5 / 6,
+// profiles/r2z_chain_occupancy_ab.log)
+#define RR_MIN_BLOCKS_X2_CHAIN_STATIC 5
+#endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
 #define RR_MIN_BLOCKS_X2_RK23 5         // ray-pair rk23 (FSAL stage + error terms per ray pair)
 #endif
@@ -3109,7 +3115,8 @@ __device__ __forceinline__ void pair_shadow(const DevParams& P, const DevLaunch&
 //                 and waits on nothing.
 template <int KIND, int NB, int PASS, bool MESH>
 __global__ void __launch_bounds__(kThreads, KIND == kBumpsRk23 ? RR_MIN_BLOCKS_X2_RK23
-                                               : KIND == kDiffeoChain ? RR_MIN_BLOCKS_X2_CHAIN
+                                               : KIND == kDiffeoChain ? (NB != 0 ? RR_MIN_BLOCKS_X2_CHAIN_STATIC
+                                                                                 : RR_MIN_BLOCKS_X2_CHAIN)
                                                : KIND == kDiffeo ? (MESH ? RR_MIN_BLOCKS_X2_TWIST_MESH
                                                                      : RR_MIN_BLOCKS_X2_TWIST)
                                                : NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
