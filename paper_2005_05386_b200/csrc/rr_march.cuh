@@ -62,6 +62,11 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #ifndef RR_X2_SCALAR_CONSTS_RK23
 #define RR_X2_SCALAR_CONSTS_RK23 1
 #endif
+#ifndef RR_TWIST_ONE_STATIC
+// 1: the one-ray kernel for single-twist scenes with meshes is a variant
+// without the general diffeo fold (rr_k_diffeo.cu)
+#define RR_TWIST_ONE_STATIC 1
+#endif
 #ifndef RR_CHAIN_STATIC
 // 1: two-stage twist/bend chains use a fold specialised at compile time
 // (rr_k_pair_chain.cu); others (and 0) the run-time stage loop
@@ -1374,7 +1379,9 @@ __device__ __forceinline__ RayResult march_fixed(const DevParams& P, bool live, 
     const float light_d = PASS == kPassShadow ? sqrtf(dist2) : 0.f;
     float mfree = 0.f;                        // mesh free distance budget (EXT meshes)
     float sfree = 0.f;                        // sphere / half-space free distance budget
-    const bool twist1 = KIND == kDiffeo && P.n_stages == 1 && P.stages[0].kind == kStageTwist;
+    // single twist: known at compile time in the NB == 1 diffeo variants (the
+    // general fold is then not compiled into the kernel), else checked here
+    const bool twist1 = KIND == kDiffeo && (NB == 1 || (P.n_stages == 1 && P.stages[0].kind == kStageTwist));
     for (;;) {
         if (!__any_sync(kFull, active)) break;
         cnt.lane_slots += 1;
