@@ -2615,6 +2615,10 @@ __global__ void __launch_bounds__(kThreads, SCHEME == 2 ? RR_MIN_BLOCKS_RK23
 march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     __shared__ uint32_t s_rgb[kThreads / 32][24];   // 8x4 RGB8 micro-tile per warp
+    __shared__ unsigned long long s_acc[kThreads / 32][8];   // the warp's stat sums (lane 0)
+    unsigned long long* acc = s_acc[threadIdx.x >> 5];
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) acc[k] = 0ull;
     for (;;) {
         unsigned unit = 0;
         if (lane == 0) unit = atomicAdd(L.counter, 1u);
@@ -2751,7 +2755,10 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
             uint8_t* dst = L.rgb + 3 * pix;
             dst[0] = dst[1] = dst[2] = 0;
         }
-        // per-unit counters: one REDUX per counter, one 64-bit atomic per warp
+        // per-unit counters: one REDUX per counter, summed per warp in shared
+        // memory and flushed with one 64-bit atomic per counter when the warp
+        // leaves the loop (per-unit atomics on the 11 shared stat words
+        // serialised in L2 for launches of cheap units)
         const unsigned steps = __reduce_add_sync(kFull, ref_steps);
         const unsigned nerr = __reduce_add_sync(kFull, errs);
         const unsigned integ = __reduce_add_sync(kFull, cnt.steps_integrated);
@@ -2761,16 +2768,26 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
         const unsigned slots = __reduce_add_sync(kFull, cnt.lane_slots);
         const unsigned jmp = __reduce_add_sync(kFull, cnt.jumps);
         if (lane == 0) {
-            if (jmp) atomicAdd(L.stats + (PASS == kPassShadow ? 9 : 8), (unsigned long long)jmp);
-            if (integ && PASS == kPassShadow) atomicAdd(L.stats + 10, (unsigned long long)integ);
-            if (steps) atomicAdd(L.stats + 0, (unsigned long long)steps);
-            if (nerr) atomicAdd(L.stats + 1, (unsigned long long)nerr);
-            if (integ) atomicAdd(L.stats + 2, (unsigned long long)integ);
-            if (evals) atomicAdd(L.stats + 3, (unsigned long long)evals);
-            if (nr) atomicAdd(L.stats + 4, (unsigned long long)nr);
-            if (shs) atomicAdd(L.stats + 5, (unsigned long long)shs);
-            if (slots) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), (unsigned long long)slots);
+            acc[0] += steps;
+            acc[1] += nerr;
+            acc[2] += integ;
+            acc[3] += evals;
+            acc[4] += nr;
+            acc[5] += shs;
+            acc[6] += slots;
+            acc[7] += jmp;
         }
+    }
+    if (lane == 0) {
+        if (acc[7]) atomicAdd(L.stats + (PASS == kPassShadow ? 9 : 8), acc[7]);
+        if (acc[2] && PASS == kPassShadow) atomicAdd(L.stats + 10, acc[2]);
+        if (acc[0]) atomicAdd(L.stats + 0, acc[0]);
+        if (acc[1]) atomicAdd(L.stats + 1, acc[1]);
+        if (acc[2]) atomicAdd(L.stats + 2, acc[2]);
+        if (acc[3]) atomicAdd(L.stats + 3, acc[3]);
+        if (acc[4]) atomicAdd(L.stats + 4, acc[4]);
+        if (acc[5]) atomicAdd(L.stats + 5, acc[5]);
+        if (acc[6]) atomicAdd(L.stats + (PASS == kPassShadow ? 7 : 6), acc[6]);
     }
     // Sharded frame mode may write into another GPU's frame (peer/IPC mapping):
     // make the stores visible system-wide before the kernel retires, ahead of
