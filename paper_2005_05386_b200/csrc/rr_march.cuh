@@ -67,6 +67,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // without the general diffeo fold (rr_k_diffeo.cu)
 #define RR_TWIST_ONE_STATIC 1
 #endif
+#ifndef RR_EUCLID_PREFETCH
+#define RR_EUCLID_PREFETCH 1   // one-ray Euclidean launches fetch their next unit index one unit ahead
+#endif
 #ifndef RR_CHAIN_STATIC
 // 1: two-stage twist/bend chains use a fold specialised at compile time
 // (rr_k_pair_chain.cu); others (and 0) the run-time stage loop
@@ -2619,11 +2622,22 @@ march_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLau
     unsigned long long* acc = s_acc[threadIdx.x >> 5];
     if (lane == 0)
         for (int k = 0; k < 8; ++k) acc[k] = 0ull;
+    // Euclidean units are cheap (straight jumps): the unit fetch's returning
+    // atomic is issued one unit ahead, so its latency overlaps the current unit
+    constexpr bool kPrefetch = KIND == kEuclid && RR_EUCLID_PREFETCH;
+    unsigned next = 0;
+    if (kPrefetch && lane == 0) next = atomicAdd(L.counter, 1u);
     for (;;) {
         unsigned unit = 0;
-        if (lane == 0) unit = atomicAdd(L.counter, 1u);
-        unit = __shfl_sync(kFull, unit, 0);
-        if (unit >= L.n_units) break;
+        if constexpr (kPrefetch) {
+            unit = __shfl_sync(kFull, next, 0);
+            if (unit >= L.n_units) break;
+            if (lane == 0) next = atomicAdd(L.counter, 1u);
+        } else {
+            if (lane == 0) unit = atomicAdd(L.counter, 1u);
+            unit = __shfl_sync(kFull, unit, 0);
+            if (unit >= L.n_units) break;
+        }
 
         bool live;
         F3 pos, dir;
