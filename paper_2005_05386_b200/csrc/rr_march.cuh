@@ -153,7 +153,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_MIN_BLOCKS_X2_CHAIN_STATIC 5
 #endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
-#define RR_MIN_BLOCKS_X2_RK23 5         // ray-pair rk23 (FSAL stage + error terms per ray pair)
+// ray-pair rk23 (FSAL stage + error terms per ray pair): 6 CTAs/SM (80
+// registers) since the pre-loop k1 and scalar constants shrank it: 10.43 vs
+// 10.48 ms at 5, 12.97 at 4 (profiles/r2z_occ_recheck_ab.log)
+#define RR_MIN_BLOCKS_X2_RK23 6
 #endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
