@@ -218,10 +218,12 @@ def spill_report():
     import re
     path = os.path.join(ROOT, "paper_2005_05386_b200", "csrc", "ptxas.log")
     want = {"march2_kernel<bumps16> (C3 frame)": "march2_kernelILi1ELi16ELi0ELb0EE",
-            "march2_kernel<bumps16> fused lit (C3 + lights)": "march2_kernelILi1ELi16ELi3ELb0EE",
+            "march2_kernel<bumps16> lit hit records (C3 + lights)": "march2_kernelILi1ELi16ELi1ELb0EE",
+            "march2_kernel<bumps16> lit shadows (C3 + lights)": "march2_kernelILi1ELi16ELi2ELb0EE",
             "march2_kernel<bumps16,rk23>": "march2_kernelILi4ELi16ELi0ELb0EE",
             "march2_kernel<twist> (C4)": "march2_kernelILi3ELi0ELi0ELb0EE",
-            "march_kernel<diffeo,mesh> (C4 + mesh)": "march_kernelILi3ELi0ELi1ELi0ELb1EE"}
+            "march_kernel<diffeo,mesh> (C4 + mesh, static twist)": "march_kernelILi3ELi1ELi1ELi0ELb1EE",
+            "march2_kernel<chain,mesh> (C4 bend + mesh, static fold)": "march2_kernelILi5ELi306ELi0ELb1EE"}
     out = {}
     try:
         lines = open(path).read().split("\n")
@@ -533,7 +535,7 @@ def run_b200(args, cfg):
 
     # ---- EXTENSION: the north-star frame — the same 1080p frame with shadow
     #      geodesics to 2 point lights (BASELINE configs[2] as specified), one
-    #      fused launch, device-timed the same way, with its own roofline,
+    #      hit-record launch + shadow launch, device-timed the same way, with its own roofline,
     #      e2e, CPU baseline (FP64 oracle extension) and parity
     shadows = None
     single = world == 1
@@ -557,7 +559,8 @@ def run_b200(args, cfg):
                    "roofline": {"bound": "fp32", "achieved": s_ach, "peak": peak, "unit": "TFLOP/s",
                                 "frac": s_ach / peak, "frac_nominal": s_ach / NOMINAL_FP32_TFLOPS,
                                 "traffic": load_traffic().get(r.last_kernel + "+lights"),
-                                "flop_per_launch": s_flop, "kernel": r.last_kernel + " (fused lit)"},
+                                "flop_per_launch": s_flop,
+                                "kernel": r.last_kernel + " (lit: hit-record + shadow launches)"},
                    "simt_efficiency": simt(sst),
                    "launches_per_frame": sst["kernel_launches"],
                    "e2e": e2e_frames(r, scfg, w, h, max(3, args.steps),

@@ -104,8 +104,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_FUSED
 // ray-pair frames with lights: 1 = one launch (primary units, then
-// (unit, light) shadow units); 0 = a hit-record launch + a shadow launch
-#define RR_X2_FUSED 1
+// (unit, light) shadow units, ready flags); 0 = a hit-record launch + a shadow
+// launch, each with its own register budget and half the code.  0 since the
+// final round-2 build: 15.32-15.34 ms (shadow launch at 7 CTAs/SM) vs 15.47-
+// 15.49 fused, bit-identical (profiles/r2z_unfused_ab.log); in round 1 the
+// fused launch had won
+#define RR_X2_FUSED 0
 #endif
 #ifndef RR_X2_RK4_UNROLL
 #define RR_X2_RK4_UNROLL 1   // 4 RK4 stages unrolled (4 small bump loops): C3 10.32 -> 9.91 ms, lights 16.94 -> 16.66
@@ -151,6 +155,12 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // registers (C4 twist + bend + mesh 34.0 / 32.7 / 35.7 ms at 4 / 5 / 6,
 // profiles/r2z_chain_occupancy_ab.log)
 #define RR_MIN_BLOCKS_X2_CHAIN_STATIC 5
+#endif
+#ifndef RR_MIN_BLOCKS_X2_SHADOW
+#define RR_MIN_BLOCKS_X2_SHADOW 7   // the shadow launch of lit frames (72 registers): 15.33 vs 15.37 ms at 6
+#endif
+#ifndef RR_MIN_BLOCKS_X2_HITS
+#define RR_MIN_BLOCKS_X2_HITS RR_MIN_BLOCKS_X2     // the hit-record launch of unfused lit frames
 #endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
 // ray-pair rk23 (FSAL stage + error terms per ray pair): 6 CTAs/SM (80
@@ -3202,7 +3212,9 @@ __global__ void __launch_bounds__(kThreads, KIND == kBumpsRk23 ? RR_MIN_BLOCKS_X
                                                                      : RR_MIN_BLOCKS_X2_TWIST)
                                                : NB <= 4 ? RR_MIN_BLOCKS_X2_SMALL
                                                : (PASS == kPassFused ? RR_MIN_BLOCKS_X2_FUSED
-                                                                     : RR_MIN_BLOCKS_X2))
+                                                  : PASS == kPassShadow ? RR_MIN_BLOCKS_X2_SHADOW
+                                                  : PASS == kPassHits ? RR_MIN_BLOCKS_X2_HITS
+                                                                      : RR_MIN_BLOCKS_X2))
 march2_kernel(const __grid_constant__ DevParams P, const __grid_constant__ DevLaunch L) {
     const int lane = threadIdx.x & 31;
     const unsigned n_pairs = (L.n_units + 1) / 2;

@@ -2,7 +2,7 @@
 benchmarked resolutions and settings.
 
 rr_render_outcomes runs the same frame launch rr_render does (the ray-pair
-march2_kernel for Gaussian-bump RK4 frames — unlit, or the fused lit launch —
+march2_kernel for Gaussian-bump RK4 frames — unlit, or the lit launches —
 and march_kernel for the diffeo/mesh frames) with a PixelOutcome sink, so
 hit primitive, endpoint, t and steps of every pixel of the benchmarked frame
 are compared with the reference (oracle/_ref, the reference compiled from its
@@ -98,7 +98,7 @@ def test_rr_march_outcomes_vs_reference_goldens(renderer, name):
 
 def test_outcome_sink_does_not_change_the_frame(renderer):
     """The sink is a branch in the production kernels: frames rendered with
-    and without it are byte-identical (unlit ray-pair, fused lit ray-pair,
+    and without it are byte-identical (unlit ray-pair, lit ray-pair,
     one-ray diffeo + mesh)."""
     for name, w, h in (("c3_bumps16_1080p", 320, 180), ("c3_bumps16_shadows_1080p", 320, 180),
                        ("c4_twist_mesh_1080p", 192, 108)):
@@ -146,12 +146,12 @@ def test_c3_1080p_full_frame_vs_reference(renderer, oracle_lib, reference_lib):
 
 
 def test_c3_lit_1080p_full_frame_vs_oracle(renderer, oracle_lib):
-    """The north-star frame: C3 + shadow geodesics to 2 point lights (fused
-    launch), every pixel, against the FP64 oracle extension."""
+    """The north-star frame: C3 + shadow geodesics to 2 point lights (hit-record
+    + shadow launches), every pixel, against the FP64 oracle extension."""
     cfg = _load("c3_bumps16_shadows_1080p")
     w, h = 1920, 1080
     rgb, out, st, kern = _gpu_frame(renderer, cfg, w, h)
-    assert kern == "march2_kernel<bumps16>" and st["kernel_launches"] - st["sort_kernels"] == 1
+    assert kern == "march2_kernel<bumps16>" and st["kernel_launches"] - st["sort_kernels"] == 2
     rep, cand, ref_st = _check_vs_oracle(oracle_lib, cfg, w, h, rgb, out)
     _log("c3_bumps16_shadows_1080p 1920x1080 full frame vs oracle", rep, cand, kern)
     assert rep.ok, f"{rep.summary()} candidates={cand}"

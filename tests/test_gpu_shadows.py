@@ -54,8 +54,7 @@ def test_shadow_frame_parity_vs_oracle(renderer, oracle_lib, name, integ, w, h):
     assert rep.ok, rep.summary()
     # ray-pair Gaussian-bump RK4 frames fuse the hit and shadow work into one
     # launch; the other kernels use a hit-record launch + a shadow launch
-    fused = cfg.integrator.scheme == "rk4" and renderer.last_kernel.startswith("march2_kernel")
-    assert st["kernel_launches"] - st["sort_kernels"] == (1 if fused else 2)
+    assert st["kernel_launches"] - st["sort_kernels"] == 2      # hit-record launch + shadow launch
     # shadow work is counted and close to the oracle's
     assert abs(st["shadow_steps"] - ref_st["shadow_steps"]) <= 0.02 * max(1, ref_st["shadow_steps"])
 
@@ -110,10 +109,11 @@ def test_larger_frame_parity_with_shadows(renderer, oracle_lib):
               {"position": [8.0, 2.0, 1.5], "intensity": 0.25}],  # visibility bytes
     [{"position": [4.0, 0.0, -3.0], "intensity": 0.9}],            # below the floor: all blocked
 ])
-def test_light_count_parity_fused_launch(renderer, oracle_lib, lights):
-    """The fused lit launch (one work item per (pixel unit, light), the unit's
-    last light to finish shades) against the oracle's shade_lit for 1, 5 and
-    an occluded light, plus byte-identity across repeated frames."""
+def test_light_count_parity_lit_launches(renderer, oracle_lib, lights):
+    """The lit ray-pair frame (a hit-record launch, then one work item per
+    (pixel unit, light), the unit's last light to finish shades) against the
+    oracle's shade_lit for 1, 5 and an occluded light, plus byte-identity
+    across repeated frames."""
     from oracle.parity import compare_rgb
     cfg = _cfg("c3_bumps16_shadows_1080p", lights=lights)
     w, h = 160, 90
@@ -123,7 +123,7 @@ def test_light_count_parity_fused_launch(renderer, oracle_lib, lights):
     rgb, st = renderer.render(cam, cfg.integrator, w, h)
     rep = compare_rgb(rgb, ref_rgb, flags)
     assert rep.ok, rep.summary()
-    assert st["kernel_launches"] - st["sort_kernels"] == 1 and renderer.last_kernel.startswith("march2_kernel")
+    assert st["kernel_launches"] - st["sort_kernels"] == 2 and renderer.last_kernel.startswith("march2_kernel")
     assert abs(st["shadow_steps"] - ref_st["shadow_steps"]) <= 0.02 * max(1, ref_st["shadow_steps"])
     for _ in range(2):
         again, _ = renderer.render(cam, cfg.integrator, w, h)
