@@ -60,7 +60,7 @@ def _load(args) -> cfgmod.RunConfig:
 
 
 def cmd_render(cfg: cfgmod.RunConfig, device: int = 0) -> int:
-    """rray_main.cpp:53-83 on the GPU (one fused launch per frame)."""
+    """rray_main.cpp:53-83 on the GPU (one launch per frame; lit frames two)."""
     from .render import Image, Renderer, write_ppm
     t0 = time.perf_counter()
     r = Renderer(device)

@@ -395,7 +395,8 @@ def pixel_direction(cam: Camera, px: int, py: int, width: int, height: int):
 
 def render(metric, scene: Scene, cam: Camera, integ: IntegratorConfig, width: int, height: int,
            opt: RenderOptions = RenderOptions()) -> RenderResult:
-    """render.cpp:43-111 on the GPU: raygen + march + shade fused in one launch."""
+    """render.cpp:43-111 on the GPU: raygen + march + shade fused in one launch (lit
+    frames: a hit-record launch + a shadow / shade launch)."""
     kind = opt.kernel if opt.kernel != KernelKind.Auto else kernel_from_env()
     if resolve_kernel(kind) != KernelKind.Cuda:
         from .errors import ValidationError
