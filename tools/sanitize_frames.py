@@ -14,9 +14,10 @@ the last-light shading must never read unpublished):
 
 whose frame digests must equal the default build's.
 
-Covers the fused lit ray-pair launch (ready flags, last-finisher shading,
+Covers the lit ray-pair launches (hit records, last-finisher shading,
 shared-memory staging), the unlit ray-pair frame with the outcome sink, the
-twist ray-pair kernel, the one-ray mesh kernel, tile shards and rr_march."""
+twist ray-pair kernel, the static chain fold with meshes, the one-ray mesh
+and Euclidean kernels (per-warp stat sums), tile shards and rr_march."""
 import os
 import sys
 
@@ -33,7 +34,8 @@ def main():
     r = Renderer(0)
     cases = [("c3_bumps16_shadows_1080p", 96, 54), ("c3_bumps16_1080p", 100, 60),
              ("c4_twist_1080p", 64, 36), ("c4_twist_mesh_1080p", 64, 36),
-             ("c3_bumps16_rk23_1080p", 64, 36), ("c2_flat_1080p", 64, 36)]
+             ("c3_bumps16_rk23_1080p", 64, 36), ("c2_flat_1080p", 64, 36),
+             ("c4_twist_bend_mesh_1080p", 64, 36), ("c1_gauss1_512", 64, 64)]
     if "--full" in sys.argv:   # the benchmarked frames at full size (lit, unlit, C4 + mesh, 4K)
         cases += [("c3_bumps16_shadows_1080p", 1920, 1080), ("c3_bumps16_1080p", 1920, 1080),
                   ("c4_twist_mesh_1080p", 1920, 1080), ("c5_bumps16_4k", 3840, 2160)]
