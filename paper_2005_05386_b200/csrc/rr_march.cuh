@@ -54,10 +54,11 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #endif
 #ifndef RR_X2_SCALAR_CONSTS_LIT
 // bump constants as scalars (DevBumpS: UR.F32 broadcast operands, 5 instead of
-// 10 LDCU.64 per bump) in the lit launch's primary and shadow marches and in
-// rk23; the unlit RK4 frame keeps the broadcast pairs (DevBumpB), measured
-// 0.3% faster there (profiles/r2z_scalar_consts_ab.log)
-#define RR_X2_SCALAR_CONSTS_LIT 1
+// 10 LDCU.64 per bump) in rk23 (and, with 1 here, in the lit marches: they won
+// inside the single fused lit launch, 15.55 -> 15.47 ms, but the two separate
+// lit launches run 0.25% faster on the broadcast pairs (DevBumpB) that the
+// unlit frames use: profiles/r2z_scalar_consts_ab.log, r2z_litvec_ab.log)
+#define RR_X2_SCALAR_CONSTS_LIT 0
 #endif
 #ifndef RR_X2_SCALAR_CONSTS_RK23
 #define RR_X2_SCALAR_CONSTS_RK23 1
