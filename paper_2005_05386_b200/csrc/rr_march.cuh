@@ -125,12 +125,13 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_X2_RK4_UNROLL_SHADOW RR_X2_RK4_UNROLL_LIT
 #endif
 #ifndef RR_MIN_BLOCKS_X2
-// ray-pair kernel occupancy (CUDA-event A/B): with the bit-loop bump block
-// and unrolled RK4 stages, 6 CTAs (80 registers, 132 B of spills) beat 7
-// (72 registers, 208 B of spills in the per-step code) on the unlit frame,
-// 9.39 vs 9.63 ms; the fused lit launch keeps 7 (16.16 vs 16.35 ms)
-// (profiles/r1i_shadow_frame.md).  The 4-slot variant (C1) uses 6.
-#define RR_MIN_BLOCKS_X2 6
+// ray-pair kernel occupancy (CUDA-event A/B).  Round 1: 6 CTAs (80
+// registers) beat 7 on the unlit frame, 9.39 vs 9.63 ms
+// (profiles/r1i_shadow_frame.md).  Final round-2 build: 7 (72 registers) ties
+// 6 on C3 (9.16 vs 9.15 ms median, 9.09-9.11 vs 9.13-9.15 min) and wins on
+// C5 4K (34.98 vs 35.27 ms); the lit hit-record launch keeps 6
+// (profiles/r2z_c3occ_ab.log).  The 4-slot variant (C1) uses its own.
+#define RR_MIN_BLOCKS_X2 7
 #endif
 #ifndef RR_MIN_BLOCKS_X2_FUSED
 #define RR_MIN_BLOCKS_X2_FUSED 7
@@ -161,7 +162,7 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_MIN_BLOCKS_X2_SHADOW 7   // the shadow launch of lit frames (72 registers): 15.33 vs 15.37 ms at 6
 #endif
 #ifndef RR_MIN_BLOCKS_X2_HITS
-#define RR_MIN_BLOCKS_X2_HITS RR_MIN_BLOCKS_X2     // the hit-record launch of unfused lit frames
+#define RR_MIN_BLOCKS_X2_HITS 6     // the hit-record launch of lit frames (80 registers)
 #endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
 // ray-pair rk23 (FSAL stage + error terms per ray pair): 6 CTAs/SM (80
