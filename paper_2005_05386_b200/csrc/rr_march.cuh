@@ -140,7 +140,10 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_MIN_BLOCKS_X2_SMALL 6
 #endif
 #ifndef RR_MIN_BLOCKS_X2_TWIST
-#define RR_MIN_BLOCKS_X2_TWIST 6        // ray-pair single-twist frames (C4 without meshes)
+// ray-pair single-twist frames (C4 without meshes): 7 CTAs/SM (72 registers)
+// since the bounds budget: 6.24-6.26 vs 6.47-6.50 ms at 6, 7.12 at 8, 7.22 at
+// 5 (profiles/r2z_occ_small_twist_ab.log)
+#define RR_MIN_BLOCKS_X2_TWIST 7
 #endif
 #ifndef RR_MIN_BLOCKS_X2_TWIST_MESH
 #define RR_MIN_BLOCKS_X2_TWIST_MESH 6   // ray-pair single-twist frames with meshes (C4)
