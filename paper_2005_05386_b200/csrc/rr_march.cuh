@@ -168,10 +168,11 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 #define RR_MIN_BLOCKS_X2_HITS 6     // the hit-record launch of lit frames (80 registers)
 #endif
 #ifndef RR_MIN_BLOCKS_X2_RK23
-// ray-pair rk23 (FSAL stage + error terms per ray pair): 6 CTAs/SM (80
-// registers) since the pre-loop k1 and scalar constants shrank it: 10.43 vs
-// 10.48 ms at 5, 12.97 at 4 (profiles/r2z_occ_recheck_ab.log)
-#define RR_MIN_BLOCKS_X2_RK23 6
+// ray-pair rk23 (FSAL stage + error terms per ray pair): 7 CTAs/SM (72
+// registers) since the pre-loop k1 and scalar constants shrank it: 10.43 /
+// 10.48 / 12.97 ms at 6 / 5 / 4 (profiles/r2z_occ_recheck_ab.log), 10.40-10.42
+// vs 10.45 at 7 vs 6 (r2z_rk23occ7_ab.log)
+#define RR_MIN_BLOCKS_X2_RK23 7
 #endif
 #ifndef RR_MIN_BLOCKS_RK23
 #define RR_MIN_BLOCKS_RK23 5   // rk23 carries the FSAL stage + error terms: <= 96 registers
