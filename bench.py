@@ -619,8 +619,10 @@ def run_b200(args, cfg):
         # centres move, cli.animated_config), so each frame pays the scene
         # upload and the device culling-grid rebuild before its render.
         # Wall clock per frame (host upload work included), device-synchronised.
-        from paper_2005_05386_b200.cli import animated_config
+        from paper_2005_05386_b200.cli import ANIMATION_CULL_GRID, animated_config
         acfg = load_config(os.path.join(ROOT, "configs", "c5_bumps16_4k.json"))
+        grid0 = r.options()["cull_grid"]
+        r.set_options(cull_grid=ANIMATION_CULL_GRID)    # as `animate` does: the grid is rebuilt per frame
         aw, ah = acfg.output.width, acfg.output.height
         abuf = torch.empty((ah, aw, 3), dtype=torch.uint8, device="cuda")
         r.set_config(acfg)
@@ -636,11 +638,13 @@ def run_b200(args, cfg):
             asteps += ast["total_steps"]
         torch.cuda.synchronize()
         ams = (time.perf_counter() - t0) * 1e3 / len(frames)
+        r.set_options(cull_grid=grid0)
         extras["c5_anim_4k"] = {"size": f"{aw}x{ah}", "frames": len(frames),
                                 "ms_per_frame": ams, "fps": 1e3 / ams,
                                 "steps_per_s": asteps / (ams * 1e-3 * len(frames)),
                                 "timing": "wall clock per frame: scene upload + device culling-grid "
                                           "rebuild + render (the render's stats D2H syncs each frame)",
+                                "cull_grid": ANIMATION_CULL_GRID,
                                 "kernel": r.last_kernel}
         del abuf
         r.set_config(cfg)

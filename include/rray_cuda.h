@@ -232,7 +232,7 @@ typedef struct rr_options {
     int32_t cull;                     /* per-warp bump culling on a voxel grid: 0 off, 1 (default)
                                          radius cull_radius_sigma for every bump, 2 equal-error
                                          radii <= cull_radius_sigma (see ensure_masks) */
-    int32_t cull_grid;                /* voxels per axis of the culling grid (default 192) */
+    int32_t cull_grid;                /* voxels per axis of the culling grid (default 256) */
     double cull_radius_sigma;         /* bump support radius in sigmas (default 5.5) */
     int32_t block_x, block_y;         /* frame tile ordering the warp units (default 32 x 32) */
     int32_t persistent;               /* 1: persistent CTAs pulling warp units (default 1) */

@@ -138,6 +138,9 @@ def cmd_geodesic(cfg: cfgmod.RunConfig, start, direction, out_path: str, device:
     return 0
 
 
+ANIMATION_CULL_GRID = 192   # culling-grid resolution for per-frame scene changes
+
+
 def animated_config(cfg: cfgmod.RunConfig, frame: int, fps: float, omega: float,
                     amp: float) -> cfgmod.RunConfig:
     """Frame `frame` of the BASELINE configs[4] bump animation (static scene)."""
@@ -167,6 +170,10 @@ def cmd_animate(cfg: cfgmod.RunConfig, frames: int, fps: float, omega: float, am
                 pattern: str | None, device: int = 0) -> int:
     from .render import Image, Renderer, write_ppm
     r = Renderer(device)
+    # every frame is a new scene, so the culling grid is rebuilt per frame:
+    # 192^3 rebuilds in ~0.1 ms, the static-frame default 256^3 in ~1.9 ms
+    # (profiles/r2z_grid_ab.log)
+    r.set_options(cull_grid=ANIMATION_CULL_GRID)
     cam = None
     w, h = cfg.output.width, cfg.output.height
     t0 = time.perf_counter()

@@ -60,8 +60,9 @@ struct Options {
     Options() {
         std::memset(&o, 0, sizeof o);
         o.cull = 1;                  // uniform radius (equal-error radii: cull = 2, measured worse per unit of error)
-        o.cull_grid = 192;           // 28 MB mask table (L2-resident): C3 9.22 -> 9.13 ms, C5 35.6 -> 35.2 ms vs
-                                     // 128; the per-scene rebuild costs ~0.9 ms more (C5 animation +0.6 ms/frame)
+        o.cull_grid = 256;           // 67 MB mask table: on the final kernels C3 9.13 -> 9.10 ms, C5 34.98 ->
+                                     // 34.76, lit 15.46 -> 15.37 vs 192; rk23 and C1 equal; 160 is slower
+                                     // (profiles/r2z_grid_ab.log)
         o.cull_radius_sigma = 5.5;   // near parity-neutral (profiles/r1i_cull_sweep_960.log)
         o.block_x = 32;
         o.block_y = 32;
@@ -466,7 +467,7 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
         double* r = &g[8 * (size_t)n++];
         for (int k = 0; k < 3; ++k) {
             r[k] = q.c[k];
-            r[3 + k] = q.s[k];
+            r[3 + k] = 1.0 / q.s[k];   // the build multiplies by 1/sigma
         }
         r[6] = c->slots[j];
         double Rj = R;

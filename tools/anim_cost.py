@@ -17,6 +17,8 @@ def main():
     cfg = load_config(os.path.join(ROOT, "configs", "c5_bumps16_4k.json"))
     w, h = cfg.output.width, cfg.output.height
     r = Renderer(0)
+    if "--grid" in sys.argv:
+        r.set_options(cull_grid=int(sys.argv[sys.argv.index("--grid") + 1]))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     rgb = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
@@ -41,7 +43,8 @@ def main():
 
     static = timed([cfg] * 10)
     anim = timed([animated_config(cfg, k, 30.0, 2.0, 0.3) for k in range(10)])
-    print(f"c5 4K static {static:.3f} ms  animated {anim:.3f} ms  rebuild {anim - static:.3f} ms")
+    print(f"c5 4K grid {r.options().get('cull_grid')}: static {static:.3f} ms  animated {anim:.3f} ms  "
+          f"rebuild {anim - static:.3f} ms")
     r.close()
 
 
