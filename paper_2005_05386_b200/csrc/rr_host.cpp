@@ -55,6 +55,10 @@ struct Compiled {
     std::vector<HostStage> stages; // diffeo chain, innermost first
 };
 
+#ifndef RR_MAX_CULL_GRID
+#define RR_MAX_CULL_GRID 256
+#endif
+
 struct Options {
     rr_options o;
     Options() {
@@ -423,7 +427,7 @@ int ensure_masks(rr_ctx* c, double h, cudaStream_t s, int levels = 1) {
         if (P.kind == rr::kBumps) P.skip = 0;   // no culling grid: no empty cells known
         return RR_OK;
     }
-    const int G = std::max(2, std::min(c->opt.o.cull_grid, 256));
+    const int G = std::max(2, std::min(c->opt.o.cull_grid, RR_MAX_CULL_GRID));
     const double R = c->opt.o.cull_radius_sigma > 0 ? c->opt.o.cull_radius_sigma : 5.5;
     const double dil = 1.5 * h;
     if (c->d_masks && c->masks_grid == G && c->masks_radius == R && c->masks_mode == c->opt.o.cull &&
@@ -973,8 +977,8 @@ const char* rr_last_error(const rr_ctx* c) { return c ? c->err.c_str() : g_creat
 int rr_set_options(rr_ctx* c, const rr_options* opt) {
     if (!c || !opt) return RR_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(c->mu);
-    if (opt->cull_grid < 0 || opt->cull_grid > 256)
-        return set_err(c, RR_ERR_CONFIG, "options.cull_grid: must be in [0, 256]");
+    if (opt->cull_grid < 0 || opt->cull_grid > RR_MAX_CULL_GRID)
+        return set_err(c, RR_ERR_CONFIG, "options.cull_grid: must be in [0, " + std::to_string(RR_MAX_CULL_GRID) + "]");
     if (opt->cull < 0 || opt->cull > 2)
         return set_err(c, RR_ERR_CONFIG, "options.cull: must be 0, 1 or 2");
     c->opt.o = *opt;
