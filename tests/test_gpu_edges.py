@@ -78,7 +78,7 @@ def test_extreme_integrator_settings(renderer, oracle_lib, integ):
 
 
 @pytest.mark.parametrize("opts", [{"cull": 0}, {"cull_grid": 16}, {"cull_grid": 128},
-                                  {"cull_radius_sigma": 8.0}, {"skip": 0}])
+                                  {"cull_grid": 192}, {"cull_radius_sigma": 8.0}, {"skip": 0}])
 def test_culling_options_keep_parity(renderer, oracle_lib, opts):
     cfg = cfg_of("c3_bumps16_1080p")
     check(renderer, oracle_lib, cfg, 96, 54, opts)
@@ -120,3 +120,15 @@ def test_pinned_host_output_is_written_by_the_kernel():
     _, _ = r.render(cam, cfg.integrator, w, h, out=pinned)
     assert np.array_equal(pinned.numpy(), lit)
     r.close()
+
+
+def test_option_validation(renderer):
+    """Out-of-range options fail with a config error and leave the context's
+    options unchanged (the culling grid is capped at 256^3)."""
+    from paper_2005_05386_b200.errors import Error
+    before = renderer.options()
+    assert before["cull_grid"] == 256                     # the static-frame default
+    for bad in ({"cull_grid": 257}, {"cull_grid": -1}, {"cull": 3}):
+        with pytest.raises(Error):
+            renderer.set_options(**bad)
+        assert renderer.options() == before

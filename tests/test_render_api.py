@@ -62,3 +62,10 @@ def test_ppm_errors(tmp_path):
         R.read_ppm(str(short))
     with pytest.raises(IoError):
         R.write_ppm(R.Image(1, 1, np.zeros((1, 1, 3), np.uint8)), str(tmp_path / "no" / "dir.ppm"))
+
+
+def test_animation_driver_grid():
+    """`animate` rebuilds the culling grid every frame and selects the grid
+    that rebuilds fast (192^3) instead of the static default (256^3)."""
+    from paper_2005_05386_b200 import cli
+    assert cli.ANIMATION_CULL_GRID == 192
