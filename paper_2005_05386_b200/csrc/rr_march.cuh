@@ -77,6 +77,9 @@ constexpr int kThreads = 128;   // 4 warps per CTA
 // to the box
 #define RR_BOUNDS_BUDGET 1
 #endif
+#ifndef RR_SMALL_LAUNCH_CTAS
+#define RR_SMALL_LAUNCH_CTAS 1   // ray-pair launches with few items per SM use fewer CTAs per SM
+#endif
 #ifndef RR_CHAIN_STATIC
 // 1: two-stage twist/bend chains use a fold specialised at compile time
 // (rr_k_pair_chain.cu); others (and 0) the run-time stage loop
@@ -3328,7 +3331,24 @@ int occupancy_of2() {
 template <int KIND, int NB, int PASS, bool MESH>
 cudaError_t launch_pass2(const DevParams& P, const DevLaunch& L, cudaStream_t s, int num_sms) {
     const unsigned warps_needed = (L.n_units + 1) / 2;
-    unsigned blocks = (unsigned)(num_sms * occupancy_of2<KIND, NB, PASS, MESH>());
+    const int occ = occupancy_of2<KIND, NB, PASS, MESH>();
+    unsigned blocks = (unsigned)(num_sms * occ);
+#if RR_SMALL_LAUNCH_CTAS
+    // Launches with few work items per SM (a 1080p frame split over 4 or 8
+    // GPUs) end on their slowest units, which run faster with fewer
+    // co-resident warps: 2 + items/18 CTAs per SM below the full occupancy
+    // (C3 shards at N = 8: 1.96 -> 1.55 ms, N = 4: 2.81 -> 2.57 ms; full
+    // frames keep the full grid: profiles/r2z_small_launch_ab.log)
+    {
+        const double items = (double)warps_needed * (PASS == kPassShadow ? (double)P.n_lights : 1.0);
+        const double per_sm = items / num_sms;
+        if (per_sm < 18.0 * (occ - 2)) {
+            const int want = (int)lround(2.0 + per_sm / 18.0);
+            const int ctas = want < 2 ? 2 : (want > occ ? occ : want);
+            blocks = (unsigned)(num_sms * ctas);
+        }
+    }
+#endif
     const unsigned max_useful = (warps_needed + 3) / 4;
     if (blocks > max_useful) blocks = max_useful;
     if (blocks == 0) blocks = 1;
